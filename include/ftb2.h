@@ -1,0 +1,146 @@
+/*
+ * ftb2 — C ABI of the B200 (sm_100a) streaming hot path.
+ *
+ * Plain pointers and sizes only: every buffer is a DEVICE pointer owned by the
+ * caller (PyTorch caching allocator in the Python host); kernels never
+ * allocate. `stream` is a cudaStream_t passed as void*. All entry points only
+ * enqueue work (no implicit synchronisation) and are CUDA-graph capturable.
+ * Return 0 on success or one of the FTB_E* codes; ftb_last_error() returns a
+ * thread-local message. The Python host maps FTB_EINVAL -> ConfigError and
+ * FTB_ENONFINITE -> NumericError (reference errors.py:4-18).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/ftlk):
+ *   ftb_gemm_bf16 ........ backends/reference.py:17-18 dense_forward (x @ w + b), plus the
+ *                          fused epilogues of net.py:230-274 (bias, GELU :266, residual
+ *                          adds :256/:261/:268, embedding sum :232) and wan-mode AdaLN gates
+ *   ftb_norm_modulate .... backends/reference.py:41-46 layernorm_forward (+ AdaLN modulation)
+ *   ftb_attention ........ backends/reference.py:77-92 mha_forward core (softmax(QK^T/sqrt(hd))V),
+ *                          self (net.py:254) and cross (net.py:259) attention
+ *   ftb_gelu_bf16 ........ backends/reference.py:28-31 gelu_forward (standalone form)
+ *   ftb_patchify_composite diffusion.py:133-135,150-179 composite assembly (Eq.1 channel stack)
+ *   ftb_unpatch_ddim ..... diffusion.py:229-236 x0 slice + DDIM update; streaming.py:298-299 tail
+ *   ftb_codec_decode ..... world.py:206-210 Codec.decode (latents @ Q)
+ *   ftb_vae_* ............ wan-mode causal VAE decoder (build-defined)
+ */
+#ifndef FTB2_H
+#define FTB2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FTB_OK 0
+#define FTB_EINVAL 1
+#define FTB_ECUDA 2
+#define FTB_ENCCL 3
+#define FTB_ENONFINITE 4
+
+int ftb_version(void);
+const char* ftb_last_error(void);
+int ftb_device_sm_count(int device);
+
+/* ---------------------------------------------------------------- GEMM */
+enum {
+  FTB_EPI_BF16 = 0,       /* out_bf16 = acc + bias                                  */
+  FTB_EPI_GELU_BF16 = 1,  /* out_bf16 = gelu_tanh(acc + bias)                       */
+  FTB_EPI_F32 = 2,        /* out_f32  = acc + bias                                  */
+  FTB_EPI_RESID_F32 = 3,  /* out_f32 += gate[g] * (acc + bias)   (gate NULL -> 1)   */
+  FTB_EPI_ROWADD_F32 = 4, /* out_f32  = acc + bias + vec[g]                         */
+  FTB_EPI_QKV_ROPE = 5    /* bf16 q|k|v with 3D RoPE on q,k; Ulysses send layout    */
+};
+
+/* 3D rotary tables (wan mode). Pair p of a head: p < pairs_t -> frame axis,
+ * p < pairs_t+pairs_h -> row axis, else column axis. cos/sin are float32
+ * [positions][pairs_axis] row-major, computed on the host in float64. */
+typedef struct ftb_rope3d {
+  const float* cos_t; const float* sin_t;
+  const float* cos_h; const float* sin_h;
+  const float* cos_w; const float* sin_w;
+  int32_t pairs_t, pairs_h, pairs_w;
+  int32_t grid_h, grid_w; /* token grid of one latent frame */
+} ftb_rope3d;
+
+typedef struct ftb_epilogue {
+  int32_t kind;
+  int32_t rows_per_group;  /* g(row) = (row + row_offset) / rows_per_group */
+  int64_t row_offset;
+  const float* bias;       /* [N] or NULL */
+  const float* group_vec;  /* [G][group_ld] gate / additive vector or NULL */
+  int64_t group_ld;
+  void* out;               /* bf16 or f32, [M][ldc] */
+  int64_t ldc;
+  /* FTB_EPI_QKV_ROPE only: column c of [0,3*heads*head_dim) -> (which, head, d);
+   * stored at ((dest*M + row)*3 + which)*hpr*hd + (head%hpr)*hd + d, dest = head/hpr. */
+  int32_t heads, head_dim, heads_per_rank;
+  const ftb_rope3d* rope;  /* NULL: no rotation */
+} ftb_epilogue;
+
+/* C[M,N] = A[M,K] . B[N,K]^T (bf16 in, fp32 accumulate, tcgen05 + TMEM, TMA-fed).
+ * A is read as a_chunks K-slices of width K/a_chunks: element (r,k) at
+ * A + (k / kc) * a_chunk_stride + r * lda + (k % kc) (Ulysses gather; a_chunks=1 plain).
+ * Requirements: lda, ldb multiples of 8 elements; K/a_chunks multiple of 64 when a_chunks>1. */
+int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_stride,
+                  const void* B, int64_t ldb, int32_t M, int32_t N, int32_t K,
+                  const ftb_epilogue* epi, void* stream);
+
+/* ---------------------------------------------------------------- norms */
+/* y = ((x - mean) * rstd) * (gamma?gamma:1) * (scale?1+scale[g]:1) + (beta?beta:0) + (shift?shift[g]:0)
+ * rstd = 1/sqrt(var + eps), population variance; g = (row+row_offset)/rows_per_group.
+ * Writes bf16 y [M][ldy]; optional f32 mean/rstd [M]. */
+int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t N,
+                      const float* gamma, const float* beta,
+                      const float* scale, const float* shift, int64_t mod_ld,
+                      int32_t rows_per_group, int64_t row_offset, float eps,
+                      void* y, int64_t ldy, float* mean_out, float* rstd_out, void* stream);
+
+/* ---------------------------------------------------------------- attention */
+/* o[r, h*hd + d] = softmax_j(q_r . k_j * scale) v_j  per head h (bidirectional, no mask
+ * beyond Lk). Row r of q at q + r*ldq + h*head_dim (bf16); same for k, v, o. */
+int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                  void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
+                  float scale, void* stream);
+/* Explicit kernel selection (tests / benchmarks): 0 = tcgen05 flash kernel
+ * (head_dim 64|128), 1 = short-KV CUDA-core kernel (Lk <= 1024). */
+int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk,
+                       const void* v, int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk,
+                       int32_t heads, int32_t head_dim, float scale, void* stream);
+
+/* ---------------------------------------------------------------- elementwise */
+int ftb_gelu_bf16(const void* x, void* y, int64_t n, void* stream);
+int ftb_silu_f32_to_bf16(const float* x, void* y, int64_t n, void* stream);
+int ftb_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
+int ftb_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream);
+
+/* Eq.1 composite -> patch tokens. motion [Lm][D][H][W], z [Lc-Lm][D][H][W],
+ * reference [D][H][W] (f32). Token (f, y, x) = f*(H/ph)*(W/pw) + y*(W/pw) + x, feature
+ * (c*ph + py)*pw + px over channels c in [z_noise(D) | z_mask(1) | z_cond(D)].
+ * out bf16 [Lc*T][ldo], columns [in_features, ldo) zero-filled. */
+int ftb_patchify_composite(const float* motion, const float* z, const float* reference,
+                           int32_t Lm, int32_t Lc, int32_t D, int32_t H, int32_t W,
+                           int32_t ph, int32_t pw, void* out, int64_t ldo, void* stream);
+
+/* x0 tokens f32 [Lc*T][ldx] (feature (c*ph+py)*pw+px) -> target frames.
+ * x0_out [Lc-Lm][D][H][W] = x0 of frames >= Lm; if update:
+ * z = a_n*x0 + s_n*(z - a_i*x0)/s_i (DDIM, diffusion.py:233-236). */
+int ftb_unpatch_ddim(const float* x0_tok, int64_t ldx, int32_t Lm, int32_t Lc, int32_t D,
+                     int32_t H, int32_t W, int32_t ph, int32_t pw, float* z, float* x0_out,
+                     float a_i, float s_i, float a_n, float s_n, int32_t update, void* stream);
+
+/* frames[n][D] = latents[n][D] @ Q[D][D]   (f32; orthogonal codec) */
+int ftb_codec_decode(const float* latents, const float* Q, float* frames, int32_t n, int32_t D,
+                     void* stream);
+
+/* Counter-based N(0,1)*scale fill (synthetic random-init weights at 14B shape). */
+int ftb_fill_normal_bf16(void* out, int64_t n, uint64_t seed, float scale, void* stream);
+int ftb_fill_normal_f32(float* out, int64_t n, uint64_t seed, float scale, void* stream);
+
+/* Reduce: out[0] = count of non-finite values in x (f32), for NumericError checks. */
+int ftb_count_nonfinite(const float* x, int64_t n, int32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

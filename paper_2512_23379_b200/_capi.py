@@ -1,0 +1,98 @@
+"""ctypes binding of the C-ABI library `_lib/libftb2.so` (include/ftb2.h).
+
+The library is REQUIRED: there is no CPU or eager-PyTorch fallback. Importing
+this module on a machine without the built library raises ImportError; any
+entry point returning a non-zero code raises (FTB_EINVAL -> ConfigError,
+FTB_ENONFINITE -> NumericError, otherwise DeviceError). ctypes releases the
+GIL for the duration of each call.
+"""
+
+import ctypes as C
+import os
+
+from .errors import ConfigError, DeviceError, NumericError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libftb2.so")
+
+FTB_OK, FTB_EINVAL, FTB_ECUDA, FTB_ENCCL, FTB_ENONFINITE = 0, 1, 2, 3, 4
+EPI_BF16, EPI_GELU_BF16, EPI_F32, EPI_RESID_F32, EPI_ROWADD_F32, EPI_QKV_ROPE = range(6)
+
+vp, i32, i64, f32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint64
+
+
+class Rope3D(C.Structure):
+    _fields_ = [("cos_t", vp), ("sin_t", vp), ("cos_h", vp), ("sin_h", vp), ("cos_w", vp), ("sin_w", vp),
+                ("pairs_t", i32), ("pairs_h", i32), ("pairs_w", i32), ("grid_h", i32), ("grid_w", i32)]
+
+
+class Epilogue(C.Structure):
+    _fields_ = [("kind", i32), ("rows_per_group", i32), ("row_offset", i64), ("bias", vp),
+                ("group_vec", vp), ("group_ld", i64), ("out", vp), ("ldc", i64),
+                ("heads", i32), ("head_dim", i32), ("heads_per_rank", i32), ("rope", C.POINTER(Rope3D))]
+
+
+_SIGS = {
+    "ftb_version": ([], i32),
+    "ftb_last_error": ([], C.c_char_p),
+    "ftb_device_sm_count": ([i32], i32),
+    "ftb_gemm_bf16": ([vp, i64, i32, i64, vp, i64, i32, i32, i32, C.POINTER(Epilogue), vp], i32),
+    "ftb_norm_modulate": ([vp, i64, i32, i32, vp, vp, vp, vp, i64, i32, i64, f32, vp, i64, vp, vp, vp], i32),
+    "ftb_attention": ([vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),
+    "ftb_attention_impl": ([i32, vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),
+    "ftb_gelu_bf16": ([vp, vp, i64, vp], i32),
+    "ftb_silu_f32_to_bf16": ([vp, vp, i64, vp], i32),
+    "ftb_cast_f32_bf16": ([vp, vp, i64, vp], i32),
+    "ftb_cast_bf16_f32": ([vp, vp, i64, vp], i32),
+    "ftb_patchify_composite": ([vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, i64, vp], i32),
+    "ftb_unpatch_ddim": ([vp, i64, i32, i32, i32, i32, i32, i32, i32, vp, vp, f32, f32, f32, f32, i32, vp], i32),
+    "ftb_codec_decode": ([vp, vp, vp, i32, i32, vp], i32),
+    "ftb_fill_normal_bf16": ([vp, i64, u64, f32, vp], i32),
+    "ftb_fill_normal_f32": ([vp, i64, u64, f32, vp], i32),
+    "ftb_count_nonfinite": ([vp, i64, vp, vp], i32),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libftb2.so not built (run `python -m paper_2512_23379_b200.build` or "
+                          "__graft_entry__.build()); there is no fallback path")
+    lib = C.CDLL(LIB_PATH)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def check(rc, what=""):
+    if rc == FTB_OK:
+        return
+    msg = (lib.ftb_last_error() or b"").decode(errors="replace")
+    if what:
+        msg = "%s: %s" % (what, msg)
+    if rc == FTB_EINVAL:
+        raise ConfigError(msg)
+    if rc == FTB_ENONFINITE:
+        raise NumericError(msg)
+    raise DeviceError(msg)
+
+
+def call(name, *args):
+    check(getattr(lib, name)(*args), name)
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,409 @@
+// Attention kernels: softmax(Q K^T * scale) V per head, bidirectional (no mask
+// beyond the key length). Restates the reference's mha_forward core
+// (backends/reference.py:77-92; Cython row loop _fast.pyx:162-209).
+//
+//  (0) fmha_tc_kernel  — tcgen05 flash attention for long sequences, head_dim 64|128.
+//      One CTA = one head x 128 query rows. Warp roles:
+//        w0 TMA producer (Q once, K/V 128-key blocks, 2-stage ring)
+//        w1 MMA issuer: S_j = Q K_j^T -> TMEM (double-buffered, S_{j+1} overlaps
+//           softmax_j), O += P_j V_j -> TMEM (V consumed MN-major)
+//        w2 TMEM allocator
+//        w4-7 softmax: one thread per query row, tcgen05.ld of S, exp2 online
+//           softmax with lazy (threshold 2^8) rescaling of O in TMEM, P -> smem bf16
+//           (128B-swizzled K-major, the A operand of the PV MMA), final O / l.
+//  (1) attn_small_kernel — CUDA-core online-softmax kernel for short key sets
+//      (cross-attention over conditioning tokens, ftlk-mode 9-token chunks).
+#include <math.h>
+
+#include "common.cuh"
+#include "ftb_internal.h"
+
+namespace ftb {
+
+struct AttnParams {
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  __nv_bfloat16* o;
+  long long ldq, ldk, ldv, ldo;
+  int Lq, Lk, heads, hd;
+  float scale_log2;  // scale * log2(e)
+};
+
+// ============================================================ tcgen05 flash kernel
+template <int HD>
+struct FmhaCfg {
+  static constexpr int BQ = 128, BKV = 128;
+  static constexpr int BOX = 128 * 64 * 2;              // one 128-row x 64-col bf16 box (16 KB)
+  static constexpr int NBOX = HD / 64;
+  static constexpr int Q_BYTES = NBOX * BOX;
+  static constexpr int KV_BYTES = NBOX * BOX;           // 128 keys x HD
+  static constexpr int P_BYTES = 2 * BOX;               // 128 rows x 128 keys
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;
+  static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int TMEM_COLS = 512;                 // S0 | S1 | O
+  static constexpr int TM_O = 256;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+    fmha_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using C = FmhaCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* v_full = bars + 3;    // [2]
+  uint64_t* kv_empty = bars + 5;  // [2]
+  uint64_t* s_full = bars + 7;    // [2]
+  uint64_t* s_empty = bars + 9;   // [2]
+  uint64_t* p_full = bars + 11;
+  uint64_t* o_done = bars + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int qblk = blockIdx.x, head = blockIdx.y;
+  const int n_kv = (p.Lk + C::BKV - 1) / C::BKV;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], 4);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int col0 = head * HD;
+      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+      for (int b = 0; b < C::NBOX; ++b) tma_load_2d(smem + C::OFF_Q + b * C::BOX, &tmQ, q_full, col0 + 64 * b, qblk * C::BQ);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
+        for (int b = 0; b < C::NBOX; ++b)
+          tma_load_2d(smem + C::OFF_K + st * C::KV_BYTES + b * C::BOX, &tmK, &k_full[st], col0 + 64 * b, j * C::BKV);
+        mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
+        for (int b = 0; b < C::NBOX; ++b)
+          tma_load_2d(smem + C::OFF_V + st * C::KV_BYTES + b * C::BOX, &tmV, &v_full[st], col0 + 64 * b, j * C::BKV);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);  // B = V, MN-major
+      const uint32_t sq = smem_u32(smem + C::OFF_Q);
+      const uint32_t sp = smem_u32(smem + C::OFF_P);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        const uint32_t sk = smem_u32(smem + C::OFF_K + st * C::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::BOX + (kk & 3) * 32;
+          mma_bf16_ss(tmem + st * 128, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024), idesc_s,
+                      kk > 0);
+        }
+        mma_commit(&s_full[st]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) {
+          const int st = (j + 1) & 1;
+          mbar_wait(&k_full[st], ((j + 1) >> 1) & 1);
+          if (j + 1 >= 2) mbar_wait(&s_empty[st], (((j + 1) >> 1) - 1) & 1);
+          tc_fence_after();
+          issue_s(j + 1);
+        }
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + C::OFF_V + (j & 1) * C::KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk) {
+          const uint64_t ad = sdesc_sw128(sp + (kk >> 2) * C::BOX + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(sv + kk * 16 * 128, C::BOX, 1024);
+          mma_bf16_ss(tmem + C::TM_O, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(o_done);
+        mma_commit(&kv_empty[j & 1]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int row = qw * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qw * 32) << 16;
+    uint8_t* prow = smem + C::OFF_P + row * 128;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[128];
+      tmem_ld32(tmem + lane_off + st * 128 + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
+      tmem_ld32(tmem + lane_off + st * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+      tmem_ld32(tmem + lane_off + st * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
+      tmem_ld32(tmem + lane_off + st * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[st]);
+      const int valid = p.Lk - j * 128;  // keys [valid, 128) are padding
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        float s = __uint_as_float(sr[c]) * p.scale_log2;
+        s = (c < valid) ? s : -INFINITY;
+        sr[c] = __float_as_uint(s);
+        mx = fmaxf(mx, s);
+      }
+      float m_use = m_ref;
+      bool rescale = false;
+      if (j == 0) {
+        m_use = mx;
+      } else if (mx > m_ref + 8.f) {
+        m_use = mx;
+        rescale = true;
+      }
+      float rs = 0.f;
+      if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: P buffer free, O stable
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {  // 16 chunks of 8 keys (16 B)
+        float e[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          e[t] = ex2(__uint_as_float(sr[ch * 8 + t]) - m_use);
+          rs += e[t];
+        }
+        uint4 w;
+        w.x = pack_bf16(e[0], e[1]);
+        w.y = pack_bf16(e[2], e[3]);
+        w.z = pack_bf16(e[4], e[5]);
+        w.w = pack_bf16(e[6], e[7]);
+        const int atom = ch >> 3, c16 = ch & 7;
+        *reinterpret_cast<uint4*>(prow + atom * C::BOX + ((c16 ^ (row & 7)) << 4)) = w;
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+        const float f = rescale ? ex2(m_ref - m_use) : 1.f;
+        l *= f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_off + C::TM_O + c0, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * f);
+          tmem_st32(tmem + lane_off + C::TM_O + c0, o);
+        }
+        tmem_st_wait();
+      }
+      l += rs;
+      m_ref = m_use;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    mbar_wait(o_done, (n_kv - 1) & 1);
+    tc_fence_after();
+    const int grow = qblk * 128 + row;
+    const float inv = 1.f / l;
+#pragma unroll 1
+    for (int c0 = 0; c0 < HD; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lane_off + C::TM_O + c0, o);
+      tmem_ld_wait();
+      if (grow < p.Lq) {
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (long long)grow * p.ldo + head * HD + c0);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(o[8 * qq + 0]) * inv, __uint_as_float(o[8 * qq + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv);
+          dst[qq] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+// ============================================================ short-KV CUDA-core kernel
+// grid (ceil(Lq/16), heads), 128 threads: warp w owns query rows 4w..4w+3 of the block.
+template <int HD>
+__global__ void __launch_bounds__(128) attn_small_kernel(const AttnParams p) {
+  constexpr int TK = 32;  // one key per lane per tile
+  constexpr int DPL = (HD + 31) / 32;
+  __shared__ float Ks[TK][HD + 1];
+  __shared__ float Vs[TK][HD];
+  __shared__ float Qs[16][HD];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const int r0 = blockIdx.x * 16;
+  for (int i = threadIdx.x; i < 16 * HD; i += 128) {
+    const int r = i / HD, d = i - (i / HD) * HD;
+    const int gr = r0 + r;
+    Qs[r][d] = (gr < p.Lq) ? __bfloat162float(p.q[(long long)gr * p.ldq + head * HD + d]) : 0.f;
+  }
+  float m[4], l[4], acc[4][DPL];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    m[r] = -INFINITY;
+    l[r] = 0.f;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) acc[r][i] = 0.f;
+  }
+  for (int k0 = 0; k0 < p.Lk; k0 += TK) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < TK * HD; i += 128) {
+      const int r = i / HD, d = i - (i / HD) * HD;
+      const int gk = k0 + r;
+      float kv = 0.f, vv = 0.f;
+      if (gk < p.Lk) {
+        kv = __bfloat162float(p.k[(long long)gk * p.ldk + head * HD + d]);
+        vv = __bfloat162float(p.v[(long long)gk * p.ldv + head * HD + d]);
+      }
+      Ks[r][d] = kv;
+      Vs[r][d] = vv;
+    }
+    __syncthreads();
+    const int nk = min(TK, p.Lk - k0);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int lr = warp * 4 + r;
+      float s0 = 0.f;
+#pragma unroll 8
+      for (int d = 0; d < HD; ++d) s0 += Qs[lr][d] * Ks[lane][d];
+      s0 = (lane < nk) ? s0 * p.scale_log2 : -INFINITY;
+      float mx = s0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float mn = fmaxf(m[r], mx);
+      const float corr = ex2(m[r] - mn);
+      const float p0 = ex2(s0 - mn);
+      float ps = p0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      l[r] = l[r] * corr + ps;
+      m[r] = mn;
+#pragma unroll
+      for (int i = 0; i < DPL; ++i) acc[r][i] *= corr;
+      for (int j = 0; j < nk; ++j) {
+        const float pj = __shfl_sync(0xffffffffu, p0, j);
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) {
+          const int d = lane + 32 * i;
+          if (d < HD) acc[r][i] += pj * Vs[j][d];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int gr = r0 + warp * 4 + r;
+    if (gr >= p.Lq) continue;
+    const float inv = 1.f / l[r];
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+      const int d = lane + 32 * i;
+      if (d < HD) p.o[(long long)gr * p.ldo + head * HD + d] = __float2bfloat16_rn(acc[r][i] * inv);
+    }
+  }
+}
+
+template <int HD>
+static int launch_fmha(const AttnParams& p, cudaStream_t s) {
+  using C = FmhaCfg<HD>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fmha_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "fmha smem attribute");
+    configured = true;
+  }
+  CUtensorMap tq, tk, tv;
+  auto mk = [&](CUtensorMap* m, const void* ptr, long long ld, int rows) {
+    uint64_t dims[2] = {(uint64_t)ld, (uint64_t)rows};
+    uint64_t strides[1] = {(uint64_t)ld * 2};
+    uint32_t box[2] = {64, 128};
+    return make_tmap_bf16(m, ptr, 2, dims, strides, box);
+  };
+  int rc;
+  if ((rc = mk(&tq, p.q, p.ldq, p.Lq))) return rc;
+  if ((rc = mk(&tk, p.k, p.ldk, p.Lk))) return rc;
+  if ((rc = mk(&tv, p.v, p.ldv, p.Lk))) return rc;
+  dim3 grid((p.Lq + 127) / 128, p.heads);
+  fmha_tc_kernel<HD><<<grid, 256, C::SMEM, s>>>(tq, tk, tv, p);
+  return check_launch("fmha_tc_kernel");
+}
+
+template <int HD>
+static int launch_small(const AttnParams& p, cudaStream_t s) {
+  dim3 grid((p.Lq + 15) / 16, p.heads);
+  attn_small_kernel<HD><<<grid, 128, 0, s>>>(p);
+  return check_launch("attn_small_kernel");
+}
+
+}  // namespace ftb
+
+using namespace ftb;
+
+extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                                  int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads,
+                                  int32_t head_dim, float scale, void* stream) {
+  if (!q || !k || !v || !o || Lq < 0 || Lk <= 0 || heads <= 0 || head_dim <= 0)
+    return set_error(FTB_EINVAL, "attention: bad arguments");
+  if (Lq == 0) return FTB_OK;
+  AttnParams p{(const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (__nv_bfloat16*)o,
+               ldq, ldk, ldv, ldo, Lq, Lk, heads, head_dim, scale * 1.4426950408889634f};
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (impl == 0) {
+    if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
+    if (head_dim == 128) return launch_fmha<128>(p, s);
+    if (head_dim == 64) return launch_fmha<64>(p, s);
+    return set_error(FTB_EINVAL, "fmha: head_dim must be 64 or 128");
+  }
+  switch (head_dim) {
+    case 8: return launch_small<8>(p, s);
+    case 16: return launch_small<16>(p, s);
+    case 32: return launch_small<32>(p, s);
+    case 64: return launch_small<64>(p, s);
+    case 128: return launch_small<128>(p, s);
+    default: return set_error(FTB_EINVAL, "attention: head_dim must be one of 8,16,32,64,128");
+  }
+}
+
+extern "C" int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                             void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
+                             float scale, void* stream) {
+  const int impl = ((head_dim == 64 || head_dim == 128) && Lk > 128) ? 0 : 1;
+  return ftb_attention_impl(impl, q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim, scale, stream);
+}

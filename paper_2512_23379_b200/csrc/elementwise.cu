@@ -1,0 +1,290 @@
+// HBM-bound kernels of the denoise step: norm + AdaLN modulation, composite
+// assembly / patchify, unpatchify + DDIM update, codec decode, casts, fills.
+// All are row- or element-parallel with vectorised, coalesced access; grids
+// are sized in multiples of the SM count.
+#include "common.cuh"
+#include "ftb_internal.h"
+
+namespace ftb {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int THREADS>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < THREADS / 32; ++i) t += red[i];
+  return t;
+}
+
+// One CTA per row; two-pass mean / population variance in fp32 (LN of
+// backends/reference.py:41-46, eps inside the sqrt), then affine / AdaLN
+// modulation and a bf16 store.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) norm_modulate_kernel(
+    const float* __restrict__ x, long long ldx, int N, const float* __restrict__ gamma,
+    const float* __restrict__ beta, const float* __restrict__ scale, const float* __restrict__ shift,
+    long long mod_ld, int rows_per_group, long long row_offset, float eps, __nv_bfloat16* __restrict__ y,
+    long long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  __shared__ float red[THREADS / 32];
+  const long long row = blockIdx.x;
+  const float* xr = x + row * ldx;
+  float s = 0.f;
+  for (int c = threadIdx.x; c < N; c += THREADS) s += xr[c];
+  const float mean = block_sum<THREADS>(s, red) / N;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < N; c += THREADS) {
+    float d = xr[c] - mean;
+    ss += d * d;
+  }
+  const float var = block_sum<THREADS>(ss, red) / N;
+  const float rstd = rsqrtf(var + eps);
+  const long long g = rows_per_group > 0 ? (row + row_offset) / rows_per_group : 0;
+  const float* sc = scale ? scale + g * mod_ld : nullptr;
+  const float* sh = shift ? shift + g * mod_ld : nullptr;
+  __nv_bfloat16* yr = y + row * ldy;
+  for (int c = threadIdx.x; c < N; c += THREADS) {
+    float v = (xr[c] - mean) * rstd;
+    if (gamma) v *= gamma[c];
+    if (sc) v *= 1.f + sc[c];
+    if (beta) v += beta[c];
+    if (sh) v += sh[c];
+    yr[c] = __float2bfloat16_rn(v);
+  }
+  if (threadIdx.x == 0) {
+    if (mean_out) mean_out[row] = mean;
+    if (rstd_out) rstd_out[row] = rstd;
+  }
+}
+
+// Composite assembly (diffusion.py:150-179 + stacked :133-135) fused with the
+// 2x2 spatial patchify of the wan-mode token grid. One thread per output element.
+__global__ void patchify_kernel(const float* __restrict__ motion, const float* __restrict__ z,
+                                const float* __restrict__ ref, int Lm, int Lc, int D, int H, int W, int ph, int pw,
+                                __nv_bfloat16* __restrict__ out, long long ldo, long long total) {
+  const int gh = H / ph, gw = W / pw;
+  const long long tpf = (long long)gh * gw;
+  const int C = 2 * D + 1;
+  const int F = C * ph * pw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long tok = i / ldo;
+    const int feat = (int)(i - tok * ldo);
+    float v = 0.f;
+    if (feat < F) {
+      const int f = (int)(tok / tpf);
+      const int rem = (int)(tok - f * tpf);
+      const int ty = rem / gw, tx = rem - (rem / gw) * gw;
+      const int c = feat / (ph * pw);
+      const int pr = feat - c * ph * pw;
+      const int py = pr / pw, px = pr - (pr / pw) * pw;
+      const int yy = ty * ph + py, xx = tx * pw + px;
+      const long long pix = (long long)yy * W + xx;
+      if (c < D) {
+        v = (f < Lm) ? motion[((long long)f * D + c) * H * W + pix] : z[((long long)(f - Lm) * D + c) * H * W + pix];
+      } else if (c == D) {
+        v = (f == 0) ? 1.f : 0.f;  // z_mask = [1, 0, ...]
+      } else {
+        v = (f == 0) ? ref[(long long)(c - D - 1) * H * W + pix] : 0.f;  // z_cond row 0 = reference
+      }
+    }
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// x0 tokens -> target-frame latents; DDIM update of the sampler state
+// (diffusion.py:229-236): eps = (z - a_i x0)/s_i ; z = a_n x0 + s_n eps.
+__global__ void unpatch_ddim_kernel(const float* __restrict__ x0t, long long ldx, int Lm, int Lc, int D, int H,
+                                    int W, int ph, int pw, float* __restrict__ z, float* __restrict__ x0_out,
+                                    float a_i, float s_i, float a_n, float s_n, int update, long long total) {
+  const int gh = H / ph, gw = W / pw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    // i indexes x0_out [(Lc-Lm)][D][H][W]
+    long long t = i;
+    const int xx = (int)(t % W);
+    t /= W;
+    const int yy = (int)(t % H);
+    t /= H;
+    const int c = (int)(t % D);
+    const int ft = (int)(t / D);
+    const int f = ft + Lm;
+    const int ty = yy / ph, py = yy - ty * ph, tx = xx / pw, px = xx - tx * pw;
+    const long long tok = (long long)f * gh * gw + (long long)ty * gw + tx;
+    const float x0 = x0t[tok * ldx + (c * ph + py) * pw + px];
+    x0_out[i] = x0;
+    if (update) {
+      const float zi = z[i];
+      const float eps = (zi - a_i * x0) / s_i;
+      z[i] = a_n * x0 + s_n * eps;
+    }
+  }
+}
+
+__global__ void codec_decode_kernel(const float* __restrict__ lat, const float* __restrict__ Q,
+                                    float* __restrict__ out, int n, int D) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * D) return;
+  const int r = i / D, c = i - (i / D) * D;
+  float acc = 0.f;
+  for (int k = 0; k < D; ++k) acc += lat[r * D + k] * Q[k * D + c];
+  out[i] = acc;
+}
+
+__global__ void gelu_bf16_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(gelu_tanh(__bfloat162float(x[i])));
+}
+__global__ void silu_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float v = x[i];
+    y[i] = __float2bfloat16_rn(v / (1.f + __expf(-v)));
+  }
+}
+__global__ void cast_f2b_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+__global__ void cast_b2f_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = __bfloat162float(x[i]);
+}
+
+// Counter-based normal: splitmix64 hash of (seed, index) -> two uniforms -> Box-Muller.
+__device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ float normal_at(uint64_t seed, long long i) {
+  uint64_t h = splitmix(seed ^ splitmix((uint64_t)i));
+  float u1 = ((uint32_t)(h >> 40) + 1) * (1.0f / 16777217.0f);
+  float u2 = ((uint32_t)(h & 0xFFFFFF)) * (1.0f / 16777216.0f);
+  return sqrtf(-2.f * __logf(u1)) * __cosf(6.28318530718f * u2);
+}
+__global__ void fill_normal_bf16_kernel(__nv_bfloat16* out, long long n, uint64_t seed, float scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(normal_at(seed, i) * scale);
+}
+__global__ void fill_normal_f32_kernel(float* out, long long n, uint64_t seed, float scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = normal_at(seed, i) * scale;
+}
+__global__ void count_nonfinite_kernel(const float* __restrict__ x, long long n, int* out) {
+  int c = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    c += !isfinite(x[i]);
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+static inline int grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  long long cap = (long long)sm_count() * 8;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace ftb
+
+using namespace ftb;
+#define S(stream) reinterpret_cast<cudaStream_t>(stream)
+
+extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t N, const float* gamma,
+                                 const float* beta, const float* scale, const float* shift, int64_t mod_ld,
+                                 int32_t rows_per_group, int64_t row_offset, float eps, void* y, int64_t ldy,
+                                 float* mean_out, float* rstd_out, void* stream) {
+  if (!x || !y || M < 0 || N <= 0) return set_error(FTB_EINVAL, "norm: bad arguments");
+  if (M == 0) return FTB_OK;
+  if ((scale || shift) && rows_per_group <= 0) return set_error(FTB_EINVAL, "norm: modulation needs rows_per_group");
+  if (N >= 1024)
+    norm_modulate_kernel<256><<<M, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, rows_per_group,
+                                                          row_offset, eps, (__nv_bfloat16*)y, ldy, mean_out, rstd_out);
+  else
+    norm_modulate_kernel<32><<<M, 32, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, rows_per_group,
+                                                        row_offset, eps, (__nv_bfloat16*)y, ldy, mean_out, rstd_out);
+  return check_launch("norm_modulate_kernel");
+}
+
+extern "C" int ftb_patchify_composite(const float* motion, const float* z, const float* reference, int32_t Lm,
+                                      int32_t Lc, int32_t D, int32_t H, int32_t W, int32_t ph, int32_t pw, void* out,
+                                      int64_t ldo, void* stream) {
+  if (!z || !reference || !out || Lc <= Lm || Lm < 0 || D <= 0 || H % ph || W % pw)
+    return set_error(FTB_EINVAL, "patchify: bad arguments");
+  if (Lm > 0 && !motion) return set_error(FTB_EINVAL, "patchify: motion required");
+  if (ldo < (int64_t)(2 * D + 1) * ph * pw) return set_error(FTB_EINVAL, "patchify: ldo too small");
+  long long tokens = (long long)Lc * (H / ph) * (W / pw);
+  long long total = tokens * ldo;
+  patchify_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(motion, z, reference, Lm, Lc, D, H, W, ph, pw,
+                                                               (__nv_bfloat16*)out, ldo, total);
+  return check_launch("patchify_kernel");
+}
+
+extern "C" int ftb_unpatch_ddim(const float* x0_tok, int64_t ldx, int32_t Lm, int32_t Lc, int32_t D, int32_t H,
+                                int32_t W, int32_t ph, int32_t pw, float* z, float* x0_out, float a_i, float s_i,
+                                float a_n, float s_n, int32_t update, void* stream) {
+  if (!x0_tok || !x0_out || Lc <= Lm || H % ph || W % pw) return set_error(FTB_EINVAL, "unpatch: bad arguments");
+  if (update && (!z || s_i == 0.f)) return set_error(FTB_EINVAL, "unpatch: DDIM update needs z and sigma > 0");
+  long long total = (long long)(Lc - Lm) * D * H * W;
+  unpatch_ddim_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(x0_tok, ldx, Lm, Lc, D, H, W, ph, pw, z, x0_out,
+                                                                   a_i, s_i, a_n, s_n, update, total);
+  return check_launch("unpatch_ddim_kernel");
+}
+
+extern "C" int ftb_codec_decode(const float* latents, const float* Q, float* frames, int32_t n, int32_t D,
+                                void* stream) {
+  if (!latents || !Q || !frames || n < 0 || D <= 0) return set_error(FTB_EINVAL, "codec: bad arguments");
+  if (n == 0) return FTB_OK;
+  codec_decode_kernel<<<(n * D + 127) / 128, 128, 0, S(stream)>>>(latents, Q, frames, n, D);
+  return check_launch("codec_decode_kernel");
+}
+
+extern "C" int ftb_gelu_bf16(const void* x, void* y, int64_t n, void* stream) {
+  if (n <= 0) return FTB_OK;
+  gelu_bf16_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)y, n);
+  return check_launch("gelu_bf16_kernel");
+}
+extern "C" int ftb_silu_f32_to_bf16(const float* x, void* y, int64_t n, void* stream) {
+  if (n <= 0) return FTB_OK;
+  silu_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(x, (__nv_bfloat16*)y, n);
+  return check_launch("silu_kernel");
+}
+extern "C" int ftb_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
+  if (n <= 0) return FTB_OK;
+  cast_f2b_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(x, (__nv_bfloat16*)y, n);
+  return check_launch("cast_f2b_kernel");
+}
+extern "C" int ftb_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream) {
+  if (n <= 0) return FTB_OK;
+  cast_b2f_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>((const __nv_bfloat16*)x, y, n);
+  return check_launch("cast_b2f_kernel");
+}
+extern "C" int ftb_fill_normal_bf16(void* out, int64_t n, uint64_t seed, float scale, void* stream) {
+  if (n <= 0) return FTB_OK;
+  fill_normal_bf16_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>((__nv_bfloat16*)out, n, seed, scale);
+  return check_launch("fill_normal_bf16_kernel");
+}
+extern "C" int ftb_fill_normal_f32(float* out, int64_t n, uint64_t seed, float scale, void* stream) {
+  if (n <= 0) return FTB_OK;
+  fill_normal_f32_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(out, n, seed, scale);
+  return check_launch("fill_normal_f32_kernel");
+}
+extern "C" int ftb_count_nonfinite(const float* x, int64_t n, int32_t* out, void* stream) {
+  if (!out) return set_error(FTB_EINVAL, "count_nonfinite: null out");
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int32_t), S(stream));
+  if (e != cudaSuccess) return set_cuda_error(e, "count_nonfinite memset");
+  if (n <= 0) return FTB_OK;
+  count_nonfinite_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(x, n, out);
+  return check_launch("count_nonfinite_kernel");
+}

@@ -1,0 +1,378 @@
+// Persistent warp-specialised tcgen05 GEMM with fused epilogues.
+//
+//   C[M,N] = A[M,K] . B[N,K]^T     bf16 x bf16 -> fp32 (TMEM) -> epilogue
+//
+// Roles (256 threads, 1 CTA / SM):
+//   warp 0     TMA producer (one elected lane): A/B k-blocks -> smem ring
+//   warp 1     MMA issuer (one lane): tcgen05.mma M=128 x N=BN x K=16, accumulators
+//              double-buffered in TMEM so tile i+1's MMAs overlap tile i's epilogue
+//   warp 2     TMEM allocator
+//   warps 4-7  epilogue: tcgen05.ld -> bias / GELU / gate*residual / row-add / RoPE -> global
+//
+// Operand tiles are 128B-swizzled K-major (TMA SWIZZLE_128B box {64, rows});
+// descriptors use SBO = 1024 B (8 rows x 128 B), K advance +32 B per UMMA_K.
+// Replaces the reference's dense_forward (backends/reference.py:17-18) and the
+// adds/activations that follow it in net.py:230-274.
+#include "common.cuh"
+#include "ftb_internal.h"
+
+namespace ftb {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 256;
+
+struct GemmParams {
+  int M, N, K;
+  int kc;  // K per A chunk (K when a_chunks == 1)
+  int kind;
+  int rows_per_group;
+  long long row_offset;
+  const float* bias;
+  const float* group_vec;
+  long long group_ld;
+  void* out;
+  long long ldc;
+  int heads, head_dim, hpr;
+  ftb_rope3d rope;
+  int has_rope;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
+  static constexpr int B_BYTES = BN * GEMM_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__device__ __forceinline__ void rope_rotate(const GemmParams& p, long long token, int pair, float& x0, float& x1) {
+  const ftb_rope3d& r = p.rope;
+  int tpf = r.grid_h * r.grid_w;
+  int f = (int)(token / tpf);
+  int rem = (int)(token - (long long)f * tpf);
+  int y = rem / r.grid_w;
+  int x = rem - y * r.grid_w;
+  float c, s;
+  if (pair < r.pairs_t) {
+    c = __ldg(r.cos_t + (long long)f * r.pairs_t + pair);
+    s = __ldg(r.sin_t + (long long)f * r.pairs_t + pair);
+  } else if (pair < r.pairs_t + r.pairs_h) {
+    int q = pair - r.pairs_t;
+    c = __ldg(r.cos_h + (long long)y * r.pairs_h + q);
+    s = __ldg(r.sin_h + (long long)y * r.pairs_h + q);
+  } else {
+    int q = pair - r.pairs_t - r.pairs_h;
+    c = __ldg(r.cos_w + (long long)x * r.pairs_w + q);
+    s = __ldg(r.sin_w + (long long)x * r.pairs_w + q);
+  }
+  float a = x0 * c - x1 * s;
+  float b = x0 * s + x1 * c;
+  x0 = a;
+  x1 = b;
+}
+
+// Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int gc0, float (&v)[32]) {
+  const int N = p.N;
+  const bool full = (gc0 + 32 <= N);
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (full || gc0 + j < N) v[j] += __ldg(p.bias + gc0 + j);
+  }
+  const long long g = (p.rows_per_group > 0) ? (gr + p.row_offset) / p.rows_per_group : 0;
+  switch (p.kind) {
+    case FTB_EPI_GELU_BF16:
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+      // fallthrough
+    case FTB_EPI_BF16: {
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)gr * p.ldc + gc0;
+      if (full && ((p.ldc & 7) == 0)) {
+        uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+          w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+          w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+          w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+          o4[q] = w;
+        }
+      } else {
+        for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] = __float2bfloat16_rn(v[j]);
+      }
+      break;
+    }
+    case FTB_EPI_F32: {
+      float* o = reinterpret_cast<float*>(p.out) + (long long)gr * p.ldc + gc0;
+      if (full && ((p.ldc & 3) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      } else {
+        for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] = v[j];
+      }
+      break;
+    }
+    case FTB_EPI_RESID_F32: {
+      float* o = reinterpret_cast<float*>(p.out) + (long long)gr * p.ldc + gc0;
+      const float* gate = p.group_vec ? p.group_vec + g * p.group_ld + gc0 : nullptr;
+      if (full && ((p.ldc & 3) == 0) && (!gate || (p.group_ld & 3) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 r = reinterpret_cast<float4*>(o)[q];
+          float4 gg = gate ? __ldg(reinterpret_cast<const float4*>(gate) + q) : make_float4(1.f, 1.f, 1.f, 1.f);
+          r.x += gg.x * v[4 * q + 0];
+          r.y += gg.y * v[4 * q + 1];
+          r.z += gg.z * v[4 * q + 2];
+          r.w += gg.w * v[4 * q + 3];
+          reinterpret_cast<float4*>(o)[q] = r;
+        }
+      } else {
+        for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] += (gate ? gate[j] : 1.f) * v[j];
+      }
+      break;
+    }
+    case FTB_EPI_ROWADD_F32: {
+      float* o = reinterpret_cast<float*>(p.out) + (long long)gr * p.ldc + gc0;
+      const float* add = p.group_vec ? p.group_vec + g * p.group_ld + gc0 : nullptr;
+      for (int j = 0; j < 32; ++j) {
+        if (!full && gc0 + j >= N) break;
+        o[j] = v[j] + (add ? __ldg(add + j) : 0.f);
+      }
+      break;
+    }
+    case FTB_EPI_QKV_ROPE: {
+      const int m = p.heads * p.head_dim;
+      const long long token = gr + p.row_offset;
+      __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.out);
+#pragma unroll 4
+      for (int j = 0; j < 32; j += 2) {
+        int c = gc0 + j;
+        if (c >= N) break;
+        int which = c / m;
+        int cm = c - which * m;
+        int h = cm / p.head_dim;
+        int d = cm - h * p.head_dim;
+        float x0 = v[j], x1 = v[j + 1];
+        if (which < 2 && p.has_rope) rope_rotate(p, token, d >> 1, x0, x1);
+        int dest = h / p.hpr;
+        int hl = h - dest * p.hpr;
+        long long idx = (((long long)dest * p.M + gr) * 3 + which) * ((long long)p.hpr * p.head_dim) +
+                        (long long)hl * p.head_dim + d;
+        *reinterpret_cast<uint32_t*>(base + idx) = pack_bf16(x0, x1);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmParams p) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int num_m = (p.M + GEMM_BM - 1) / GEMM_BM;
+  const int num_n = (p.N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          const int k0 = kb * GEMM_BK;
+          const int chunk = k0 / p.kc;
+          tma_load_3d(sa, &tmA, &full_bar[stage], k0 - chunk * p.kc, m_blk * GEMM_BM, chunk);
+          tma_load_2d(sb, &tmB, &full_bar[stage], k0, n_blk * BN);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(GEMM_BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
+            uint64_t bd = sdesc_sw128(sb + k * 32, 16, 1024);
+            mma_bf16_ss(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue
+    const int q = warp & 3;  // TMEM lane quadrant
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int gr = m_blk * GEMM_BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int gc0 = n_blk * BN + c0;
+        if (gc0 >= p.N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (gr < p.M) epilogue_chunk(p, gr, gc0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+template <int BN>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
+    configured = true;
+  }
+  const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, C::SMEM, stream>>>(ta, tb, p);
+  return check_launch("gemm_tc_kernel");
+}
+
+}  // namespace ftb
+
+using namespace ftb;
+
+extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_stride, const void* B,
+                             int64_t ldb, int32_t M, int32_t N, int32_t K, const ftb_epilogue* epi, void* stream) {
+  if (!A || !B || !epi || !epi->out) return set_error(FTB_EINVAL, "gemm: null pointer");
+  if (M <= 0 || N <= 0 || K <= 0) return set_error(FTB_EINVAL, "gemm: empty problem");
+  if ((lda & 7) || (ldb & 7)) return set_error(FTB_EINVAL, "gemm: lda/ldb must be multiples of 8 elements");
+  if (a_chunks < 1) a_chunks = 1;
+  if (K % a_chunks) return set_error(FTB_EINVAL, "gemm: K not divisible by a_chunks");
+  const int kc = K / a_chunks;
+  if (a_chunks > 1 && (kc % GEMM_BK)) return set_error(FTB_EINVAL, "gemm: K/a_chunks must be a multiple of 64");
+  if (a_chunks > 1 && (a_chunk_stride & 7)) return set_error(FTB_EINVAL, "gemm: chunk stride alignment");
+  if (epi->kind < FTB_EPI_BF16 || epi->kind > FTB_EPI_QKV_ROPE) return set_error(FTB_EINVAL, "gemm: bad epilogue");
+  if (epi->kind == FTB_EPI_QKV_ROPE) {
+    if (epi->heads <= 0 || epi->head_dim <= 0 || (epi->head_dim & 1) || epi->heads_per_rank <= 0 ||
+        epi->heads % epi->heads_per_rank || N != 3 * epi->heads * epi->head_dim)
+      return set_error(FTB_EINVAL, "gemm: bad QKV layout");
+  }
+  GemmParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.kc = kc;
+  p.kind = epi->kind;
+  p.rows_per_group = epi->rows_per_group;
+  p.row_offset = epi->row_offset;
+  p.bias = epi->bias;
+  p.group_vec = epi->group_vec;
+  p.group_ld = epi->group_ld;
+  p.out = epi->out;
+  p.ldc = epi->ldc;
+  p.heads = epi->heads;
+  p.head_dim = epi->head_dim;
+  p.hpr = epi->heads_per_rank;
+  p.has_rope = epi->rope != nullptr;
+  if (epi->rope) p.rope = *epi->rope;
+
+  const int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  CUtensorMap ta, tb;
+  // A: 3D {kc, M, chunks}
+  {
+    uint64_t dims[3] = {(uint64_t)kc, (uint64_t)M, (uint64_t)a_chunks};
+    uint64_t strides[2] = {(uint64_t)lda * 2, (uint64_t)(a_chunks > 1 ? a_chunk_stride : (int64_t)lda * M) * 2};
+    uint32_t box[3] = {GEMM_BK, GEMM_BM, 1};
+    int rc = make_tmap_bf16(&ta, A, 3, dims, strides, box);
+    if (rc) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
+    uint64_t strides[1] = {(uint64_t)ldb * 2};
+    uint32_t box[2] = {GEMM_BK, (uint32_t)BN};
+    int rc = make_tmap_bf16(&tb, B, 2, dims, strides, box);
+    if (rc) return rc;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (BN == 64) return launch_gemm<64>(ta, tb, p, s);
+  if (BN == 128) return launch_gemm<128>(ta, tb, p, s);
+  return launch_gemm<256>(ta, tb, p, s);
+}

@@ -1,0 +1,158 @@
+"""Device-tensor wrappers over the C-ABI kernels (torch tensors for memory and
+streams only; all arithmetic happens in libftb2.so).
+
+Conventions: activations are row-major with an explicit leading dimension
+(row stride); weights are stored transposed, W^T [N, K] bf16 (K-major), which
+is the tcgen05 B-operand layout. The reference stores (in, out) and computes
+x @ W + b (`backends/reference.py:17-18`); W^T is the same matrix.
+"""
+
+import ctypes as C
+
+import torch
+
+from . import _capi as A
+from .errors import ConfigError
+
+KINDS = {"bf16": A.EPI_BF16, "gelu_bf16": A.EPI_GELU_BF16, "f32": A.EPI_F32,
+         "resid_f32": A.EPI_RESID_F32, "rowadd_f32": A.EPI_ROWADD_F32, "qkv_rope": A.EPI_QKV_ROPE}
+
+
+def _ld(t):
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ConfigError("expected a 2-d row-major tensor (unit column stride)")
+    return t.stride(0)
+
+
+def _need(t, dtype, name):
+    if not t.is_cuda or t.dtype != dtype:
+        raise ConfigError("%s must be a CUDA %s tensor" % (name, dtype))
+
+
+class RopeTables:
+    """Device copy of host-computed 3D RoPE cos/sin tables (see rope.py)."""
+
+    def __init__(self, tables, grid_h, grid_w, device):
+        self.t = {k: torch.as_tensor(v, dtype=torch.float32).contiguous().to(device) for k, v in tables.items()}
+        self.struct = A.Rope3D(A.ptr(self.t["cos_t"]), A.ptr(self.t["sin_t"]), A.ptr(self.t["cos_h"]),
+                               A.ptr(self.t["sin_h"]), A.ptr(self.t["cos_w"]), A.ptr(self.t["sin_w"]),
+                               self.t["cos_t"].shape[1], self.t["cos_h"].shape[1], self.t["cos_w"].shape[1],
+                               grid_h, grid_w)
+
+
+def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=0, row_offset=0,
+         M=None, K=None, lda=None, a_chunks=1, a_chunk_stride=0, heads=0, head_dim=0,
+         heads_per_rank=0, rope=None, stream=None):
+    """out <- epilogue(a[M,K] @ w_t[N,K]^T). `a` may be a raw buffer when
+    a_chunks > 1 (Ulysses gather: M, K, lda, a_chunk_stride explicit)."""
+    _need(a, torch.bfloat16, "A")
+    _need(w_t, torch.bfloat16, "W^T")
+    N, Kw = w_t.shape
+    if M is None:
+        M, K = a.shape
+        lda = _ld(a)
+    if K != Kw:
+        raise ConfigError("gemm: K mismatch %d vs %d" % (K, Kw))
+    k = KINDS[kind]
+    ldc = 0 if k == A.EPI_QKV_ROPE else _ld(out)
+    if k in (A.EPI_BF16, A.EPI_GELU_BF16, A.EPI_QKV_ROPE):
+        _need(out, torch.bfloat16, "out")
+    else:
+        _need(out, torch.float32, "out")
+    group_ld = 0
+    if group_vec is not None:
+        _need(group_vec, torch.float32, "group_vec")
+        group_ld = _ld(group_vec)
+    if bias is not None:
+        _need(bias, torch.float32, "bias")
+    epi = A.Epilogue(k, rows_per_group, row_offset, A.ptr(bias), A.ptr(group_vec), group_ld, A.ptr(out), ldc,
+                     heads, head_dim, heads_per_rank, C.pointer(rope.struct) if rope is not None else None)
+    A.call("ftb_gemm_bf16", A.ptr(a), lda, a_chunks, a_chunk_stride, A.ptr(w_t), _ld(w_t), M, N, K,
+           C.byref(epi), A.stream_ptr(stream))
+    return out
+
+
+def norm_modulate(x, out, *, gamma=None, beta=None, scale=None, shift=None, rows_per_group=0, row_offset=0,
+                  eps=1e-6, mean_out=None, rstd_out=None, stream=None):
+    _need(x, torch.float32, "x")
+    _need(out, torch.bfloat16, "out")
+    M, N = x.shape
+    mod_ld = 0
+    for t in (scale, shift):
+        if t is not None:
+            mod_ld = _ld(t)
+    if scale is not None and shift is not None and scale.stride(0) != shift.stride(0):
+        raise ConfigError("scale/shift strides differ")
+    A.call("ftb_norm_modulate", A.ptr(x), _ld(x), M, N, A.ptr(gamma), A.ptr(beta), A.ptr(scale), A.ptr(shift),
+           mod_ld, rows_per_group, row_offset, float(eps), A.ptr(out), _ld(out), A.ptr(mean_out),
+           A.ptr(rstd_out), A.stream_ptr(stream))
+    return out
+
+
+def attention(q, k, v, out, heads, head_dim, Lq, Lk, scale, *, impl=None, stream=None):
+    """q/k/v/out are 2-d views (rows, ld) whose head h lives at columns
+    [h*head_dim, (h+1)*head_dim)."""
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
+        _need(t, torch.bfloat16, nm)
+    args = (A.ptr(q), _ld(q), A.ptr(k), _ld(k), A.ptr(v), _ld(v), A.ptr(out), _ld(out),
+            Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))
+    if impl is None:
+        A.call("ftb_attention", *args)
+    else:
+        A.call("ftb_attention_impl", int(impl), *args)
+    return out
+
+
+def patchify(motion, z, reference, Lm, Lc, D, H, W, ph, pw, out, stream=None):
+    A.call("ftb_patchify_composite", A.ptr(motion) if Lm > 0 else None, A.ptr(z), A.ptr(reference),
+           Lm, Lc, D, H, W, ph, pw, A.ptr(out), _ld(out), A.stream_ptr(stream))
+    return out
+
+
+def unpatch_ddim(x0_tok, Lm, Lc, D, H, W, ph, pw, z, x0_out, coeffs=None, stream=None):
+    if coeffs is None:
+        a_i = s_i = a_n = s_n = 0.0
+        upd = 0
+    else:
+        a_i, s_i, a_n, s_n = coeffs
+        upd = 1
+    A.call("ftb_unpatch_ddim", A.ptr(x0_tok), _ld(x0_tok), Lm, Lc, D, H, W, ph, pw, A.ptr(z), A.ptr(x0_out),
+           float(a_i), float(s_i), float(a_n), float(s_n), upd, A.stream_ptr(stream))
+
+
+def codec_decode(latents, Q, out, stream=None):
+    n, D = latents.shape
+    A.call("ftb_codec_decode", A.ptr(latents), A.ptr(Q), A.ptr(out), n, D, A.stream_ptr(stream))
+    return out
+
+
+def silu_to_bf16(x, out, stream=None):
+    A.call("ftb_silu_f32_to_bf16", A.ptr(x), A.ptr(out), x.numel(), A.stream_ptr(stream))
+    return out
+
+
+def cast_f32_bf16(x, out, stream=None):
+    A.call("ftb_cast_f32_bf16", A.ptr(x), A.ptr(out), x.numel(), A.stream_ptr(stream))
+    return out
+
+
+def gelu_bf16(x, out, stream=None):
+    A.call("ftb_gelu_bf16", A.ptr(x), A.ptr(out), x.numel(), A.stream_ptr(stream))
+    return out
+
+
+def fill_normal_(t, seed, scale=1.0, stream=None):
+    if t.dtype == torch.bfloat16:
+        A.call("ftb_fill_normal_bf16", A.ptr(t), t.numel(), int(seed) & ((1 << 64) - 1), float(scale),
+               A.stream_ptr(stream))
+    elif t.dtype == torch.float32:
+        A.call("ftb_fill_normal_f32", A.ptr(t), t.numel(), int(seed) & ((1 << 64) - 1), float(scale),
+               A.stream_ptr(stream))
+    else:
+        raise ConfigError("fill_normal_: bf16 or f32 only")
+    return t
+
+
+def count_nonfinite(x, flag, stream=None):
+    A.call("ftb_count_nonfinite", A.ptr(x), x.numel(), A.ptr(flag), A.stream_ptr(stream))
+    return flag

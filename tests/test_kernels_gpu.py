@@ -1,0 +1,255 @@
+"""Kernel-level numerics on the B200: every sm_100a kernel against a plain
+PyTorch fp32 reference of the same op on the same (bf16-exact) inputs.
+
+Tolerances: fp32-output GEMMs accumulate in fp32 over bf16 inputs that are
+exactly representable, so they match an fp32 matmul to ~1e-5 relative;
+bf16 outputs add one rounding (<= 2^-8 relative); attention stores P in bf16
+(flash kernel) -> 1e-2 relative L2 (the north-star bf16 budget).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+def bf(x):
+    return x.to(torch.bfloat16)
+
+
+@pytest.fixture(scope="module")
+def ops(cuda):
+    from paper_2512_23379_b200 import ops as O
+    return O
+
+
+GEMM_SHAPES = [(128, 256, 64), (9, 32, 24), (9, 8, 32), (300, 200, 160), (1000, 768, 1536),
+               (257, 64, 96), (2048, 1536, 1536), (130, 4608, 512), (64, 48, 200)]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_f32_bias(ops, cuda, M, N, K):
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    b = torch.randn(N, generator=g).to(cuda)
+    out = torch.empty(M, N, device=cuda)
+    ops.gemm(a, w, out, "f32", bias=b)
+    ref = a.float() @ w.float().t() + b
+    torch.cuda.synchronize()
+    assert rel(out, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 200, 160), (1024, 1024, 512)])
+def test_gemm_bf16_and_gelu(ops, cuda, M, N, K):
+    g = torch.Generator().manual_seed(3)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    b = torch.randn(N, generator=g).to(cuda)
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    ops.gemm(a, w, out, "bf16", bias=b)
+    ref = a.float() @ w.float().t() + b
+    assert rel(out.float(), ref) < 5e-3
+    ops.gemm(a, w, out, "gelu_bf16", bias=b)
+    refg = 0.5 * ref * (1 + torch.tanh(math.sqrt(2 / math.pi) * (ref + 0.044715 * ref ** 3)))
+    assert rel(out.float(), refg) < 5e-3
+
+
+def test_gemm_resid_gate_and_rowadd(ops, cuda):
+    g = torch.Generator().manual_seed(5)
+    M, N, K, rpg = 9 * 40, 256, 128, 40
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    b = torch.randn(N, generator=g).to(cuda)
+    gate = torch.randn(9, N, generator=g).to(cuda)
+    h = torch.randn(M, N, generator=g).to(cuda)
+    h0 = h.clone()
+    ops.gemm(a, w, h, "resid_f32", bias=b, group_vec=gate, rows_per_group=rpg)
+    grp = torch.arange(M, device=cuda) // rpg
+    ref = h0 + gate[grp] * (a.float() @ w.float().t() + b)
+    assert rel(h, ref) < 1e-5
+    ops.gemm(a, w, h, "resid_f32")
+    assert rel(h, ref + a.float() @ w.float().t()) < 1e-5
+    out = torch.empty(M, N, device=cuda)
+    ops.gemm(a, w, out, "rowadd_f32", bias=b, group_vec=gate, rows_per_group=rpg)
+    assert rel(out, a.float() @ w.float().t() + b + gate[grp]) < 1e-5
+
+
+def test_gemm_chunked_a(ops, cuda):
+    """Ulysses gather layout: A's K dim arrives as g head-group slices."""
+    g = torch.Generator().manual_seed(9)
+    chunks, M, kc, N = 4, 300, 128, 192
+    raw = bf(torch.randn(chunks, M, kc, generator=g)).to(cuda)
+    w = bf(torch.randn(N, chunks * kc, generator=g) / 20).to(cuda)
+    out = torch.empty(M, N, device=cuda)
+    ops.gemm(raw, w, out, "f32", M=M, K=chunks * kc, lda=kc, a_chunks=chunks, a_chunk_stride=M * kc)
+    a = raw.permute(1, 0, 2).reshape(M, chunks * kc)
+    assert rel(out, a.float() @ w.float().t()) < 1e-5
+
+
+def _rope_tables(frames, gh, gw, hd, theta=10000.0):
+    from paper_2512_23379_b200.rope import rope3d_tables
+    return rope3d_tables(frames, gh, gw, hd, theta)
+
+
+@pytest.mark.parametrize("hpr", [4, 2, 1])
+def test_gemm_qkv_rope_layout(ops, cuda, hpr):
+    from paper_2512_23379_b200.ops import RopeTables
+    heads, hd, frames, gh, gw = 4, 64, 3, 4, 6
+    m = heads * hd
+    M = frames * gh * gw
+    g = torch.Generator().manual_seed(2)
+    a = bf(torch.randn(M, m, generator=g)).to(cuda)
+    w = bf(torch.randn(3 * m, m, generator=g) / 16).to(cuda)
+    tabs = _rope_tables(frames, gh, gw, hd)
+    rt = RopeTables(tabs, gh, gw, cuda)
+    out = torch.empty(M * 3 * m, device=cuda, dtype=torch.bfloat16)
+    ops.gemm(a, w, out.view(M, 3 * m), "qkv_rope", heads=heads, head_dim=hd, heads_per_rank=hpr, rope=rt)
+    y = (a.float() @ w.float().t()).cpu().double().numpy().reshape(M, 3, heads, hd)
+    # reference rotation on (q, k)
+    ang = np.zeros((M, hd // 2))
+    pt, ph, pw = tabs["cos_t"].shape[1], tabs["cos_h"].shape[1], tabs["cos_w"].shape[1]
+    cos = np.zeros((M, hd // 2))
+    sin = np.zeros((M, hd // 2))
+    for t in range(M):
+        f, rem = divmod(t, gh * gw)
+        yy, xx = divmod(rem, gw)
+        cos[t] = np.concatenate([tabs["cos_t"][f], tabs["cos_h"][yy], tabs["cos_w"][xx]])
+        sin[t] = np.concatenate([tabs["sin_t"][f], tabs["sin_h"][yy], tabs["sin_w"][xx]])
+    ref = y.copy()
+    for which in (0, 1):
+        x0, x1 = y[:, which, :, 0::2], y[:, which, :, 1::2]
+        ref[:, which, :, 0::2] = x0 * cos[:, None] - x1 * sin[:, None]
+        ref[:, which, :, 1::2] = x0 * sin[:, None] + x1 * cos[:, None]
+    g_ = heads // hpr
+    got = out.float().cpu().double().numpy().reshape(g_, M, 3, hpr, hd)
+    got = got.transpose(1, 2, 0, 3, 4).reshape(M, 3, heads, hd)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 5e-3
+    del ang, pt, ph, pw
+
+
+def torch_attn(q, k, v, heads, hd, scale):
+    Lq, Lk = q.shape[0], k.shape[0]
+    qh = q.float().view(Lq, heads, hd).transpose(0, 1)
+    kh = k.float().view(Lk, heads, hd).transpose(0, 1)
+    vh = v.float().view(Lk, heads, hd).transpose(0, 1)
+    p = torch.softmax(qh @ kh.transpose(1, 2) * scale, dim=-1)
+    return (p @ vh).transpose(0, 1).reshape(Lq, heads * hd)
+
+
+@pytest.mark.parametrize("Lq,Lk,heads,hd", [(128, 128, 1, 128), (300, 300, 2, 128), (1170, 1170, 3, 128),
+                                            (500, 777, 2, 64), (2340, 2340, 2, 128), (129, 1000, 1, 64)])
+def test_fmha_tcgen05(ops, cuda, Lq, Lk, heads, hd):
+    g = torch.Generator().manual_seed(Lq + Lk)
+    q = bf(torch.randn(Lq, heads * hd, generator=g)).to(cuda)
+    k = bf(torch.randn(Lk, heads * hd, generator=g)).to(cuda)
+    v = bf(torch.randn(Lk, heads * hd, generator=g)).to(cuda)
+    o = torch.empty(Lq, heads * hd, device=cuda, dtype=torch.bfloat16)
+    scale = 1 / math.sqrt(hd)
+    ops.attention(q, k, v, o, heads, hd, Lq, Lk, scale, impl=0)
+    assert rel(o.float(), torch_attn(q, k, v, heads, hd, scale)) < 1e-2
+
+
+def test_fmha_strided_qkv_layout(ops, cuda):
+    """q|k|v interleaved per token ([L, 3, H, hd]) as produced by the QKV epilogue."""
+    L, heads, hd = 700, 3, 128
+    g = torch.Generator().manual_seed(1)
+    qkv = bf(torch.randn(L, 3 * heads * hd, generator=g) * 2).to(cuda)
+    m = heads * hd
+    q, k, v = qkv[:, :m], qkv[:, m:2 * m], qkv[:, 2 * m:]
+    o = torch.empty(L, m, device=cuda, dtype=torch.bfloat16)
+    ops.attention(q, k, v, o, heads, hd, L, L, 1 / math.sqrt(hd), impl=0)
+    assert rel(o.float(), torch_attn(q, k, v, heads, hd, 1 / math.sqrt(hd))) < 1e-2
+
+
+@pytest.mark.parametrize("Lq,Lk,heads,hd", [(9, 9, 2, 16), (9, 10, 2, 16), (1170, 37, 4, 128), (100, 70, 3, 64),
+                                            (5, 3, 4, 8), (33, 100, 2, 32)])
+def test_attention_small(ops, cuda, Lq, Lk, heads, hd):
+    g = torch.Generator().manual_seed(Lq * 3 + Lk)
+    q = bf(torch.randn(Lq, heads * hd, generator=g)).to(cuda)
+    k = bf(torch.randn(Lk, heads * hd, generator=g)).to(cuda)
+    v = bf(torch.randn(Lk, heads * hd, generator=g)).to(cuda)
+    o = torch.empty(Lq, heads * hd, device=cuda, dtype=torch.bfloat16)
+    scale = 1 / math.sqrt(hd)
+    ops.attention(q, k, v, o, heads, hd, Lq, Lk, scale, impl=1)
+    assert rel(o.float(), torch_attn(q, k, v, heads, hd, scale)) < 5e-3
+
+
+@pytest.mark.parametrize("M,N", [(9, 32), (300, 1536), (17, 5120)])
+def test_norm_modulate(ops, cuda, M, N):
+    g = torch.Generator().manual_seed(N)
+    x = (torch.randn(M, N, generator=g) * 3 + 1.5).to(cuda)
+    gam, bet = torch.randn(N, generator=g).to(cuda), torch.randn(N, generator=g).to(cuda)
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    mean = torch.empty(M, device=cuda)
+    rstd = torch.empty(M, device=cuda)
+    ops.norm_modulate(x, out, gamma=gam, beta=bet, mean_out=mean, rstd_out=rstd)
+    mu = x.double().mean(1)
+    var = x.double().var(1, unbiased=False)
+    rs = 1 / torch.sqrt(var + 1e-6)
+    ref = (x.double() - mu[:, None]) * rs[:, None] * gam.double() + bet.double()
+    assert rel(out.float(), ref.float()) < 5e-3
+    assert rel(mean, mu.float()) < 1e-5 and rel(rstd, rs.float()) < 1e-5
+    # AdaLN: per-group (1 + scale), shift
+    G = 3
+    rpg = (M + G - 1) // G
+    mod = torch.randn(G, 2, N, generator=g).to(cuda)
+    ops.norm_modulate(x, out, scale=mod[:, 0], shift=mod[:, 1], rows_per_group=rpg)
+    grp = torch.arange(M, device=cuda) // rpg
+    ref2 = (x.double() - mu[:, None]) * rs[:, None] * (1 + mod[grp, 0].double()) + mod[grp, 1].double()
+    assert rel(out.float(), ref2.float()) < 5e-3
+
+
+def test_patchify_unpatch_roundtrip(ops, cuda):
+    Lm, Lc, D, H, W, ph, pw = 2, 5, 3, 4, 6, 2, 2
+    g = torch.Generator().manual_seed(0)
+    motion = torch.randn(Lm, D, H, W, generator=g)
+    z = torch.randn(Lc - Lm, D, H, W, generator=g)
+    ref = torch.randn(D, H, W, generator=g)
+    F = (2 * D + 1) * ph * pw
+    ldo = 32
+    T = (H // ph) * (W // pw)
+    out = torch.empty(Lc * T, ldo, dtype=torch.bfloat16, device=cuda)
+    ops.patchify(motion.to(cuda), z.to(cuda), ref.to(cuda), Lm, Lc, D, H, W, ph, pw, out)
+    # numpy reference of Eq.1 + patchify
+    zn = torch.cat([motion, z]).numpy()
+    mask = np.zeros((Lc, 1, H, W))
+    mask[0] = 1
+    cond = np.zeros((Lc, D, H, W))
+    cond[0] = ref.numpy()
+    st = np.concatenate([zn, mask, cond], axis=1)  # (Lc, C, H, W)
+    C_ = st.shape[1]
+    tok = st.reshape(Lc, C_, H // ph, ph, W // pw, pw).transpose(0, 2, 4, 1, 3, 5).reshape(Lc * T, C_ * ph * pw)
+    got = out.float().cpu().numpy()
+    assert np.allclose(got[:, :F], tok.astype(np.float32), atol=2e-2, rtol=1e-2)
+    assert np.all(got[:, F:] == 0)
+    # unpatch: x0 tokens -> frames, with DDIM update
+    x0t = torch.randn(Lc * T, 16, generator=g).to(cuda)
+    zs = torch.randn(Lc - Lm, D, H, W, generator=g).to(cuda)
+    z0 = zs.clone()
+    x0o = torch.empty(Lc - Lm, D, H, W, device=cuda)
+    ops.unpatch_ddim(x0t[:, :D * ph * pw], Lm, Lc, D, H, W, ph, pw, zs, x0o, coeffs=(0.25, 0.75, 0.5, 0.5))
+    xt = x0t[:, :D * ph * pw].cpu().numpy().reshape(Lc, H // ph, W // pw, D, ph, pw)
+    frames = xt.transpose(0, 3, 1, 4, 2, 5).reshape(Lc, D, H, W)[Lm:]
+    assert np.allclose(x0o.cpu().numpy(), frames, atol=1e-6)
+    eps = (z0.cpu().numpy() - 0.25 * frames) / 0.75
+    assert np.allclose(zs.cpu().numpy(), 0.5 * frames + 0.5 * eps, atol=1e-5)
+
+
+def test_fill_normal_statistics(ops, cuda):
+    t = torch.empty(1 << 22, device=cuda, dtype=torch.bfloat16)
+    ops.fill_normal_(t, 1234, 1.0)
+    x = t.float()
+    assert abs(float(x.mean())) < 5e-3 and abs(float(x.std()) - 1) < 5e-3
+    t2 = torch.empty_like(t)
+    ops.fill_normal_(t2, 1234, 1.0)
+    assert torch.equal(t, t2)
