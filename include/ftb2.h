@@ -133,6 +133,9 @@ int ftb_unpatch_ddim(const float* x0_tok, int64_t ldx, int32_t Lm, int32_t Lc, i
 int ftb_codec_decode(const float* latents, const float* Q, float* frames, int32_t n, int32_t D,
                      void* stream);
 
+/* out[l][f][j] = a[f][j] + b[l][j], l < Lb, f < F, j < n (AdaLN tables). */
+int ftb_add_bcast_f32(const float* a, int64_t F, int64_t n, const float* b, int64_t Lb, float* out, void* stream);
+
 /* Counter-based N(0,1)*scale fill (synthetic random-init weights at 14B shape). */
 int ftb_fill_normal_bf16(void* out, int64_t n, uint64_t seed, float scale, void* stream);
 int ftb_fill_normal_f32(float* out, int64_t n, uint64_t seed, float scale, void* stream);

@@ -50,6 +50,7 @@ _SIGS = {
     "ftb_fill_normal_bf16": ([vp, i64, u64, f32, vp], i32),
     "ftb_fill_normal_f32": ([vp, i64, u64, f32, vp], i32),
     "ftb_count_nonfinite": ([vp, i64, vp, vp], i32),
+    "ftb_add_bcast_f32": ([vp, i64, i64, vp, i64, vp, vp], i32),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -259,13 +259,15 @@ __global__ void __launch_bounds__(256, 1)
 
 // ============================================================ short-KV CUDA-core kernel
 // grid (ceil(Lq/16), heads), 128 threads: warp w owns query rows 4w..4w+3 of the block.
-template <int HD>
+// HDMAX bounds the shared-memory tile; the head width itself is runtime (any hd <= HDMAX).
+template <int HDMAX>
 __global__ void __launch_bounds__(128) attn_small_kernel(const AttnParams p) {
+  const int HD = p.hd;
   constexpr int TK = 32;  // one key per lane per tile
-  constexpr int DPL = (HD + 31) / 32;
-  __shared__ float Ks[TK][HD + 1];
-  __shared__ float Vs[TK][HD];
-  __shared__ float Qs[16][HD];
+  constexpr int DPL = (HDMAX + 31) / 32;
+  __shared__ float Ks[TK][HDMAX + 1];
+  __shared__ float Vs[TK][HDMAX];
+  __shared__ float Qs[16][HDMAX];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y;
   const int r0 = blockIdx.x * 16;
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(128) attn_small_kernel(const AttnParams p) {
     for (int r = 0; r < 4; ++r) {
       const int lr = warp * 4 + r;
       float s0 = 0.f;
-#pragma unroll 8
+#pragma unroll 4
       for (int d = 0; d < HD; ++d) s0 += Qs[lr][d] * Ks[lane][d];
       s0 = (lane < nk) ? s0 * p.scale_log2 : -INFINITY;
       float mx = s0;
@@ -365,10 +367,10 @@ static int launch_fmha(const AttnParams& p, cudaStream_t s) {
   return check_launch("fmha_tc_kernel");
 }
 
-template <int HD>
+template <int HDMAX>
 static int launch_small(const AttnParams& p, cudaStream_t s) {
   dim3 grid((p.Lq + 15) / 16, p.heads);
-  attn_small_kernel<HD><<<grid, 128, 0, s>>>(p);
+  attn_small_kernel<HDMAX><<<grid, 128, 0, s>>>(p);
   return check_launch("attn_small_kernel");
 }
 
@@ -391,14 +393,11 @@ extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, cons
     if (head_dim == 64) return launch_fmha<64>(p, s);
     return set_error(FTB_EINVAL, "fmha: head_dim must be 64 or 128");
   }
-  switch (head_dim) {
-    case 8: return launch_small<8>(p, s);
-    case 16: return launch_small<16>(p, s);
-    case 32: return launch_small<32>(p, s);
-    case 64: return launch_small<64>(p, s);
-    case 128: return launch_small<128>(p, s);
-    default: return set_error(FTB_EINVAL, "attention: head_dim must be one of 8,16,32,64,128");
-  }
+  if (head_dim <= 16) return launch_small<16>(p, s);
+  if (head_dim <= 32) return launch_small<32>(p, s);
+  if (head_dim <= 64) return launch_small<64>(p, s);
+  if (head_dim <= 128) return launch_small<128>(p, s);
+  return set_error(FTB_EINVAL, "attention: head_dim must be <= 128");
 }
 
 extern "C" int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,

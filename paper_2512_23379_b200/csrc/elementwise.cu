@@ -188,6 +188,17 @@ __global__ void count_nonfinite_kernel(const float* __restrict__ x, long long n,
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// out[l][f][j] = a[f][j] + b[l][j]  (per-frame AdaLN vectors + per-layer learned offsets)
+__global__ void add_bcast_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out,
+                                 long long F, long long n, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long j = i % n;
+    const long long lf = i / n;
+    const long long f = lf % F, l = lf / F;
+    out[i] = a[f * n + j] + b[l * n + j];
+  }
+}
+
 static inline int grid_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   long long cap = (long long)sm_count() * 8;
@@ -287,4 +298,12 @@ extern "C" int ftb_count_nonfinite(const float* x, int64_t n, int32_t* out, void
   if (n <= 0) return FTB_OK;
   count_nonfinite_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(x, n, out);
   return check_launch("count_nonfinite_kernel");
+}
+
+extern "C" int ftb_add_bcast_f32(const float* a, int64_t F, int64_t n, const float* b, int64_t Lb, float* out,
+                                 void* stream) {
+  if (!a || !b || !out || F <= 0 || n <= 0 || Lb <= 0) return set_error(FTB_EINVAL, "add_bcast: bad arguments");
+  long long total = (long long)Lb * F * n;
+  add_bcast_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(a, b, out, F, n, total);
+  return check_launch("add_bcast_kernel");
 }

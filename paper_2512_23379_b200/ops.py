@@ -51,7 +51,7 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
     if M is None:
         M, K = a.shape
         lda = _ld(a)
-    if K != Kw:
+    if K > Kw or (K != Kw and (Kw - K) >= 8):
         raise ConfigError("gemm: K mismatch %d vs %d" % (K, Kw))
     k = KINDS[kind]
     ldc = 0 if k == A.EPI_QKV_ROPE else _ld(out)
@@ -156,3 +156,11 @@ def fill_normal_(t, seed, scale=1.0, stream=None):
 def count_nonfinite(x, flag, stream=None):
     A.call("ftb_count_nonfinite", A.ptr(x), x.numel(), A.ptr(flag), A.stream_ptr(stream))
     return flag
+
+
+def add_bcast(a, b, out, stream=None):
+    """out[l, f, :] = a[f, :] + b[l, :]"""
+    F, n = a.shape
+    Lb = b.shape[0]
+    A.call("ftb_add_bcast_f32", A.ptr(a), F, n, A.ptr(b), Lb, A.ptr(out), A.stream_ptr(stream))
+    return out

@@ -107,3 +107,22 @@ def test_rollout_and_decode_pinned(golden):
 def test_windows_exact(golden, lc, lm):
     wins = np.stack([O.window(golden["w_signal"], c, lc, lm) for c in range(4)])
     assert np.array_equal(wins, golden["w_%d_%d" % (lc, lm)])
+
+
+@pytest.mark.parametrize("name", list(CFGS))
+def test_product_param_init_matches_reference(golden, name):
+    """The product ParamStore.init reproduces the reference init bit for bit."""
+    from paper_2512_23379_b200.config import NetConfig
+    from paper_2512_23379_b200.net import ParamStore
+    _, m, layers, ff, d, seed = CFGS[name]
+    heads = CFGS[name][0]["heads"]
+    st = ParamStore.init(NetConfig(m, layers, heads, ff, d), seed)
+    assert st.checksum() == str(golden["p_%s_checksum" % name])
+
+
+@pytest.mark.parametrize("steps", [4, 2, 1])
+def test_product_chunk_noise_bit_exact(golden, steps):
+    """Initial sampler noise: the product's host draw is the reference's draw."""
+    from paper_2512_23379_b200.seeding import chunk_noise
+    z = chunk_noise(5, 3, golden["s_steps%d_z" % steps][0].shape)
+    assert np.array_equal(z, golden["s_steps%d_z" % steps][0])
