@@ -1,0 +1,399 @@
+"""Chunked streaming engine on the B200 (reference `pkg/src/ftlk/streaming.py`).
+
+Same public surface as the reference: `StreamConfig`, `start_stream`,
+`StreamSession.push_signal / next_frames / stats / persistent_state_nbytes /
+close`, `EmittedFrame`, `StreamStats`, plus the synchronous twin `generate`
+(reference `metrics.rollout_stream`, metrics.py:128-149).
+
+Geometry is the reference's, bit-exact (streaming.py:246-306):
+  chunk c is ready once (c+1)*S driving samples arrived (S = L_c - L_m);
+  window = samples[c*S - L_m, c*S - L_m + L_c), indices < 0 read 0.0;
+  pending samples below (c+1)*S - L_m are pruned;
+  noise = rng_for(seed, STREAM_NOISE, c) drawn on the host;
+  motion <- last L_m latent frames of [motion; x0]; cold start = L_m copies
+  of the encoded reference; emitted frame index = c * frames_per_chunk + j.
+
+Execution: three host threads as in the reference, but the denoise stage
+runs the whole 4-step ladder on a dedicated CUDA stream (device-resident
+weights, motion cache and sampler state) and hands the chunk's target latents
+to the decode stage through a CUDA event; the decode stage decodes on its own
+stream (orthogonal codec or the causal VAE), copies frames to pinned host
+memory and emits them, so decoding chunk n overlaps denoising chunk n+1.
+"""
+
+import collections
+import queue
+import sys
+import threading
+import time
+import types
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .config import PACING_MODES, SamplerPlan, StreamConfig  # noqa: F401
+from .errors import ConfigError
+from .net import device_runner
+from .seeding import chunk_noise
+
+_RECENT = 64
+_CYCLE_KEYS = ("signal_ms", "denoise_ms", "decode_ms", "motion_encode_ms", "misc_ms")
+
+
+@dataclass
+class StreamStats:
+    startup_ms: float
+    fps: float
+    frames_emitted: int
+    chunks_emitted: int
+    generate_ms: float
+    cycle: dict
+
+
+@dataclass
+class EmittedFrame:
+    index: int
+    chunk: int
+    state: np.ndarray
+
+
+def chunk_window(get, c, chunk_len, motion_len):
+    """Indices and values of chunk c's driving window (streaming.py:262-264)."""
+    stride = chunk_len - motion_len
+    lo = c * stride - motion_len
+    idx = list(range(lo, lo + chunk_len))
+    return idx, [get(j) if j >= 0 else None for j in idx]
+
+
+class DeviceStreamer:
+    """Device state of one stream: denoiser at the stream geometry, motion
+    cache, sampler state, and the codec. Used by StreamSession and generate()."""
+
+    def __init__(self, runner, cfg: StreamConfig, codec, reference_latent, latent_hw=(1, 1)):
+        self.runner, self.scfg, self.codec = runner, cfg, codec
+        self.ncfg = runner.cfg
+        self.dev = runner.device
+        self.d = runner.denoiser(cfg.chunk_len, cfg.motion_len, latent_hw)
+        d = self.d
+        self.fshape = (self.ncfg.latent_dim, d.H, d.W)
+        self.ref_host = np.asarray(reference_latent, dtype=np.float64).reshape(
+            self.fshape if self.ncfg.mode == "wan" else (self.ncfg.latent_dim,))
+        self.ref = torch.as_tensor(self.ref_host.reshape(self.fshape), dtype=torch.float32).to(self.dev)
+        lm = cfg.motion_len
+        self.motion = self.ref.unsqueeze(0).repeat(lm, 1, 1, 1).contiguous() if lm else None
+        nt = cfg.stride
+        self.z = torch.empty((nt,) + self.fshape, dtype=torch.float32, device=self.dev)
+        self.noise_host = torch.empty((nt,) + self.fshape, dtype=torch.float32).pin_memory()
+        self.slots = [torch.empty((nt,) + self.fshape, dtype=torch.float32, device=self.dev) for _ in range(4)]
+        self.slot = 0
+
+    def reset(self):
+        lm = self.scfg.motion_len
+        if lm:
+            self.motion.copy_(self.ref.unsqueeze(0).expand(lm, *self.fshape))
+
+    def denoise_chunk(self, c, window, noise=None):
+        """Runs chunk c on the current stream; returns the device x0 slot
+        (targets). `noise` (host f64) defaults to the reference draw."""
+        cfg = self.scfg
+        nt = cfg.stride
+        if noise is None:
+            noise = chunk_noise(cfg.seed, c, (nt,) + self.ref_host.shape)
+        self.noise_host.copy_(torch.from_numpy(np.asarray(noise, dtype=np.float32).reshape(self.noise_host.shape)))
+        self.z.copy_(self.noise_host, non_blocking=True)
+        self.d.prepare_cond(window, self.ref_host)
+        x0 = self.slots[self.slot]
+        self.slot = (self.slot + 1) % len(self.slots)
+        self.d.sample(self.motion, self.ref, self.z, cfg.sampler, x0)
+        lm = cfg.motion_len
+        if lm:
+            if lm <= nt:
+                self.motion.copy_(x0[nt - lm:])
+            else:  # carried rows still include older motion rows
+                keep = lm - nt
+                self.motion.copy_(torch.cat([self.motion[lm - keep:], x0], 0))
+        return x0
+
+
+class StreamSession:
+    """One live stream; command it from a single controller thread."""
+
+    def __init__(self, store, net_cfg, codec, reference_frame, cfg: StreamConfig, *, device="cuda",
+                 reference_latent=None, latent_hw=(1, 1)):
+        self.cfg = cfg
+        self.codec = codec
+        runner = device_runner(net_cfg, store, device)
+        if reference_latent is None:
+            reference_frame = np.asarray(reference_frame, dtype=np.float64)
+            if net_cfg.mode == "ftlk" and reference_frame.shape != (net_cfg.latent_dim,):
+                raise ConfigError("reference frame dimension does not match the net")
+            reference_latent = codec.encode(reference_frame[None])[0]
+        self._reference = np.asarray(reference_latent, dtype=np.float64)
+        self._ds = DeviceStreamer(runner, cfg, codec, self._reference, latent_hw)
+        self._sample_is_array = net_cfg.mode == "wan"
+        self._pending = {}
+        self._next_sample = 0
+        self._next_window = 0
+        self._inbox = queue.Queue()
+        self._to_denoise = queue.Queue(maxsize=2)
+        self._to_decode = queue.Queue(maxsize=2)
+        self._out = collections.deque()
+        self._out_cond = threading.Condition()
+        self._lock = threading.Lock()
+        self._closed = threading.Event()
+        self._error = None
+        self._t_start = time.perf_counter()
+        self._startup_ms = -1.0
+        self._last_emit_t = -1.0
+        self._cycle_ring = np.zeros(_RECENT)
+        self._cycle_count = 0
+        self._frames_emitted = 0
+        self._chunks_emitted = 0
+        self._last_generate_ms = 0.0
+        self._last_cycle = {k: 0.0 for k in _CYCLE_KEYS}
+        self._denoise_stream = torch.cuda.Stream(device=runner.device)
+        self._decode_stream = torch.cuda.Stream(device=runner.device)
+        self._workers = [
+            threading.Thread(target=self._ingest_loop, daemon=True, name="ftb-ingest"),
+            threading.Thread(target=self._denoise_loop, daemon=True, name="ftb-denoise"),
+            threading.Thread(target=self._decode_loop, daemon=True, name="ftb-decode"),
+        ]
+        for w in self._workers:
+            w.start()
+
+    # ---------------------------------------------------------------- controller API
+    def push_signal(self, samples) -> int:
+        if self._closed.is_set():
+            raise ConfigError("session is closed")
+        self._raise_pending_error()
+        batch = []
+        for i, v in samples:
+            i = int(i)
+            if i != self._next_sample:
+                raise ConfigError("driving sample index %d out of order (expected %d)" % (i, self._next_sample))
+            v = np.asarray(v, dtype=np.float64) if self._sample_is_array else float(v)
+            if not np.all(np.isfinite(v)):
+                raise ConfigError("driving sample %d is not finite" % i)
+            batch.append((i, v))
+            self._next_sample += 1
+        self._inbox.put(batch)
+        return len(batch)
+
+    def next_frames(self, wait: bool = False, timeout: float = 0.05):
+        self._raise_pending_error()
+        with self._out_cond:
+            if wait and not self._out and not self._closed.is_set():
+                self._out_cond.wait(timeout)
+            frames = list(self._out)
+            self._out.clear()
+        self._raise_pending_error()
+        return frames, self.stats()
+
+    def stats(self) -> StreamStats:
+        with self._lock:
+            n = min(self._cycle_count, _RECENT)
+            mean_cycle = float(np.mean(self._cycle_ring[:n])) if n else 0.0
+            fpc = self.frames_per_chunk
+            fps = (fpc * 1000.0 / mean_cycle) if mean_cycle > 0 else 0.0
+            return StreamStats(max(self._startup_ms, 0.0), fps, self._frames_emitted, self._chunks_emitted,
+                               self._last_generate_ms, dict(self._last_cycle))
+
+    @property
+    def frames_per_chunk(self):
+        return self.cfg.stride * getattr(self.codec, "frames_per_latent", 1)
+
+    def persistent_state_nbytes(self) -> int:
+        for _ in range(50):
+            try:
+                return _deep_nbytes(self.__dict__)
+            except RuntimeError:
+                time.sleep(0.002)
+        return _deep_nbytes(self.__dict__)
+
+    def close(self) -> None:
+        if self._closed.is_set():
+            return
+        self._closed.set()
+        self._inbox.put(None)
+        with self._out_cond:
+            self._out_cond.notify_all()
+        for w in self._workers:
+            w.join(timeout=10.0)
+
+    # ---------------------------------------------------------------- workers
+    def _fail(self, exc):
+        self._error = exc
+        self._closed.set()
+        with self._out_cond:
+            self._out_cond.notify_all()
+
+    def _raise_pending_error(self):
+        if self._error is not None:
+            raise self._error
+
+    def _ingest_loop(self):
+        cfg = self.cfg
+        received = 0
+        zero = None
+        try:
+            while not self._closed.is_set():
+                batch = self._inbox.get()
+                if batch is None:
+                    break
+                t0 = time.perf_counter()
+                for i, v in batch:
+                    self._pending[i] = v
+                    if zero is None:
+                        zero = np.zeros_like(v) if isinstance(v, np.ndarray) else 0.0
+                received += len(batch)
+                signal_ms = (time.perf_counter() - t0) * 1000.0
+                while received >= (self._next_window + 1) * cfg.stride:
+                    c = self._next_window
+                    t1 = time.perf_counter()
+                    _, vals = chunk_window(lambda j: self._pending.get(j, zero), c, cfg.chunk_len, cfg.motion_len)
+                    window = np.array([zero if v is None else v for v in vals], dtype=np.float64)
+                    keep_from = (c + 1) * cfg.stride - cfg.motion_len
+                    self._pending = {j: v for j, v in self._pending.items() if j >= keep_from}
+                    self._next_window += 1
+                    noise = chunk_noise(cfg.seed, c, (cfg.stride,) + self._reference.shape)
+                    signal_ms += (time.perf_counter() - t1) * 1000.0
+                    t_origin = time.perf_counter() - signal_ms / 1000.0
+                    self._to_denoise.put((c, window, noise, signal_ms, t_origin))
+                    signal_ms = 0.0
+        except Exception as exc:  # noqa: BLE001
+            self._fail(exc)
+        finally:
+            self._to_denoise.put(None)
+
+    def _denoise_loop(self):
+        try:
+            with torch.cuda.device(self._ds.dev), torch.cuda.stream(self._denoise_stream):
+                self._ds.d.stream = self._denoise_stream
+                while True:
+                    item = self._to_denoise.get()
+                    if item is None:
+                        break
+                    c, window, noise, signal_ms, t_ready = item
+                    t0 = time.perf_counter()
+                    x0 = self._ds.denoise_chunk(c, window, noise)
+                    ev = torch.cuda.Event()
+                    ev.record(self._denoise_stream)
+                    ev.synchronize()
+                    denoise_ms = (time.perf_counter() - t0) * 1000.0
+                    self._to_decode.put((c, x0, ev, signal_ms, denoise_ms, 0.0, t_ready))
+        except Exception as exc:  # noqa: BLE001
+            self._fail(exc)
+        finally:
+            self._to_decode.put(None)
+
+    def _decode_loop(self):
+        cfg = self.cfg
+        chunk_period = self.frames_per_chunk / cfg.target_fps
+        next_due = None
+        try:
+            with torch.cuda.device(self._ds.dev), torch.cuda.stream(self._decode_stream):
+                while True:
+                    item = self._to_decode.get()
+                    if item is None:
+                        break
+                    c, x0, ev, signal_ms, denoise_ms, motion_ms, t_ready = item
+                    if cfg.pacing == "realtime":
+                        now = time.perf_counter()
+                        if next_due is None:
+                            next_due = now
+                        if next_due > now:
+                            time.sleep(next_due - now)
+                        next_due += chunk_period
+                    t0 = time.perf_counter()
+                    self._decode_stream.wait_event(ev)
+                    frames = self.codec.decode_device(x0, self._decode_stream)
+                    decode_ms = (time.perf_counter() - t0) * 1000.0
+                    fpc = len(frames)
+                    emitted = [EmittedFrame(c * fpc + j, c, frames[j]) for j in range(fpc)]
+                    t_emit = time.perf_counter()
+                    total_ms = (t_emit - t_ready) * 1000.0
+                    misc_ms = max(0.0, total_ms - signal_ms - denoise_ms - decode_ms - motion_ms)
+                    with self._lock:
+                        if self._startup_ms < 0:
+                            self._startup_ms = (t_emit - self._t_start) * 1000.0
+                        if self._last_emit_t >= 0:
+                            self._cycle_ring[self._cycle_count % _RECENT] = (t_emit - self._last_emit_t) * 1000.0
+                            self._cycle_count += 1
+                        self._last_emit_t = t_emit
+                        self._frames_emitted += fpc
+                        self._chunks_emitted += 1
+                        self._last_generate_ms = denoise_ms + decode_ms
+                        self._last_cycle = {"signal_ms": signal_ms, "denoise_ms": denoise_ms,
+                                            "decode_ms": decode_ms, "motion_encode_ms": motion_ms,
+                                            "misc_ms": misc_ms}
+                    with self._out_cond:
+                        self._out.extend(emitted)
+                        self._out_cond.notify_all()
+        except Exception as exc:  # noqa: BLE001
+            self._fail(exc)
+
+
+def start_stream(store, net_cfg, codec, reference_frame, cfg: StreamConfig, **kw) -> StreamSession:
+    return StreamSession(store, net_cfg, codec, reference_frame, cfg, **kw)
+
+
+def generate(store, net_cfg, codec, reference_latent, signal, n_frames, *, cfg: StreamConfig = None,
+             device="cuda", latent_hw=(1, 1), decode=True, motion_override=None):
+    """Synchronous chunked generation with the engine's exact geometry (the
+    reference's `rollout_stream`, metrics.py:128-149). Returns
+    (targets (n_frames_latent, ...), motions per chunk, decoded frames or None).
+    `motion_override[c]` teacher-forces chunk c's motion rows (parity tests)."""
+    cfg = cfg or StreamConfig()
+    runner = device_runner(net_cfg, store, device)
+    ds = DeviceStreamer(runner, cfg, codec, reference_latent, latent_hw)
+    stride = cfg.stride
+    n_chunks = int(np.ceil(n_frames / stride))
+    signal = np.asarray(signal, dtype=np.float64)
+    zero = np.zeros(signal.shape[1:]) if signal.ndim > 1 else 0.0
+    outs, motions, frames = [], [], []
+    for c in range(n_chunks):
+        _, vals = chunk_window(lambda j: signal[j] if j < len(signal) else zero, c, cfg.chunk_len, cfg.motion_len)
+        window = np.array([zero if v is None else v for v in vals], dtype=np.float64)
+        if motion_override is not None and cfg.motion_len:
+            ds.motion.copy_(torch.as_tensor(np.asarray(motion_override[c], dtype=np.float32)).reshape(
+                ds.motion.shape))
+        motions.append(ds.motion.double().cpu().numpy().reshape((cfg.motion_len,) + ds.ref_host.shape)
+                       if cfg.motion_len else np.zeros((0,) + ds.ref_host.shape))
+        x0 = ds.denoise_chunk(c, window)
+        outs.append(x0.double().cpu().numpy().reshape((stride,) + ds.ref_host.shape))
+        if decode and codec is not None:
+            frames.append(codec.decode_device(x0, torch.cuda.current_stream()))
+    targets = np.concatenate(outs, axis=0)[:n_frames]
+    fr = np.concatenate(frames, axis=0) if frames else None
+    return targets, motions, fr
+
+
+_SIZE_OPAQUE = (type, types.ModuleType, types.FunctionType, types.MethodType, types.BuiltinFunctionType,
+                threading.Thread)
+
+
+def _deep_nbytes(obj, seen=None):
+    """Host-side deep size of the live session (streaming.py:93-120); device
+    tensors count their storage bytes so device-state growth shows too."""
+    if isinstance(obj, (int, float, complex, bool, str, bytes, type(None))):
+        return sys.getsizeof(obj)
+    if seen is None:
+        seen = set()
+    if id(obj) in seen:
+        return 0
+    seen.add(id(obj))
+    if isinstance(obj, np.ndarray):
+        return int(obj.nbytes) + sys.getsizeof(obj)
+    if isinstance(obj, torch.Tensor):
+        return int(obj.numel() * obj.element_size())
+    if isinstance(obj, _SIZE_OPAQUE) or isinstance(obj, (torch.cuda.Stream, torch.cuda.Event)):
+        return 0
+    size = sys.getsizeof(obj)
+    if isinstance(obj, dict):
+        size += sum(_deep_nbytes(k, seen) + _deep_nbytes(v, seen) for k, v in obj.items())
+    elif isinstance(obj, (list, tuple, set, frozenset, collections.deque)):
+        size += sum(_deep_nbytes(x, seen) for x in obj)
+    elif hasattr(obj, "__dict__"):
+        size += _deep_nbytes(obj.__dict__, seen)
+    return size
