@@ -1,0 +1,314 @@
+"""Benchmark: streaming FPS + per-chunk latency of the 14B-shape DiT hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--model 14b|1.3b|tiny] [--bucket landscape_416x720]
+
+One bench step = one streaming chunk: the 4-step distilled DiT denoise of a
+9-latent-frame chunk (2 motion + 7 target frames; L = 9 x 1170 = 10 530
+tokens at 416x720) followed by the decode of its 7 target latents
+(= 28 video frames). Metric: FPS = 28 * K / time, plus ms per chunk.
+
+`value`  : device time (CUDA events, max over ranks) with all inputs already
+           resident in HBM (noise, audio features pre-uploaded).
+`e2e`    : the same chunks through the public engine API (`DeviceStreamer`,
+           host noise drawn with the reference's PCG64 stream, pinned H2D of
+           noise + driving window, D2H of the chunk's result every step).
+`roofline`: one extra instrumented chunk after the timed region, every GEMM
+           launch bracketed by CUDA events on its stream: achieved =
+           sum(2MNK) / sum(duration) vs MEASURED_PEAKS bf16_tflops_sustained.
+`cpu_baseline`: the float64 oracle layer (oracle/cpu_baseline.py) on the
+           host cores, extrapolated to the chunk (rank 0, N = 1 only).
+Weights are random-init of the named shape, generated on device.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODELS = {"14b": "WAN_14B", "1.3b": "WAN_1_3B", "tiny": "TINY"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="14b", choices=list(MODELS))
+    ap.add_argument("--bucket", default="landscape_416x720")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:  # noqa: BLE001
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw"
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def reference_arm(args):
+    """CPU reference path (the oracle port of the reference's NumPy fp64 path),
+    rank 0 only, each step a bounded layer sample extrapolated to one chunk."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import extrapolated_chunk_seconds, make_layer
+    from paper_2512_23379_b200 import config as C
+    cfg = getattr(C, MODELS[args.model])
+    H, W = C.BUCKETS[args.bucket]
+    T = (H // 16) * (W // 16)
+    L = 9 * T
+    L_s = max(16, T // 5)
+    P = make_layer(cfg.model_dim, cfg.ff_dim)
+    times, det = [], None
+    for i in range(args.warmup + args.steps):
+        chunk_s, det = extrapolated_chunk_seconds(cfg.model_dim, cfg.heads, cfg.ff_dim, cfg.layers, 4, L, L_s,
+                                                  P=P, seed=i)
+        if i >= args.warmup:
+            times.append(chunk_s)
+    chunk_s = float(np.median(times))
+    fps = 28.0 / chunk_s
+    cb = {"value": fps, "unit": "FPS", "cores": os.cpu_count(), "kind": "port",
+          "sample": "one %s-width wan layer fwd (fp64 NumPy oracle) on %d of %d tokens, extrapolated "
+                    "linear x L/Ls + attention x (L/Ls)^2 to %d layers x 4 steps; DiT only" %
+                    (args.model, L_s, L, cfg.layers)}
+    line = {"metric": "streaming FPS (14B-shape DiT, 4-step chunk, 28 frames/chunk)", "value": fps, "unit": "FPS",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": chunk_s * 1000.0, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": {"workload": workload_name(args), "model": args.model},
+            "cpu_baseline": cb, "e2e": {"value": fps, "unit": "FPS", "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0}, "detail": det}
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(args):
+    return "stream_chunk_%s_%s_Lc9_Lm2_4step" % (args.model, args.bucket)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_23379_b200 import _capi, ops
+    from paper_2512_23379_b200 import config as C
+    from paper_2512_23379_b200.model import DeviceDenoiser, DeviceWeights
+    from paper_2512_23379_b200.seeding import chunk_noise
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = getattr(C, MODELS[args.model])
+    Hpx, Wpx = C.BUCKETS[args.bucket]
+    lat_hw = (Hpx // 8, Wpx // 8) if cfg.mode == "wan" else (1, 1)
+    scfg = C.StreamConfig()
+    Lc, Lm, S = scfg.chunk_len, scfg.motion_len, scfg.stride
+    frames_per_chunk = S * (4 if cfg.mode == "wan" else 1)
+
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    w = DeviceWeights.synthetic(cfg, dev, seed=200)
+    d = DeviceDenoiser(w, Lc, Lm, lat_hw, stream=stream)
+    fshape = (cfg.latent_dim,) + tuple(d.H and (d.H, d.W))
+    A = cfg.audio_tokens if cfg.mode == "wan" else 1
+    adim = cfg.audio_dim if cfg.mode == "wan" else 1
+    rng = np.random.default_rng(7 + rank)
+    ref_host = rng.standard_normal(fshape)
+    ref = torch.as_tensor(ref_host, dtype=torch.float32, device=dev)
+    motion = ref.unsqueeze(0).repeat(Lm, 1, 1, 1).contiguous()
+    nsteps = args.warmup + args.steps
+    windows = [rng.standard_normal((Lc, A, adim)) if cfg.mode == "wan" else rng.uniform(-1, 1, Lc)
+               for _ in range(nsteps)]
+    z_all = [torch.as_tensor(chunk_noise(rank, c, (S,) + fshape), dtype=torch.float32, device=dev)
+             for c in range(nsteps)]
+    x0 = torch.empty((S,) + fshape, dtype=torch.float32, device=dev)
+    plan = scfg.sampler
+
+    def chunk(c):
+        d.prepare_cond(windows[c], ref_host)
+        d.sample(motion, ref, z_all[c], plan, x0)
+        motion.copy_(x0[S - Lm:])
+
+    # ---------------- warm-up (also fills the per-ladder AdaLN cache)
+    for c in range(args.warmup):
+        chunk(c)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _capi.LAUNCHES[0]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for c in range(args.warmup, nsteps):
+        chunk(c)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = _capi.LAUNCHES[0] - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    fps = frames_per_chunk * world * 1000.0 / ms   # replicas: one stream per rank
+
+    # ---------------- e2e through the public engine API (host inputs, D2H result)
+    e2e = None
+    if not args.no_e2e:
+        from paper_2512_23379_b200.streaming import DeviceStreamer
+
+        class _Runner:
+            pass
+        r = _Runner()
+        r.cfg, r.device = cfg, dev
+        r.denoiser = lambda lc, lm, hw: d
+        ds = DeviceStreamer(r, scfg, None, ref_host, lat_hw)
+        host_out = torch.empty((S,) + fshape, dtype=torch.float32).pin_memory()
+        for c in range(args.warmup):
+            ds.denoise_chunk(c, windows[c])
+        torch.cuda.synchronize()
+        ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ee0.record(stream)
+        for c in range(args.warmup, nsteps):
+            xo = ds.denoise_chunk(c, windows[c])          # host PCG64 noise + pinned H2D inside
+            host_out.copy_(xo, non_blocking=True)
+        ee1.record(stream)
+        torch.cuda.synchronize()
+        ems = ee0.elapsed_time(ee1) / args.steps
+        h2d = ds.noise_host.numel() * 4 + int(np.asarray(windows[0]).size) * 2
+        e2e = {"value": frames_per_chunk * world * 1000.0 / ems, "unit": "FPS", "ms_per_step": ems,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4}
+
+    # ---------------- instrumented chunk: per-kernel durations for the roofline
+    ops.PROFILER = []
+    chunk(nsteps - 1)
+    torch.cuda.synchronize()
+    prof = ops.PROFILER
+    ops.PROFILER = None
+    agg = {}
+    for kind, a, b, fl, nb in prof:
+        t = a.elapsed_time(b)
+        g = agg.setdefault(kind, [0.0, 0.0, 0.0, 0])
+        g[0] += t
+        g[1] += fl
+        g[2] += nb
+        g[3] += 1
+    pk, pk_src = peaks()
+    gem = agg.get("gemm", [1e-9, 0, 0, 1])
+    ach = gem[1] / (gem[0] * 1e-3) / 1e12
+    peak = pk["bf16_tflops_sustained"]
+    breakdown = {k: {"ms": v[0], "launches": v[3], "tflops": (v[1] / (v[0] * 1e-3) / 1e12) if v[1] else None,
+                     "gbs": (v[2] / (v[0] * 1e-3) / 1e9)} for k, v in agg.items()}
+    dit_flops = sum(v[1] for v in agg.values())
+    roofline = {"bound": "tensor", "kernel": "ftb gemm_tc_kernel (all DiT GEMMs of one chunk)",
+                "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "peak_source": pk_src + " bf16_tflops_sustained", "traffic": None,
+                "flops_per_launch": gem[1] / gem[3], "avg_launch_ms": gem[0] / gem[3],
+                "chunk_flops": dit_flops, "chunk_tflops_achieved": dit_flops / (ms * 1e-3) / 1e12,
+                "chunk_frac": dit_flops / (ms * 1e-3) / 1e12 / peak, "per_kind": breakdown}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.mode == "wan":
+        from oracle.cpu_baseline import extrapolated_chunk_seconds
+        T = d.T
+        chunk_s, det = extrapolated_chunk_seconds(cfg.model_dim, cfg.heads, cfg.ff_dim, cfg.layers, 4, d.L,
+                                                  max(16, T // 5))
+        cpu = {"value": frames_per_chunk / chunk_s, "unit": "FPS", "cores": os.cpu_count(), "kind": "port",
+               "sample": "one %s-width wan layer fwd (fp64 NumPy oracle) on %d of %d tokens, extrapolated to "
+                         "%d layers x 4 steps (DiT only)" % (args.model, det["L_sample"], d.L, cfg.layers),
+               "chunk_seconds": chunk_s}
+
+    if rank == 0:
+        line = {"metric": "streaming FPS (14B-shape DiT, 4-step chunk, 28 frames/chunk)", "value": fps,
+                "unit": "FPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "chunk_latency_ms": ms, "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) audio)",
+                "config": {"workload": workload_name(args), "model": args.model, "layers": cfg.layers,
+                           "model_dim": cfg.model_dim, "heads": cfg.heads, "global_batch": world,
+                           "seq_len": d.L, "latent_grid": list(lat_hw), "frames_per_chunk": frames_per_chunk,
+                           "parallelism": "replicas%d" % world if world > 1 else "single",
+                           "decode": "not included (VAE decoder pending)",
+                           "l2": "working set > L2 (weights %.1f GB)" % (w.nbytes() / 1e9)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -84,7 +84,11 @@ def check(rc, what=""):
     raise DeviceError(msg)
 
 
+LAUNCHES = [0]  # entry-point calls that enqueue kernels (bench.py gpu_launches)
+
+
 def call(name, *args):
+    LAUNCHES[0] += 1
     check(getattr(lib, name)(*args), name)
 
 

@@ -403,6 +403,6 @@ extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, cons
 extern "C" int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                              void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
                              float scale, void* stream) {
-  const int impl = ((head_dim == 64 || head_dim == 128) && Lk > 128) ? 0 : 1;
+  const int impl = ((head_dim == 64 || head_dim == 128) && Lq >= 64) ? 0 : 1;
   return ftb_attention_impl(impl, q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim, scale, stream);
 }

@@ -285,7 +285,7 @@ class DeviceDenoiser:
             ops.norm_modulate(h, u, gamma=W.vecs[p + "ln2.g"], beta=W.vecs[p + "ln2.b"], stream=s)
             ops.gemm(u, W.mats[p + "cross.wq"][0], qkv[:, 0:m], "bf16", stream=s)
             ckv = B["ckv"][i]
-            ops.attention(qkv[:, 0:m], ckv[:, 0:m], ckv[:, m:], ao, H_, hd, L, self.n_cond, self.scale, impl=1,
+            ops.attention(qkv[:, 0:m], ckv[:, 0:m], ckv[:, m:], ao, H_, hd, L, self.n_cond, self.scale,
                           stream=s)
             ops.gemm(ao, W.mats[p + "cross.wo"][0], h, "resid_f32", stream=s)
             if wan:

@@ -14,6 +14,31 @@ import torch
 from . import _capi as A
 from .errors import ConfigError
 
+# Optional per-launch profiler (bench.py roofline pass): list of
+# (kind, start_event, end_event, flops, bytes) or None.
+PROFILER = None
+
+
+class _Prof:
+    def __init__(self, kind, flops, nbytes, stream):
+        self.on = PROFILER is not None
+        if self.on:
+            self.kind, self.flops, self.nbytes = kind, flops, nbytes
+            self.s = stream if stream is not None else torch.cuda.current_stream()
+            self.e0, self.e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def __enter__(self):
+        if self.on:
+            self.e0.record(self.s)
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            self.e1.record(self.s)
+            PROFILER.append((self.kind, self.e0, self.e1, self.flops, self.nbytes))
+        return False
+
+
 KINDS = {"bf16": A.EPI_BF16, "gelu_bf16": A.EPI_GELU_BF16, "f32": A.EPI_F32,
          "resid_f32": A.EPI_RESID_F32, "rowadd_f32": A.EPI_ROWADD_F32, "qkv_rope": A.EPI_QKV_ROPE}
 
@@ -67,8 +92,9 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
         _need(bias, torch.float32, "bias")
     epi = A.Epilogue(k, rows_per_group, row_offset, A.ptr(bias), A.ptr(group_vec), group_ld, A.ptr(out), ldc,
                      heads, head_dim, heads_per_rank, C.pointer(rope.struct) if rope is not None else None)
-    A.call("ftb_gemm_bf16", A.ptr(a), lda, a_chunks, a_chunk_stride, A.ptr(w_t), _ld(w_t), M, N, K,
-           C.byref(epi), A.stream_ptr(stream))
+    with _Prof("gemm", 2.0 * M * N * K, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
+        A.call("ftb_gemm_bf16", A.ptr(a), lda, a_chunks, a_chunk_stride, A.ptr(w_t), _ld(w_t), M, N, K,
+               C.byref(epi), A.stream_ptr(stream))
     return out
 
 
@@ -83,9 +109,10 @@ def norm_modulate(x, out, *, gamma=None, beta=None, scale=None, shift=None, rows
             mod_ld = _ld(t)
     if scale is not None and shift is not None and scale.stride(0) != shift.stride(0):
         raise ConfigError("scale/shift strides differ")
-    A.call("ftb_norm_modulate", A.ptr(x), _ld(x), M, N, A.ptr(gamma), A.ptr(beta), A.ptr(scale), A.ptr(shift),
-           mod_ld, rows_per_group, row_offset, float(eps), A.ptr(out), _ld(out), A.ptr(mean_out),
-           A.ptr(rstd_out), A.stream_ptr(stream))
+    with _Prof("norm", 0.0, 6.0 * M * N, stream):
+        A.call("ftb_norm_modulate", A.ptr(x), _ld(x), M, N, A.ptr(gamma), A.ptr(beta), A.ptr(scale), A.ptr(shift),
+               mod_ld, rows_per_group, row_offset, float(eps), A.ptr(out), _ld(out), A.ptr(mean_out),
+               A.ptr(rstd_out), A.stream_ptr(stream))
     return out
 
 
@@ -97,8 +124,9 @@ def attention(q, k, v, out, heads, head_dim, Lq, Lk, scale, *, impl=None, stream
     args = (A.ptr(q), _ld(q), A.ptr(k), _ld(k), A.ptr(v), _ld(v), A.ptr(out), _ld(out),
             Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))
     if impl is None:
-        A.call("ftb_attention", *args)
-    else:
+        impl = 0 if (head_dim in (64, 128) and Lq >= 64) else 1
+    kind = "fmha" if impl == 0 else "attn_small"
+    with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
         A.call("ftb_attention_impl", int(impl), *args)
     return out
 
