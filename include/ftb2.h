@@ -136,6 +136,31 @@ int ftb_codec_decode(const float* latents, const float* Q, float* frames, int32_
 /* out[l][f][j] = a[f][j] + b[l][j], l < Lb, f < F, j < n (AdaLN tables). */
 int ftb_add_bcast_f32(const float* a, int64_t F, int64_t n, const float* b, int64_t Lb, float* out, void* stream);
 
+/* ---------------------------------------------------------------- VAE decoder (wan mode) */
+/* Causal 3D conv as implicit GEMM (tcgen05): in bf16 [T_in][H][W][Cin] channel-last,
+ * w_t bf16 [Cout][KT*KH*KW*Cin] (k = ((dt*KH+dy)*KW+dx)*Cin + c), stride 1, spatial
+ * zero padding KH/2, KW/2; output frame t reads input frames t0+t .. t0+t+KT-1 (the
+ * caller keeps the causal cache frames in front). mode 0: out bf16 [T_out][H][W][out_ld]
+ * = acc + bias (+ resid[pix*resid_ld + n]); mode 1: time split, channel block j of
+ * Cout/2 goes to output frame 2t+j; mode 2: uint8 RGB = clamp(rint((acc+bias+1)*127.5)). */
+int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t W, int32_t Cin,
+                    const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0,
+                    const float* bias, const void* resid, int64_t resid_ld,
+                    void* out, int64_t out_ld, int32_t T_out, int32_t mode, void* stream);
+/* y = [silu](x / max(||x||_2, eps) * sqrt(C) * gamma) per pixel, channel-last bf16. */
+int ftb_rmsnorm_silu_bf16(const void* x, int64_t n_pix, int32_t C, const float* gamma, float eps,
+                          int32_t silu, void* y, void* stream);
+/* Nearest 2x spatial upsample, channel-last bf16 [T][H][W][C] -> [T][2H][2W][C]. */
+int ftb_upsample2x_bf16(const void* x, int32_t T, int32_t H, int32_t W, int32_t C, void* y, void* stream);
+/* fp32 residual-stream variants: RMS norm (+SiLU) f32 -> bf16; nearest 2x upsample f32 -> bf16.
+ * conv3d `mode` also carries flags: bit 4 = fp32 output, bit 5 = fp32 residual. */
+int ftb_rmsnorm_silu_f32(const float* x, int64_t n_pix, int32_t C, const float* gamma, float eps, int32_t silu,
+                         void* y, void* stream);
+int ftb_upsample2x_f32_bf16(const float* x, int32_t T, int32_t H, int32_t W, int32_t C, void* y, void* stream);
+/* Sampler latents f32 [T][C][H][W] -> channel-last bf16 [T][H][W][ldy]. */
+int ftb_nchw_to_nhwc_bf16(const float* x, int32_t T, int32_t C, int32_t H, int32_t W, void* y, int32_t ldy,
+                          void* stream);
+
 /* Counter-based N(0,1)*scale fill (synthetic random-init weights at 14B shape). */
 int ftb_fill_normal_bf16(void* out, int64_t n, uint64_t seed, float scale, void* stream);
 int ftb_fill_normal_f32(float* out, int64_t n, uint64_t seed, float scale, void* stream);

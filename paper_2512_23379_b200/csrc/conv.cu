@@ -1,0 +1,328 @@
+// Causal 3D convolution as an implicit GEMM on tcgen05 (wan-mode VAE decoder).
+//
+//   out[t, y, x, n] = bias[n] + sum_{dt,dy,dx,c} in[t+dt+t0, y+dy-ph, x+dx-pw, c] * W[n, (dt,dy,dx), c]
+//
+// Activations are channel-last bf16 [T][H][W][C]; the causal time padding is
+// the 2 cached frames the caller keeps in front of the current chunk's frames
+// (t0 = 0 with a KT=3 kernel reads frames t, t+1, t+2 of the padded buffer).
+// An M tile is 128 consecutive output pixels of one (t, y) row; for every tap
+// the producer issues one 4D TMA box {BK channels, 128 px, 1 row, 1 frame} at
+// the shifted coordinates — spatial zero padding is the TMA out-of-bounds
+// fill. The B operand is W^T [Cout][taps*Cin] (K-major). Same warp-specialised
+// pipeline as gemm.cu (TMA warp, single-thread MMA issuer, 4 epilogue warps,
+// double-buffered TMEM accumulators). Epilogue modes: bias (+ residual) bf16
+// store; time-split store for the temporal x2 upsample conv; RGB8 for the head.
+#include "common.cuh"
+#include "ftb_internal.h"
+
+namespace ftb {
+
+struct ConvParams {
+  int T, H, W, Cin, Cout;
+  int KT, KH, KW, t0, pad_h, pad_w;
+  int num_xt, kb_per_tap, taps;
+  const float* bias;
+  const __nv_bfloat16* resid;
+  long long resid_ld;
+  void* out;
+  long long out_ld;
+  int mode;       // 0 store, 1 time split, 2 RGB8
+  int out_f32;    // mode bit 4: fp32 output
+  int resid_f32;  // mode bit 5: fp32 residual
+};
+
+template <int BN, int BK>
+struct ConvCfg {
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 4u;  // SW128 / SW64
+  static constexpr uint32_t SBO = 8 * BK * 2;               // 8 rows of one swizzle atom
+};
+
+__device__ __forceinline__ void conv_epilogue(const ConvParams& p, int t, int y, int x, int gc0, float (&v)[32]) {
+  const bool full = gc0 + 32 <= p.Cout;
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (full || gc0 + j < p.Cout) v[j] += __ldg(p.bias + gc0 + j);
+  }
+  const long long pix = ((long long)t * p.H + y) * p.W + x;
+  if (p.mode == 2) {  // RGB8 head: frames in [-1, 1] -> uint8
+    uint8_t* o = reinterpret_cast<uint8_t*>(p.out) + pix * p.out_ld;
+    for (int j = 0; j < 32 && gc0 + j < p.Cout; ++j) {
+      float f = rintf((v[j] + 1.f) * 127.5f);
+      f = fminf(fmaxf(f, 0.f), 255.f);
+      o[gc0 + j] = (uint8_t)f;
+    }
+    return;
+  }
+  long long dst = pix;
+  int c0 = gc0;
+  if (p.mode == 1) {  // time split: channel block j of width Cout/2 -> output frame 2t + j
+    const int half = p.Cout >> 1;
+    const int j = gc0 / half;
+    c0 = gc0 - j * half;
+    dst = ((long long)(2 * t + j) * p.H + y) * p.W + x;
+  }
+  if (p.resid && p.resid_f32) {
+    const float4* r = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.resid) + pix * p.resid_ld + gc0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 f = r[q];
+      v[4 * q] += f.x;
+      v[4 * q + 1] += f.y;
+      v[4 * q + 2] += f.z;
+      v[4 * q + 3] += f.w;
+    }
+  } else if (p.resid) {
+    const __nv_bfloat16* r = p.resid + pix * p.resid_ld + gc0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 w = *reinterpret_cast<const uint4*>(r + 8 * q);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(h2[e]);
+        v[8 * q + 2 * e] += f.x;
+        v[8 * q + 2 * e + 1] += f.y;
+      }
+    }
+  }
+  if (p.out_f32) {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + dst * p.out_ld + c0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return;
+  }
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + dst * p.out_ld + c0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 w;
+    w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+    w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+    w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+    w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+    reinterpret_cast<uint4*>(o)[q] = w;
+  }
+}
+
+template <int BN, int BK>
+__global__ void __launch_bounds__(256, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const ConvParams p) {
+  using C = ConvCfg<BN, BK>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int num_m = p.T * p.H * p.num_xt;
+  const int num_n = (p.Cout + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = p.taps * p.kb_per_tap;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+        const int xt = m_blk % p.num_xt;
+        const int ty = m_blk / p.num_xt;
+        const int y = ty % p.H, t = ty / p.H;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int tap = kb / p.kb_per_tap, cb = kb - tap * p.kb_per_tap;
+          const int dx = tap % p.KW, dy = (tap / p.KW) % p.KH, dt = tap / (p.KW * p.KH);
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          tma_load_4d(sa, &tmA, &full_bar[stage], cb * BK, xt * 128 + dx - p.pad_w, y + dy - p.pad_h, t + dt + p.t0);
+          tma_load_2d(sb, &tmB, &full_bar[stage], tap * p.Cin + cb * BK, n_blk * BN);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16_ss(tmem_d, sdesc(sa + k * 32, 16, C::SBO, C::LAYOUT), sdesc(sb + k * 32, 16, C::SBO, C::LAYOUT),
+                        idesc, (kb | k) ? 1u : 0u);
+          mma_commit(&empty_bar[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+      const int xt = m_blk % p.num_xt;
+      const int ty = m_blk / p.num_xt;
+      const int y = ty % p.H, t = ty / p.H;
+      const int x = xt * 128 + q * 32 + lane;
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int gc0 = n_blk * BN + c0;
+        if (gc0 >= p.Cout) break;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (x < p.W) conv_epilogue(p, t, y, x, gc0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+template <int BN, int BK>
+static int launch_conv(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s) {
+  using C = ConvCfg<BN, BK>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<BN, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "conv smem attribute");
+    configured = true;
+  }
+  CUtensorMap ta, tb;
+  {
+    uint64_t dims[4] = {(uint64_t)p.Cin, (uint64_t)p.W, (uint64_t)p.H, (uint64_t)T_in};
+    uint64_t strides[3] = {(uint64_t)p.Cin * 2, (uint64_t)p.W * p.Cin * 2, (uint64_t)p.H * p.W * p.Cin * 2};
+    uint32_t box[4] = {BK, 128, 1, 1};
+    int rc = make_tmap_bf16(&ta, in, 4, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  {
+    const long long ktot = (long long)p.taps * p.Cin;
+    uint64_t dims[2] = {(uint64_t)ktot, (uint64_t)p.Cout};
+    uint64_t strides[1] = {(uint64_t)ktot * 2};
+    uint32_t box[2] = {BK, BN};
+    int rc = make_tmap_bf16(&tb, w_t, 2, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  const int tiles = p.T * p.H * p.num_xt * ((p.Cout + BN - 1) / BN);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  conv_tc_kernel<BN, BK><<<grid, 256, C::SMEM, s>>>(ta, tb, p);
+  return check_launch("conv_tc_kernel");
+}
+
+}  // namespace ftb
+
+using namespace ftb;
+
+extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t W, int32_t Cin, const void* w_t,
+                               int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0, const float* bias,
+                               const void* resid, int64_t resid_ld, void* out, int64_t out_ld, int32_t T_out,
+                               int32_t mode, void* stream) {
+  if (!in || !w_t || !out || T_out <= 0 || H <= 0 || W <= 0 || Cin <= 0 || Cout <= 0)
+    return set_error(FTB_EINVAL, "conv3d: bad arguments");
+  const int out_f32 = (mode >> 4) & 1, resid_f32 = (mode >> 5) & 1;
+  mode &= 15;
+  if (Cin % 8) return set_error(FTB_EINVAL, "conv3d: Cin must be a multiple of 8");
+  if ((KH != 1 && KH != 3) || (KW != 1 && KW != 3) || KT < 1 || KT > 3)
+    return set_error(FTB_EINVAL, "conv3d: kernel must be {1..3} x {1,3} x {1,3}");
+  if (t0 < 0 || t0 + T_out - 1 + KT - 1 >= T_in) return set_error(FTB_EINVAL, "conv3d: input frames out of range");
+  if (mode != 2 && (Cout % 32)) return set_error(FTB_EINVAL, "conv3d: Cout must be a multiple of 32");
+  if (mode == 1 && (Cout % 64)) return set_error(FTB_EINVAL, "conv3d: time-split needs Cout multiple of 64");
+  if (resid && (resid_ld % 8)) return set_error(FTB_EINVAL, "conv3d: resid_ld alignment");
+  if (mode != 2 && (out_ld % 8)) return set_error(FTB_EINVAL, "conv3d: out_ld alignment");
+  ConvParams p{};
+  p.T = T_out;
+  p.H = H;
+  p.W = W;
+  p.Cin = Cin;
+  p.Cout = Cout;
+  p.KT = KT;
+  p.KH = KH;
+  p.KW = KW;
+  p.t0 = t0;
+  p.pad_h = KH / 2;
+  p.pad_w = KW / 2;
+  p.num_xt = (W + 127) / 128;
+  p.taps = KT * KH * KW;
+  p.bias = bias;
+  p.resid = reinterpret_cast<const __nv_bfloat16*>(resid);
+  p.resid_ld = resid_ld;
+  p.out = out;
+  p.out_ld = out_ld;
+  p.mode = mode;
+  p.out_f32 = out_f32;
+  p.resid_f32 = resid_f32;
+  const bool bk32 = (Cin % 64) != 0 && (Cin % 32) == 0;
+  const int BK = (Cin <= 32 || bk32) ? 32 : 64;
+  p.kb_per_tap = (Cin + BK - 1) / BK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int bn = Cout <= 32 ? 32 : (Cout == 96 ? 96 : 192);
+  if (Cout > 32 && Cout != 96 && (Cout % 192) && Cout != 64 && Cout != 128)
+    ;  // falls through to 192 tiles with a masked tail
+  if (BK == 32) {
+    if (bn == 32) return launch_conv<32, 32>(in, T_in, w_t, p, s);
+    if (bn == 96) return launch_conv<96, 32>(in, T_in, w_t, p, s);
+    return launch_conv<192, 32>(in, T_in, w_t, p, s);
+  }
+  if (bn == 32) return launch_conv<32, 64>(in, T_in, w_t, p, s);
+  if (bn == 96) return launch_conv<96, 64>(in, T_in, w_t, p, s);
+  return launch_conv<192, 64>(in, T_in, w_t, p, s);
+}

@@ -13,5 +13,5 @@ int check_launch(const char* what);
 int sm_count();
 // bf16 tensor map, SWIZZLE_128B, OOB -> zero. dims/box innermost first; strides in bytes (rank-1 entries).
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
-                   const uint32_t* box);
+                   const uint32_t* box, int swizzle_bytes = 128);
 }  // namespace ftb

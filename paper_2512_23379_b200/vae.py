@@ -1,0 +1,316 @@
+"""Causal 3D VAE decoder (wan mode), streaming with per-conv causal caches.
+
+Build-defined "Wan-2.1-shaped" decoder (PAPER.md:151 names the Wan2.1 VAE;
+the reference stands it in with an orthogonal codec, world.py:181-210):
+
+  conv_in  CausalConv3d(z -> d0, 3x3x3)
+  mid      2 x ResBlock(d0)                     (Wan's mid attention block: see DESIGN.md)
+  stage i  (num_res_blocks+1) x ResBlock(in_i -> d_{i+1});
+           i < 3: [time_conv CausalConv3d(C -> 2C, 3x1x1) -> frames x2]  (temporal_upsample[i])
+                   nearest 2x spatial upsample -> Conv2d 3x3 (C -> C/2)
+  head     RMSNorm -> SiLU -> CausalConv3d(d_last -> 3, 3x3x3) -> RGB
+  ResBlock(x) = conv2(silu(rms2(conv1(silu(rms1(x)))))) + (x | conv1x1(x))
+
+dims = base * [m_last] + base * reversed(mult) = [384, 384, 384, 192, 96] at base 96.
+Every causal conv keeps the last 2 input frames of the previous chunk as its
+cache (zeros at stream start), so decoding the chunks' target latents in
+order equals one causal decode of the whole latent stream; each latent frame
+yields 4 video frames (7 latents -> 28 frames per chunk).
+
+Device layout: channel-last bf16 activations, convs are tcgen05 implicit GEMMs
+(`ftb_conv3d_bf16`), norms/upsample are HBM-bound kernels. Weight layout on
+the host is PyTorch's Conv3d (Cout, Cin, kt, kh, kw) float64.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _capi as A
+from . import ops
+from .errors import ConfigError
+from .seeding import INIT, rng_for
+
+
+@dataclass(frozen=True)
+class VAEConfig:
+    z_dim: int = 16
+    base_dim: int = 96
+    dim_mult: tuple = (1, 2, 4, 4)
+    num_res_blocks: int = 2
+    temporal_upsample: tuple = (True, True, False)
+
+    @property
+    def dims(self):
+        m = tuple(self.dim_mult)
+        return [self.base_dim * m[-1]] + [self.base_dim * u for u in reversed(m)]
+
+    @property
+    def time_factor(self):
+        return 2 ** sum(bool(t) for t in self.temporal_upsample)
+
+    @property
+    def space_factor(self):
+        return 2 ** (len(self.dim_mult) - 1)
+
+
+def _conv(name, cin, cout, k):
+    return [(name + ".w", (cout, cin) + tuple(k)), (name + ".b", (cout,))]
+
+
+def _res(name, cin, cout):
+    s = [(name + ".norm1.g", (cin,))] + _conv(name + ".conv1", cin, cout, (3, 3, 3))
+    s += [(name + ".norm2.g", (cout,))] + _conv(name + ".conv2", cout, cout, (3, 3, 3))
+    if cin != cout:
+        s += _conv(name + ".shortcut", cin, cout, (1, 1, 1))
+    return s
+
+
+def vae_program(cfg: VAEConfig):
+    """Ordered op list: (op, name, cin, cout) with op in
+    conv_in | res | time | resample | head; plus param shapes."""
+    d = cfg.dims
+    prog = [("conv_in", "conv_in", cfg.z_dim, d[0])]
+    shapes = _conv("conv_in", cfg.z_dim, d[0], (3, 3, 3))
+    for j in range(2):
+        prog.append(("res", "mid.%d" % j, d[0], d[0]))
+        shapes += _res("mid.%d" % j, d[0], d[0])
+    n_up = len(cfg.dim_mult)
+    for i in range(n_up):
+        cin = d[i] // 2 if i > 0 else d[i]
+        cout = d[i + 1]
+        for j in range(cfg.num_res_blocks + 1):
+            nm = "up.%d.res.%d" % (i, j)
+            prog.append(("res", nm, cin, cout))
+            shapes += _res(nm, cin, cout)
+            cin = cout
+        if i != n_up - 1:
+            if cfg.temporal_upsample[i]:
+                prog.append(("time", "up.%d.time" % i, cout, 2 * cout))
+                shapes += _conv("up.%d.time" % i, cout, 2 * cout, (3, 1, 1))
+            prog.append(("resample", "up.%d.resample" % i, cout, cout // 2))
+            shapes += _conv("up.%d.resample" % i, cout, cout // 2, (1, 3, 3))
+    prog.append(("head", "head", d[-1], 3))
+    shapes += [("head.norm.g", (d[-1],))] + _conv("head.conv", d[-1], 3, (3, 3, 3))
+    return prog, shapes
+
+
+def init_vae_params(cfg: VAEConfig, seed: int) -> dict:
+    """Host float64 params: conv weights N(0,1)/sqrt(fan_in), biases 0, gains 1."""
+    rng = rng_for(seed, INIT, 1)
+    _, shapes = vae_program(cfg)
+    out = {}
+    for name, shape in shapes:
+        if name.endswith(".g"):
+            out[name] = np.ones(shape)
+        elif name.endswith(".b"):
+            out[name] = np.zeros(shape)
+        else:
+            fan_in = int(np.prod(shape[1:]))
+            out[name] = rng.standard_normal(shape) / np.sqrt(fan_in)
+    return out
+
+
+class _ConvW:
+    """Device conv weights W^T [Cout_pad][taps*Cin] bf16 + bias, and its causal cache."""
+
+    def __init__(self, w, b, device, pad_cout_to=None):
+        cout, cin, kt, kh, kw = w.shape
+        self.cin, self.cout, self.k = cin, cout, (kt, kh, kw)
+        rows = pad_cout_to or cout
+        wt = np.zeros((rows, kt * kh * kw * cin))
+        wt[:cout] = np.transpose(w, (0, 2, 3, 4, 1)).reshape(cout, -1)
+        self.wt = torch.as_tensor(wt).to(torch.bfloat16).to(device).contiguous()
+        bb = np.zeros(rows)
+        bb[:cout] = b
+        self.b = torch.as_tensor(bb, dtype=torch.float32).to(device)
+        self.cache = None
+
+    @classmethod
+    def synthetic(cls, shape, device, seed, pad_cout_to=None):
+        self = cls.__new__(cls)
+        cout, cin, kt, kh, kw = shape
+        self.cin, self.cout, self.k = cin, cout, (kt, kh, kw)
+        rows = pad_cout_to or cout
+        self.wt = torch.zeros(rows, kt * kh * kw * cin, dtype=torch.bfloat16, device=device)
+        tmp = torch.empty(cout, kt * kh * kw * cin, dtype=torch.bfloat16, device=device)
+        ops.fill_normal_(tmp, seed, 1.0 / np.sqrt(cin * kt * kh * kw))
+        self.wt[:cout] = tmp
+        self.b = torch.zeros(rows, dtype=torch.float32, device=device)
+        self.cache = None
+        return self
+
+
+class DeviceVAEDecoder:
+    """Streaming causal decoder on one device. `decode_device(z)` decodes one
+    chunk of target latents [T, z_dim, h, w] and advances the causal caches."""
+
+    def __init__(self, cfg: VAEConfig, device, params=None, seed=0, rgb8=True):
+        self.cfg = cfg
+        self.dev = torch.device(device)
+        self.prog, shapes = vae_program(cfg)
+        self.rgb8 = rgb8
+        self.frames_per_latent = cfg.time_factor
+        self.W, self.G = {}, {}
+        for idx, (name, shape) in enumerate(shapes):
+            if name.endswith(".g"):
+                g = np.ones(shape) if params is None else params[name]
+                self.G[name[:-2]] = torch.as_tensor(g, dtype=torch.float32).to(self.dev)
+            elif name.endswith(".w"):
+                base = name[:-2]
+                pad = 32 if base == "head.conv" else None
+                if params is None:
+                    self.W[base] = _ConvW.synthetic(shape, self.dev, seed * 7919 + idx, pad)
+                else:
+                    self.W[base] = _ConvW(params[name], params[base + ".b"], self.dev, pad)
+        self._geo = None
+        self._host = {}
+
+    # ------------------------------------------------------------ buffers
+    def _setup(self, T, h, w):
+        key = (T, h, w)
+        if self._geo == key:
+            return
+        self._geo = key
+        geo = [dict(T=T, H=h, W=w, C=0)]
+        ups = 1
+        for op, name, cin, cout in self.prog:
+            cur = geo[-1]
+            if op in ("conv_in", "res"):
+                cur["C"] = max(cur["C"], cin, cout)
+            elif op == "head":
+                cur["C"] = max(cur["C"], cin)
+            elif op == "time":
+                cur["C"] = max(cur["C"], cin)
+                geo.append(dict(T=2 * cur["T"], H=cur["H"], W=cur["W"], C=cin))
+            elif op == "resample":
+                cur["C"] = max(cur["C"], cin)
+                ups = max(ups, cur["T"] * 4 * cur["H"] * cur["W"] * cin)
+                geo.append(dict(T=cur["T"], H=2 * cur["H"], W=2 * cur["W"], C=cout))
+        bf, f32 = torch.bfloat16, torch.float32
+        levels = {}
+        for l, g in enumerate(geo):
+            px, C = g["T"] * g["H"] * g["W"], g["C"]
+            levels[l] = dict(g, x=torch.empty(px * C, dtype=f32, device=self.dev),      # residual stream
+                             sc=torch.empty(px * C, dtype=f32, device=self.dev),     # 1x1 shortcut
+                             h=torch.empty(px * C, dtype=bf, device=self.dev),       # conv1 output
+                             xb=torch.empty(px * C, dtype=bf, device=self.dev),      # bf16 view of x
+                             work=torch.empty((g["T"] + 2) * g["H"] * g["W"] * C, dtype=bf, device=self.dev))
+        self.levels = levels
+        self.upbuf = torch.empty(ups, dtype=bf, device=self.dev)
+        last = levels[len(geo) - 1]
+        npx = last["T"] * last["H"] * last["W"]
+        self.out_rgb = torch.empty(npx * 3, dtype=torch.uint8, device=self.dev)
+        self.out_f = torch.empty(npx * 32, dtype=f32, device=self.dev)
+        for cw in self.W.values():
+            cw.cache = None
+        self.reset()
+
+    def reset(self):
+        """Zero the causal caches (stream start)."""
+        for cw in self.W.values():
+            if cw.cache is not None:
+                cw.cache.zero_()
+
+    # ------------------------------------------------------------ primitive wrappers
+    OUT_F32, RESID_F32 = 16, 32
+
+    def _causal(self, cw, L, Cin, producer, out, out_ld, mode, resid=None, resid_ld=0, stream=None):
+        """KT=3 causal conv on level L: cache -> work[0:2], producer fills
+        work[2:], conv, last 2 input frames -> cache (for the next chunk)."""
+        T, H, W = L["T"], L["H"], L["W"]
+        fr = H * W * Cin
+        work = L["work"][:(T + 2) * fr]
+        if cw.cache is None:
+            cw.cache = torch.zeros(2 * fr, dtype=torch.bfloat16, device=self.dev)
+        work[:2 * fr].copy_(cw.cache)
+        producer(work[2 * fr:])
+        self._conv(work, T + 2, H, W, Cin, cw, out, out_ld, 0, mode, resid, resid_ld, T, stream)
+        cw.cache.copy_(work[T * fr:(T + 2) * fr])
+
+    def _conv(self, inp, T_in, H, W, Cin, cw, out, out_ld, t0, mode, resid, resid_ld, T_out, stream):
+        kt, kh, kw = cw.k
+        cout = cw.cout if (mode & 15) != 0 or cw.cout % 32 == 0 else cw.wt.shape[0]
+        with ops._Prof("conv", 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
+            A.call("ftb_conv3d_bf16", A.ptr(inp), T_in, H, W, Cin, A.ptr(cw.wt), cout, kt, kh, kw, t0,
+                   A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld, T_out, mode, A.stream_ptr(stream))
+
+    def _rms(self, x, npix, C, g, y, stream):
+        fn = "ftb_rmsnorm_silu_f32" if x.dtype == torch.float32 else "ftb_rmsnorm_silu_bf16"
+        A.call(fn, A.ptr(x), npix, C, A.ptr(g), 1e-12, 1, A.ptr(y), A.stream_ptr(stream))
+
+    # ------------------------------------------------------------ decode
+    def decode_device_tensor(self, z, stream=None):
+        """z: device f32 [T, z_dim, h, w] -> device output (uint8 [T*tf, H, W, 3] if
+        rgb8 else f32 [T*tf, H, W, 32] with channels 0..2 valid)."""
+        if z.dim() != 4 or z.shape[1] != self.cfg.z_dim:
+            raise ConfigError("VAE input must be [T, z_dim, h, w]")
+        T, _, h, w = z.shape
+        self._setup(T, h, w)
+        s = stream
+        lv = self.levels
+        F32, R32 = self.OUT_F32, self.RESID_F32
+        l = 0
+        cw = self.W["conv_in"]
+        zc = self.cfg.z_dim
+        self._causal(cw, lv[0], zc,
+                     lambda dst: A.call("ftb_nchw_to_nhwc_bf16", A.ptr(z), T, zc, h, w, A.ptr(dst), zc,
+                                        A.stream_ptr(s)),
+                     lv[0]["x"], cw.cout, F32, stream=s)
+        for op, name, cin, cout in self.prog[1:]:
+            L = lv[l]
+            T_, H_, W_ = L["T"], L["H"], L["W"]
+            npx = T_ * H_ * W_
+            x = L["x"]
+            if op == "res":
+                c1, c2 = self.W[name + ".conv1"], self.W[name + ".conv2"]
+                if cin != cout:  # 1x1 shortcut of the block input
+                    ops.cast_f32_bf16(x[:npx * cin], L["xb"][:npx * cin], stream=s)
+                    self._conv(L["xb"], T_, H_, W_, cin, self.W[name + ".shortcut"], L["sc"], cout, 0, F32, None, 0,
+                               T_, s)
+                    resid = L["sc"]
+                else:
+                    resid = x
+                self._causal(c1, L, cin, lambda dst: self._rms(x[:npx * cin], npx, cin, self.G[name + ".norm1"],
+                                                               dst, s), L["h"], cout, 0, stream=s)
+                # conv2 updates the fp32 residual stream in place (one thread reads and writes each pixel)
+                self._causal(c2, L, cout, lambda dst: self._rms(L["h"][:npx * cout], npx, cout,
+                                                                self.G[name + ".norm2"], dst, s),
+                             x, cout, F32 | R32, resid=resid, resid_ld=cout, stream=s)
+            elif op == "time":
+                nxt = lv[l + 1]
+                self._causal(self.W[name], L, cin, lambda dst: ops.cast_f32_bf16(x[:npx * cin], dst, stream=s),
+                             nxt["x"], cin, 1 | F32, stream=s)
+                l += 1
+            elif op == "resample":
+                up = self.upbuf[:npx * 4 * cin]
+                A.call("ftb_upsample2x_f32_bf16", A.ptr(x), T_, H_, W_, cin, A.ptr(up), A.stream_ptr(s))
+                nxt = lv[l + 1]
+                self._conv(up, T_, 2 * H_, 2 * W_, cin, self.W[name], nxt["x"], cout, 0, F32, None, 0, T_, s)
+                l += 1
+            elif op == "head":
+                hw_ = self.W["head.conv"]
+                prod = lambda dst: self._rms(x[:npx * cin], npx, cin, self.G["head.norm"], dst, s)  # noqa: E731
+                if self.rgb8:
+                    self._causal(hw_, L, cin, prod, self.out_rgb, 3, 2, stream=s)
+                    return self.out_rgb[:npx * 3].view(T_, H_, W_, 3)
+                self._causal(hw_, L, cin, prod, self.out_f, 32, F32, stream=s)
+                return self.out_f[:npx * 32].view(T_, H_, W_, 32)
+        raise ConfigError("VAE program has no head")
+
+    def decode_device(self, z, stream):
+        """Codec interface of the streaming engine: device latents -> host frames."""
+        with torch.cuda.stream(stream):
+            out = self.decode_device_tensor(z.reshape(z.shape[0], self.cfg.z_dim, *z.shape[-2:]), stream)
+            key = tuple(out.shape) + (out.dtype,)
+            host = self._host.get(key)
+            if host is None:
+                host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+                self._host[key] = host
+            host.copy_(out, non_blocking=True)
+        stream.synchronize()
+        return host.numpy().copy() if host.dtype == torch.uint8 else host.float().numpy()
+
+    def encode(self, frames):  # pragma: no cover - encoder is out of scope
+        raise ConfigError("the VAE encoder is out of scope; pass reference_latent to start_stream")

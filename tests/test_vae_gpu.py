@@ -1,0 +1,117 @@
+"""VAE decoder kernels and the streaming causal decoder on the B200 vs the
+float64 oracle (oracle/vae_oracle.py)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import vae_oracle as VO
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def bfr(x):
+    return torch.as_tensor(x).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+CONV_CASES = [  # T_out, H, W, Cin, Cout, k
+    (3, 5, 7, 16, 32, (3, 3, 3)),
+    (2, 4, 130, 96, 96, (3, 3, 3)),
+    (2, 3, 200, 192, 384, (3, 3, 3)),
+    (3, 6, 9, 64, 128, (3, 1, 1)),
+    (2, 5, 260, 32, 64, (1, 3, 3)),
+    (2, 4, 33, 128, 64, (1, 1, 1)),
+]
+
+
+@pytest.mark.parametrize("T,H,W,Cin,Cout,k", CONV_CASES)
+def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k):
+    from paper_2512_23379_b200 import _capi as A
+    r = np.random.default_rng(T * 100 + W)
+    kt = k[0]
+    x = bfr(r.standard_normal((T + kt - 1, H, W, Cin)))
+    w = bfr(r.standard_normal((Cout, Cin) + k) / np.sqrt(Cin * np.prod(k)))
+    b = r.standard_normal(Cout)
+    resid = bfr(r.standard_normal((T, H, W, Cout)))
+    want = VO.conv3d(x, w, b) + resid
+    xd = torch.as_tensor(x).to(torch.bfloat16).to(cuda)
+    wt = torch.as_tensor(np.transpose(w, (0, 2, 3, 4, 1)).reshape(Cout, -1)).to(torch.bfloat16).to(cuda).contiguous()
+    bd = torch.as_tensor(b, dtype=torch.float32).to(cuda)
+    rd = torch.as_tensor(resid).to(torch.bfloat16).to(cuda)
+    out = torch.empty(T, H, W, Cout, dtype=torch.bfloat16, device=cuda)
+    A.call("ftb_conv3d_bf16", A.ptr(xd), T + kt - 1, H, W, Cin, A.ptr(wt), Cout, *k, 0, A.ptr(bd), A.ptr(rd),
+           Cout, A.ptr(out), Cout, T, 0, A.stream_ptr())
+    assert rel(out.float().cpu().numpy(), want) < 8e-3
+
+
+def test_conv3d_time_split_and_rgb8(cuda):
+    from paper_2512_23379_b200 import _capi as A
+    r = np.random.default_rng(5)
+    T, H, W, C = 3, 4, 6, 64
+    x = bfr(r.standard_normal((T + 2, H, W, C)))
+    w = bfr(r.standard_normal((2 * C, C, 3, 1, 1)) / 14)
+    y = VO.conv3d(x, w, np.zeros(2 * C))
+    want = np.stack([y[..., :C], y[..., C:]], 1).reshape(2 * T, H, W, C)
+    xd = torch.as_tensor(x).to(torch.bfloat16).to(cuda)
+    wt = torch.as_tensor(np.transpose(w, (0, 2, 3, 4, 1)).reshape(2 * C, -1)).to(torch.bfloat16).to(cuda)
+    out = torch.empty(2 * T, H, W, C, dtype=torch.bfloat16, device=cuda)
+    A.call("ftb_conv3d_bf16", A.ptr(xd), T + 2, H, W, C, A.ptr(wt.contiguous()), 2 * C, 3, 1, 1, 0, None, None, 0,
+           A.ptr(out), C, T, 1, A.stream_ptr())
+    assert rel(out.float().cpu().numpy(), want) < 8e-3
+    # RGB8 head: 3 output channels quantised
+    w3 = bfr(r.standard_normal((3, C, 3, 3, 3)) / 40)
+    f = VO.conv3d(x, w3, np.zeros(3))
+    wt3 = torch.zeros(32, 27 * C, dtype=torch.bfloat16)
+    wt3[:3] = torch.as_tensor(np.transpose(w3, (0, 2, 3, 4, 1)).reshape(3, -1)).to(torch.bfloat16)
+    rgb = torch.empty(T, H, W, 3, dtype=torch.uint8, device=cuda)
+    A.call("ftb_conv3d_bf16", A.ptr(xd), T + 2, H, W, C, A.ptr(wt3.to(cuda)), 3, 3, 3, 3, 0, None, None, 0,
+           A.ptr(rgb), 3, T, 2, A.stream_ptr())
+    got = rgb.cpu().numpy().astype(int)
+    assert np.abs(got - VO.to_rgb8(f).astype(int)).max() <= 1
+
+
+def test_rmsnorm_and_upsample(cuda):
+    from paper_2512_23379_b200 import _capi as A
+    r = np.random.default_rng(1)
+    x = bfr(r.standard_normal((2, 3, 5, 96)) * 3)
+    g = r.standard_normal(96)
+    xd = torch.as_tensor(x).to(torch.bfloat16).to(cuda)
+    y = torch.empty_like(xd)
+    A.call("ftb_rmsnorm_silu_bf16", A.ptr(xd), 30, 96, A.ptr(torch.as_tensor(g, dtype=torch.float32).to(cuda)),
+           1e-12, 1, A.ptr(y), A.stream_ptr())
+    assert rel(y.float().cpu().numpy(), VO.rms(x, g)) < 5e-3
+    up = torch.empty(2, 6, 10, 96, dtype=torch.bfloat16, device=cuda)
+    A.call("ftb_upsample2x_bf16", A.ptr(xd), 2, 3, 5, 96, A.ptr(up), A.stream_ptr())
+    assert np.array_equal(up.float().cpu().numpy(), x.repeat(2, 1).repeat(2, 2))
+
+
+SMALL = dict(z_dim=16, base_dim=32, dim_mult=(1, 2, 4, 4), num_res_blocks=2, temporal_upsample=(True, True, False))
+
+
+def test_streaming_vae_decoder_two_chunks(cuda):
+    from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig, init_vae_params
+    cfg = VAEConfig(**SMALL)
+    P = init_vae_params(cfg, 3)
+    Pb = {k: (bfr(v) if k.endswith(".w") else v) for k, v in P.items()}
+    orc = VO.VAEOracle(Pb, **SMALL)
+    dec = DeviceVAEDecoder(cfg, cuda, params=P, rgb8=False)
+    dec8 = DeviceVAEDecoder(cfg, cuda, params=P, rgb8=True)
+    r = np.random.default_rng(0)
+    s = torch.cuda.current_stream()
+    for chunk in range(2):
+        z = r.standard_normal((3, 16, 4, 6))
+        want = orc.decode(z)
+        zd = torch.as_tensor(z, dtype=torch.float32).to(cuda)
+        got = dec.decode_device(zd, s)[..., :3]
+        assert got.shape == want.shape == (12, 32, 48, 3)
+        e = rel(got, want)
+        print("chunk %d decode rel-L2 %.2e" % (chunk, e))
+        assert e < 1e-2
+        rgb = dec8.decode_device(zd, s)
+        assert rgb.dtype == np.uint8 and rgb.shape == (12, 32, 48, 3)
+        assert np.mean(np.abs(rgb.astype(int) - VO.to_rgb8(want).astype(int)) <= 2) > 0.99
