@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--bucket", default="landscape_416x720")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
     return ap.parse_args()
 
 
@@ -195,11 +196,17 @@ def main():
              for c in range(nsteps)]
     x0 = torch.empty((S,) + fshape, dtype=torch.float32, device=dev)
     plan = scfg.sampler
+    vae = None
+    if cfg.mode == "wan" and not args.no_decode:
+        from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig
+        vae = DeviceVAEDecoder(VAEConfig(z_dim=cfg.latent_dim), dev, params=None, seed=201, rgb8=True)
 
     def chunk(c):
         d.prepare_cond(windows[c], ref_host)
         d.sample(motion, ref, z_all[c], plan, x0)
         motion.copy_(x0[S - Lm:])
+        if vae is not None:
+            vae.decode_device_tensor(x0, stream)
 
     # ---------------- warm-up (also fills the per-ladder AdaLN cache)
     for c in range(args.warmup):
@@ -236,22 +243,31 @@ def main():
         r = _Runner()
         r.cfg, r.device = cfg, dev
         r.denoiser = lambda lc, lm, hw: d
-        ds = DeviceStreamer(r, scfg, None, ref_host, lat_hw)
+        ds = DeviceStreamer(r, scfg, vae, ref_host, lat_hw)
         host_out = torch.empty((S,) + fshape, dtype=torch.float32).pin_memory()
+        d2h = [0]
+
+        def e2e_chunk(c):
+            xo = ds.denoise_chunk(c, windows[c])          # host PCG64 noise + pinned H2D inside
+            if vae is not None:
+                frames = vae.decode_device(xo, stream)    # decoded uint8 frames -> pinned host
+                d2h[0] = frames.nbytes
+            else:
+                host_out.copy_(xo, non_blocking=True)
+                d2h[0] = host_out.numel() * 4
         for c in range(args.warmup):
-            ds.denoise_chunk(c, windows[c])
+            e2e_chunk(c)
         torch.cuda.synchronize()
         ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ee0.record(stream)
         for c in range(args.warmup, nsteps):
-            xo = ds.denoise_chunk(c, windows[c])          # host PCG64 noise + pinned H2D inside
-            host_out.copy_(xo, non_blocking=True)
+            e2e_chunk(c)
         ee1.record(stream)
         torch.cuda.synchronize()
         ems = ee0.elapsed_time(ee1) / args.steps
         h2d = ds.noise_host.numel() * 4 + int(np.asarray(windows[0]).size) * 2
         e2e = {"value": frames_per_chunk * world * 1000.0 / ems, "unit": "FPS", "ms_per_step": ems,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": host_out.numel() * 4}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0]}
 
     # ---------------- instrumented chunk: per-kernel durations for the roofline
     ops.PROFILER = []
@@ -269,6 +285,7 @@ def main():
         g[3] += 1
     pk, pk_src = peaks()
     gem = agg.get("gemm", [1e-9, 0, 0, 1])
+    conv = agg.get("conv", [1e-9, 0, 0, 1])
     ach = gem[1] / (gem[0] * 1e-3) / 1e12
     peak = pk["bf16_tflops_sustained"]
     breakdown = {k: {"ms": v[0], "launches": v[3], "tflops": (v[1] / (v[0] * 1e-3) / 1e12) if v[1] else None,
@@ -279,7 +296,8 @@ def main():
                 "peak_source": pk_src + " bf16_tflops_sustained", "traffic": None,
                 "flops_per_launch": gem[1] / gem[3], "avg_launch_ms": gem[0] / gem[3],
                 "chunk_flops": dit_flops, "chunk_tflops_achieved": dit_flops / (ms * 1e-3) / 1e12,
-                "chunk_frac": dit_flops / (ms * 1e-3) / 1e12 / peak, "per_kind": breakdown}
+                "chunk_frac": dit_flops / (ms * 1e-3) / 1e12 / peak, "per_kind": breakdown,
+                "vae_conv_tflops": conv[1] / (conv[0] * 1e-3) / 1e12 if conv[1] else None}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.mode == "wan":
@@ -301,7 +319,8 @@ def main():
                            "model_dim": cfg.model_dim, "heads": cfg.heads, "global_batch": world,
                            "seq_len": d.L, "latent_grid": list(lat_hw), "frames_per_chunk": frames_per_chunk,
                            "parallelism": "replicas%d" % world if world > 1 else "single",
-                           "decode": "not included (VAE decoder pending)",
+                           "decode": "causal VAE decoder, 7 latents -> 28 RGB8 frames %dx%d" % (Hpx, Wpx)
+                           if vae is not None else "none",
                            "l2": "working set > L2 (weights %.1f GB)" % (w.nbytes() / 1e9)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk}
