@@ -86,6 +86,9 @@ int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_
                   const void* B, int64_t ldb, int32_t M, int32_t N, int32_t K,
                   const ftb_epilogue* epi, void* stream);
 
+/* Kernel variant for ftb_gemm_bf16: 0 auto (CTA pair when M,N >= 256), 1 single CTA, 2 CTA pair. */
+int ftb_set_gemm_variant(int32_t variant);
+
 /* ---------------------------------------------------------------- norms */
 /* y = ((x - mean) * rstd) * (gamma?gamma:1) * (scale?1+scale[g]:1) + (beta?beta:0) + (shift?shift[g]:0)
  * rstd = 1/sqrt(var + eps), population variance; g = (row+row_offset)/rows_per_group.

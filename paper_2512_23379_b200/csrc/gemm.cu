@@ -300,6 +300,165 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
+// ------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): one 256 x 256 tile per pair, UMMA M=256, each CTA
+// stages its 128 rows of A and 128 rows of B^T (half the operand bytes of two 1-CTA
+// tiles), 6-stage ring, TMEM accumulators double-buffered (2 x 256 columns). Tiles
+// are rasterised in groups of GROUP_M m-blocks so a wave of pairs shares B in L2.
+constexpr int PAIR_STAGES = 6;
+constexpr int PAIR_A_BYTES = 128 * GEMM_BK * 2;
+constexpr int PAIR_B_BYTES = 128 * GEMM_BK * 2;
+constexpr int PAIR_STAGE_BYTES = PAIR_A_BYTES + PAIR_B_BYTES;
+constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 1024 + 256;
+constexpr int PAIR_GROUP_M = 8;
+
+__device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int& m_blk, int& n_blk) {
+  const int group = PAIR_GROUP_M * num_n;
+  const int g = tile / group;
+  const int first_m = g * PAIR_GROUP_M;
+  const int gm = min(num_m - first_m, PAIR_GROUP_M);
+  const int local = tile - g * group;
+  m_blk = first_m + local % gm;
+  n_blk = local / gm;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + PAIR_STAGES;
+  uint64_t* tfull_bar = empty_bar + PAIR_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int num_m = (p.M + 255) / 256;
+  const int num_n = (p.N + 255) / 256;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < PAIR_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        int m_blk, n_blk;
+        pair_raster(tile, num_m, num_n, m_blk, n_blk);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * PAIR_STAGE_BYTES;
+          uint8_t* sb = sa + PAIR_A_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * PAIR_STAGE_BYTES);
+          const int k0 = kb * GEMM_BK;
+          const int chunk = k0 / p.kc;
+          tma_load_3d_pair(sa, &tmA, &full_bar[stage], k0 - chunk * p.kc, m_blk * 256 + rank * 128, chunk);
+          tma_load_2d_pair(sb, &tmB, &full_bar[stage], k0, n_blk * 256 + rank * 128);
+          if (++stage == PAIR_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(256, 256, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * 256;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * PAIR_STAGE_BYTES);
+          const uint32_t sb = sa + PAIR_A_BYTES;
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k)
+            mma_bf16_ss_pair(tmem_d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
+                             (kb | k) ? 1u : 0u);
+          mma_commit_pair(&empty_bar[stage], 0x3);
+          if (++stage == PAIR_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull_bar[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+      int m_blk, n_blk;
+      pair_raster(tile, num_m, num_n, m_blk, n_blk);
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 256; c0 += 32) {
+        const int gc0 = n_blk * 256 + c0;
+        if (gc0 >= p.N) break;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256 + c0, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (gr < p.M) epilogue_chunk(p, gr, gc0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<512>(tmem_base);
+}
+
+static int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
+    configured = true;
+  }
+  const int tiles = ((p.M + 255) / 256) * ((p.N + 255) / 256);
+  const int max_pairs = sm_count() / 2;
+  const int pairs = tiles < max_pairs ? tiles : max_pairs;
+  gemm_tc_pair_kernel<<<2 * pairs, GEMM_THREADS, PAIR_SMEM, stream>>>(ta, tb, p);
+  return check_launch("gemm_tc_pair_kernel");
+}
+
 template <int BN>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
   using C = GemmCfg<BN>;
@@ -318,6 +477,14 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
 }  // namespace ftb
 
 using namespace ftb;
+
+static int g_gemm_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
+
+extern "C" int ftb_set_gemm_variant(int32_t v) {
+  if (v < 0 || v > 2) return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair)");
+  g_gemm_variant = v;
+  return FTB_OK;
+}
 
 extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_stride, const void* B,
                              int64_t ldb, int32_t M, int32_t N, int32_t K, const ftb_epilogue* epi, void* stream) {
@@ -355,6 +522,7 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   if (epi->rope) p.rope = *epi->rope;
 
   const int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  const bool pair = g_gemm_variant == 2 || (g_gemm_variant == 0 && M >= 256 && N >= 256);
   CUtensorMap ta, tb;
   // A: 3D {kc, M, chunks}
   {
@@ -367,11 +535,12 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   {
     uint64_t dims[2] = {(uint64_t)K, (uint64_t)N};
     uint64_t strides[1] = {(uint64_t)ldb * 2};
-    uint32_t box[2] = {GEMM_BK, (uint32_t)BN};
+    uint32_t box[2] = {GEMM_BK, pair ? 128u : (uint32_t)BN};
     int rc = make_tmap_bf16(&tb, B, 2, dims, strides, box);
     if (rc) return rc;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (pair) return launch_gemm_pair(ta, tb, p, s);
   if (BN == 64) return launch_gemm<64>(ta, tb, p, s);
   if (BN == 128) return launch_gemm<128>(ta, tb, p, s);
   return launch_gemm<256>(ta, tb, p, s);

@@ -253,3 +253,31 @@ def test_fill_normal_statistics(ops, cuda):
     t2 = torch.empty_like(t)
     ops.fill_normal_(t2, 1234, 1.0)
     assert torch.equal(t, t2)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 512, 160), (1000, 768, 1536), (2048, 1536, 1536),
+                                   (10530 // 4, 1024, 512), (257, 4608, 96)])
+def test_gemm_variants(ops, cuda, variant, M, N, K):
+    """Single-CTA and CTA-pair (cta_group::2) kernels give the same fp32 result."""
+    from paper_2512_23379_b200 import _capi as A
+    g = torch.Generator().manual_seed(M + N + K)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    b = torch.randn(N, generator=g).to(cuda)
+    h = torch.randn(M, N, generator=g).to(cuda)
+    h0 = h.clone()
+    A.call("ftb_set_gemm_variant", variant)
+    try:
+        out = torch.empty(M, N, device=cuda)
+        ops.gemm(a, w, out, "f32", bias=b)
+        ops.gemm(a, w, h, "resid_f32", bias=b)
+        ob = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+        ops.gemm(a, w, ob, "gelu_bf16", bias=b)
+    finally:
+        A.call("ftb_set_gemm_variant", 0)
+    ref = a.float() @ w.float().t() + b
+    assert rel(out, ref) < 1e-5
+    assert rel(h, h0 + ref) < 1e-5
+    refg = 0.5 * ref * (1 + torch.tanh(math.sqrt(2 / math.pi) * (ref + 0.044715 * ref ** 3)))
+    assert rel(ob.float(), refg) < 5e-3
