@@ -127,9 +127,12 @@ class DeviceDenoiser:
     """Denoiser bound to device weights and one chunk geometry.
 
     Geometry: chunk_len L_c frames, motion_len L_m, latent grid (H, W)
-    (ftlk: H = W = 1). Token count L = L_c * (H/ph) * (W/pw)."""
+    (ftlk: H = W = 1). Token count L = L_c * (H/ph) * (W/pw). With a
+    communicator of world g > 1 the step runs Ulysses sequence parallel
+    (dist.py): this rank owns tokens [start, start + Ls) of the padded chunk."""
 
-    def __init__(self, weights: DeviceWeights, chunk_len, motion_len, latent_hw=(1, 1), stream=None):
+    def __init__(self, weights: DeviceWeights, chunk_len, motion_len, latent_hw=(1, 1), stream=None, comm=None):
+        from .dist import LocalComm, ShardPlan
         cfg = weights.cfg
         self.cfg, self.w = cfg, weights
         self.dev = weights.device
@@ -143,33 +146,45 @@ class DeviceDenoiser:
         self.gh, self.gw = self.H // self.ph, self.W // self.pw
         self.T = self.gh * self.gw
         self.L = self.Lc * self.T
+        self.comm = comm if comm is not None else LocalComm()
+        self.plan = ShardPlan(self.L, self.comm.world, self.comm.rank)
+        self.hpr = self.plan.heads_per_rank(cfg.heads)
         m, ff = cfg.model_dim, cfg.ff_dim
         self.n_cond = self.Lc * (cfg.audio_tokens if cfg.mode == "wan" else 1) + 1
         d = self.dev
         bf, f32 = torch.bfloat16, torch.float32
-        L = self.L
+        L, Lp, Ls, g = self.L, self.plan.L_pad, self.plan.Ls, self.plan.world
+        hw = self.hpr * cfg.head_dim
+        F = self.Lc + 1  # per-frame tables carry one extra (padding) frame
         self.kin = round8(cfg.in_features)
+        self.ko = round8(cfg.out_features)
         self.buf = {
-            "tok": torch.zeros(L, self.kin, dtype=bf, device=d),
-            "h": torch.empty(L, m, dtype=f32, device=d),
-            "u": torch.empty(L, m, dtype=bf, device=d),
-            "qkv": torch.empty(L, 3 * m, dtype=bf, device=d),
-            "ao": torch.empty(L, m, dtype=bf, device=d),
-            "ff": torch.empty(L, ff, dtype=bf, device=d),
-            "x0tok": torch.empty(L, round8(cfg.out_features), dtype=f32, device=d),
+            "tok": torch.zeros(Lp, self.kin, dtype=bf, device=d),
+            "h": torch.empty(Ls, m, dtype=f32, device=d),
+            "u": torch.empty(Ls, m, dtype=bf, device=d),
+            "qkv": torch.empty(Ls, 3 * m, dtype=bf, device=d),     # Ulysses send layout
+            "ao": torch.empty(Ls, m, dtype=bf, device=d),
+            "ff": torch.empty(Ls, ff, dtype=bf, device=d),
+            "x0loc": torch.empty(Ls, self.ko, dtype=f32, device=d),
             "cond_in": torch.zeros(self.n_cond, round8(max(cfg.cond_dim, cfg.latent_dim)), dtype=bf, device=d),
             "cond": torch.empty(self.n_cond, m, dtype=f32, device=d),
             "cond_bf": torch.empty(self.n_cond, m, dtype=bf, device=d),
             "ckv": torch.empty(cfg.layers, self.n_cond, 2 * m, dtype=bf, device=d),
-            "tfeat": torch.empty(self.Lc, m, dtype=bf, device=d),
-            "temb": torch.empty(self.Lc, m, dtype=f32, device=d),
-            "temb_act": torch.empty(self.Lc, m, dtype=bf, device=d),
-            "e0": torch.empty(self.Lc, 6 * m, dtype=f32, device=d),
+            "tfeat": torch.empty(F, m, dtype=bf, device=d),
+            "temb": torch.empty(F, m, dtype=f32, device=d),
+            "temb_act": torch.empty(F, m, dtype=bf, device=d),
+            "e0": torch.empty(F, 6 * m, dtype=f32, device=d),
         }
-        self.pos = torch.from_numpy(sinusoid(np.arange(self.Lc), m)).to(f32).to(d)  # chunk-relative frames
+        if g > 1:
+            self.buf["qkv_recv"] = torch.empty(Lp, 3 * hw, dtype=bf, device=d)
+            self.buf["attn_full"] = torch.empty(Lp, hw, dtype=bf, device=d)
+            self.buf["x0tok"] = torch.empty(Lp, self.ko, dtype=f32, device=d)
+        else:
+            self.buf["x0tok"] = self.buf["x0loc"]
+        self.pos = torch.from_numpy(sinusoid(np.arange(F), m)).to(f32).to(d)  # chunk-relative frames
         self.rope = None
         if cfg.mode == "wan":
-            self.rope_host = rope3d_tables(self.Lc, self.gh, self.gw, cfg.head_dim, cfg.rope_theta)
+            self.rope_host = rope3d_tables(F, self.gh, self.gw, cfg.head_dim, cfg.rope_theta)
             self.rope = ops.RopeTables(self.rope_host, self.gh, self.gw, d)
         self._frame_cache = {}
         self.scale = 1.0 / math.sqrt(cfg.head_dim)
@@ -179,19 +194,21 @@ class DeviceDenoiser:
     def frame_vectors(self, frame_t):
         """Per-frame time conditioning for a frame_t vector, cached (the ladder
         repeats every chunk). ftlk: rowvec[f] = temb[f] + pos[f] (net.py:229-232).
-        wan: mods[l, f] = silu(temb)@tproj + b + layer.mod (6 x m), final[f] = final.mod + temb[f]."""
+        wan: mods[l, f] = silu(temb)@tproj + b + layer.mod (6 x m), final[f] = final.mod + temb[f].
+        One extra frame (t = 0) backs the Ulysses padding tokens."""
         key = tuple(float(t) for t in np.asarray(frame_t, dtype=np.float64).reshape(-1))
         hit = self._frame_cache.get(key)
         if hit is not None:
             return hit
         cfg, B, W = self.cfg, self.buf, self.w
         m = cfg.model_dim
-        tf = torch.from_numpy(sinusoid(np.asarray(key) * TIME_SCALE, m)).to(torch.bfloat16).to(self.dev)
+        F = self.Lc + 1
+        tf = torch.from_numpy(sinusoid(np.asarray(key + (0.0,)) * TIME_SCALE, m)).to(torch.bfloat16).to(self.dev)
         B["tfeat"].copy_(tf)
         wt, _ = W.mats["time.w"]
         out = {}
         if cfg.mode == "ftlk":
-            rv = torch.empty(self.Lc, m, dtype=torch.float32, device=self.dev)
+            rv = torch.empty(F, m, dtype=torch.float32, device=self.dev)
             ops.gemm(B["tfeat"], wt, rv, "rowadd_f32", bias=W.vecs["time.b"], group_vec=self.pos, rows_per_group=1,
                      stream=self.stream)
             out["rowvec"] = rv
@@ -200,15 +217,14 @@ class DeviceDenoiser:
             ops.silu_to_bf16(B["temb"], B["temb_act"], stream=self.stream)
             ops.gemm(B["temb_act"], W.mats["tproj.w"][0], B["e0"], "f32", bias=W.vecs["tproj.b"],
                      stream=self.stream)
-            mods = torch.empty(cfg.layers, self.Lc, 6 * m, dtype=torch.float32, device=self.dev)
+            mods = torch.empty(cfg.layers, F, 6 * m, dtype=torch.float32, device=self.dev)
             ops.add_bcast(B["e0"], W.vecs["layers.mod"], mods, stream=self.stream)
-            fin = torch.empty(1, self.Lc, 2 * m, dtype=torch.float32, device=self.dev)
+            fin = torch.empty(F, 1, 2 * m, dtype=torch.float32, device=self.dev)
             # final.mod (2, m) + temb[f] broadcast over the 2 slots
             ops.add_bcast(W.vecs["final.mod"].reshape(1, 2 * m),
-                          torch.cat([B["temb"], B["temb"]], 1).contiguous(), fin.view(self.Lc, 1, 2 * m),
-                          stream=self.stream)
+                          torch.cat([B["temb"], B["temb"]], 1).contiguous(), fin, stream=self.stream)
             out["mods"] = mods
-            out["final"] = fin.view(self.Lc, 2 * m)
+            out["final"] = fin.view(F, 2 * m)
         self._frame_cache[key] = out
         return out
 
@@ -218,7 +234,6 @@ class DeviceDenoiser:
         per-layer cross-attention K|V projections of it (cond does not change
         across the sampler's steps, so K/V are computed once per chunk)."""
         cfg, B, W = self.cfg, self.buf, self.w
-        m = cfg.model_dim
         nsig = self.n_cond - 1
         ci = B["cond_in"]
         ci.zero_()
@@ -233,89 +248,100 @@ class DeviceDenoiser:
             A = cfg.audio_tokens
         ci[:nsig, :sig.shape[1]].copy_(sig.to(torch.bfloat16))
         ci[nsig:, :ref.shape[1]].copy_(ref.to(torch.bfloat16))
-        ksig = W.mats["sig.w"][1]
-        kref = W.mats["ref.w"][1]
         ops.gemm(ci[:nsig], W.mats["sig.w"][0], B["cond"][:nsig], "rowadd_f32", bias=W.vecs["sig.b"],
-                 group_vec=self.pos, rows_per_group=A, M=nsig, K=ksig, lda=ci.stride(0), stream=self.stream)
+                 group_vec=self.pos, rows_per_group=A, M=nsig, K=W.mats["sig.w"][1], lda=ci.stride(0),
+                 stream=self.stream)
         ops.gemm(ci[nsig:], W.mats["ref.w"][0], B["cond"][nsig:], "f32", bias=W.vecs["ref.b"],
-                 M=1, K=kref, lda=ci.stride(0), stream=self.stream)
+                 M=1, K=W.mats["ref.w"][1], lda=ci.stride(0), stream=self.stream)
         ops.cast_f32_bf16(B["cond"], B["cond_bf"], stream=self.stream)
         for i in range(cfg.layers):
             ops.gemm(B["cond_bf"], W.mats["layers.%d.cross.wkv" % i][0], B["ckv"][i], "bf16", stream=self.stream)
-        del m
-
-    def upload_cond_inputs(self, signal, reference):
-        self.prepare_cond(signal, reference)
 
     # ------------------------------------------------------------ one denoise step
     def step(self, motion, z, reference, fv, x0_out=None, ddim=None):
         """One Denoiser.forward on device. motion [L_m, D, H, W], z [L_c-L_m, D, H, W],
-        reference [D, H, W] (fp32 device). Writes x0 tokens to buf['x0tok']; if
-        x0_out is given, also unpatchifies the target frames (and applies the
-        DDIM update to z when ddim=(a_i, s_i, a_n, s_n))."""
+        reference [D, H, W] (fp32 device). Writes x0 tokens to buf['x0tok'] (all L
+        tokens on every rank); if x0_out is given, also unpatchifies the target frames
+        (and applies the DDIM update to z when ddim=(a_i, s_i, a_n, s_n))."""
         cfg, B, W = self.cfg, self.buf, self.w
         m, H_, hd = cfg.model_dim, cfg.heads, cfg.head_dim
         L, T, s = self.L, self.T, self.stream
+        pl = self.plan
+        s0, Ls, g, hpr = pl.start, pl.Ls, pl.world, self.hpr
+        hw = hpr * hd
         D = cfg.latent_dim
-        ops.patchify(motion, z, reference, self.Lm, self.Lc, D, self.H, self.W, self.ph, self.pw, B["tok"], stream=s)
+        ops.patchify(motion, z, reference, self.Lm, self.Lc, D, self.H, self.W, self.ph, self.pw, B["tok"][:L],
+                     stream=s)
         h = B["h"]
+        tok = B["tok"][s0:s0 + Ls]
         wan = cfg.mode == "wan"
         if wan:
-            ops.gemm(B["tok"], W.mats["in.w"][0], h, "f32", bias=W.vecs["in.b"], K=W.mats["in.w"][1], M=L,
+            ops.gemm(tok, W.mats["in.w"][0], h, "f32", bias=W.vecs["in.b"], K=W.mats["in.w"][1], M=Ls,
                      lda=self.kin, stream=s)
         else:
-            ops.gemm(B["tok"], W.mats["in.w"][0], h, "rowadd_f32", bias=W.vecs["in.b"], group_vec=fv["rowvec"],
-                     rows_per_group=T, K=W.mats["in.w"][1], M=L, lda=self.kin, stream=s)
+            ops.gemm(tok, W.mats["in.w"][0], h, "rowadd_f32", bias=W.vecs["in.b"], group_vec=fv["rowvec"],
+                     rows_per_group=T, row_offset=s0, K=W.mats["in.w"][1], M=Ls, lda=self.kin, stream=s)
         u, qkv, ao, ffb = B["u"], B["qkv"], B["ao"], B["ff"]
         for i in range(cfg.layers):
             p = "layers.%d." % i
             if wan:
-                md = fv["mods"][i]  # [L_c, 6m]
-                ops.norm_modulate(h, u, shift=md[:, 0:m], scale=md[:, m:2 * m], rows_per_group=T, stream=s)
+                md = fv["mods"][i]  # [L_c + 1, 6m]
+                ops.norm_modulate(h, u, shift=md[:, 0:m], scale=md[:, m:2 * m], rows_per_group=T, row_offset=s0,
+                                  stream=s)
             else:
                 ops.norm_modulate(h, u, gamma=W.vecs[p + "ln1.g"], beta=W.vecs[p + "ln1.b"], stream=s)
-            ops.gemm(u, W.mats[p + "self.wqkv"][0], qkv, "qkv_rope", heads=H_, head_dim=hd, heads_per_rank=H_,
-                     rope=self.rope, stream=s)
-            ops.attention(qkv[:, 0:m], qkv[:, m:2 * m], qkv[:, 2 * m:], ao, H_, hd, L, L, self.scale, stream=s)
-            if wan:
-                ops.gemm(ao, W.mats[p + "self.wo"][0], h, "resid_f32", group_vec=md[:, 2 * m:3 * m],
-                         rows_per_group=T, stream=s)
+            ops.gemm(u, W.mats[p + "self.wqkv"][0], qkv, "qkv_rope", heads=H_, head_dim=hd, heads_per_rank=hpr,
+                     row_offset=s0, rope=self.rope, stream=s)
+            if g == 1:
+                ops.attention(qkv[:, 0:m], qkv[:, m:2 * m], qkv[:, 2 * m:], ao, H_, hd, L, L, self.scale, stream=s)
+                o_in = dict(a=ao)
             else:
-                ops.gemm(ao, W.mats[p + "self.wo"][0], h, "resid_f32", stream=s)
+                rq, af = B["qkv_recv"], B["attn_full"]
+                self.comm.all_to_all(rq, qkv, stream=s)                       # heads <- sequence
+                ops.attention(rq[:, 0:hw], rq[:, hw:2 * hw], rq[:, 2 * hw:], af, hpr, hd, pl.L_pad, L, self.scale,
+                              stream=s)
+                self.comm.all_to_all(ao, af, stream=s)                        # sequence <- heads
+                o_in = dict(a=ao, M=Ls, K=m, lda=hw, a_chunks=g, a_chunk_stride=Ls * hw)
+            if wan:
+                ops.gemm(o_in.pop("a"), W.mats[p + "self.wo"][0], h, "resid_f32", group_vec=md[:, 2 * m:3 * m],
+                         rows_per_group=T, row_offset=s0, stream=s, **o_in)
+            else:
+                ops.gemm(o_in.pop("a"), W.mats[p + "self.wo"][0], h, "resid_f32", stream=s, **o_in)
             ops.norm_modulate(h, u, gamma=W.vecs[p + "ln2.g"], beta=W.vecs[p + "ln2.b"], stream=s)
             ops.gemm(u, W.mats[p + "cross.wq"][0], qkv[:, 0:m], "bf16", stream=s)
             ckv = B["ckv"][i]
-            ops.attention(qkv[:, 0:m], ckv[:, 0:m], ckv[:, m:], ao, H_, hd, L, self.n_cond, self.scale,
-                          stream=s)
+            ops.attention(qkv[:, 0:m], ckv[:, 0:m], ckv[:, m:], ao, H_, hd, Ls, self.n_cond, self.scale, stream=s)
             ops.gemm(ao, W.mats[p + "cross.wo"][0], h, "resid_f32", stream=s)
             if wan:
                 ops.norm_modulate(h, u, shift=md[:, 3 * m:4 * m], scale=md[:, 4 * m:5 * m], rows_per_group=T,
-                                  stream=s)
+                                  row_offset=s0, stream=s)
             else:
                 ops.norm_modulate(h, u, gamma=W.vecs[p + "ln3.g"], beta=W.vecs[p + "ln3.b"], stream=s)
             ops.gemm(u, W.mats[p + "ffn.w1"][0], ffb, "gelu_bf16", bias=W.vecs[p + "ffn.b1"], stream=s)
             if wan:
                 ops.gemm(ffb, W.mats[p + "ffn.w2"][0], h, "resid_f32", bias=W.vecs[p + "ffn.b2"],
-                         group_vec=md[:, 5 * m:6 * m], rows_per_group=T, stream=s)
+                         group_vec=md[:, 5 * m:6 * m], rows_per_group=T, row_offset=s0, stream=s)
             else:
                 ops.gemm(ffb, W.mats[p + "ffn.w2"][0], h, "resid_f32", bias=W.vecs[p + "ffn.b2"], stream=s)
         if wan:
             fm = fv["final"]
-            ops.norm_modulate(h, u, shift=fm[:, 0:m], scale=fm[:, m:2 * m], rows_per_group=T, stream=s)
+            ops.norm_modulate(h, u, shift=fm[:, 0:m], scale=fm[:, m:2 * m], rows_per_group=T, row_offset=s0, stream=s)
         else:
             ops.norm_modulate(h, u, gamma=W.vecs["final.g"], beta=W.vecs["final.b"], stream=s)
+        ops.gemm(u, W.mats["out.w"][0], B["x0loc"], "f32", bias=W.vecs["out.b"], stream=s)
         x0t = B["x0tok"]
-        ops.gemm(u, W.mats["out.w"][0], x0t, "f32", bias=W.vecs["out.b"], stream=s)
+        if g > 1:
+            self.comm.all_gather(x0t, B["x0loc"], stream=s)
         if x0_out is not None:
-            ops.unpatch_ddim(x0t[:, :cfg.out_features], self.Lm, self.Lc, D, self.H, self.W, self.ph, self.pw, z,
+            ops.unpatch_ddim(x0t[:L, :cfg.out_features], self.Lm, self.Lc, D, self.H, self.W, self.ph, self.pw, z,
                              x0_out, coeffs=ddim, stream=s)
-        return x0t
+        return x0t[:L]
 
     # ------------------------------------------------------------ full-chunk output (reference forward)
     def tokens_to_frames(self, x0t):
         """x0 tokens [L, out_features] -> (L_c, D, H, W) float tensor (device)."""
         cfg = self.cfg
-        x = x0t[:, :cfg.out_features].reshape(self.Lc, self.gh, self.gw, cfg.latent_dim, self.ph, self.pw)
+        x = x0t[:self.L, :cfg.out_features].reshape(self.Lc, self.gh, self.gw, cfg.latent_dim, self.ph, self.pw)
         return x.permute(0, 3, 1, 4, 2, 5).reshape(self.Lc, cfg.latent_dim, self.H, self.W)
 
     # ------------------------------------------------------------ the few-step sampler on device

@@ -1,0 +1,70 @@
+"""Multi-process host logic of the Ulysses path on CPU (gloo, world_size 2):
+shard plan arithmetic and the collective layouts the device path relies on."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2512_23379_b200.dist import ShardPlan
+
+
+def test_shard_plan_arithmetic():
+    for L, g in [(10530, 1), (10530, 2), (10530, 4), (10530, 8), (162, 4), (9, 2)]:
+        plans = [ShardPlan(L, g, r) for r in range(g)]
+        assert all(p.Ls * g == p.L_pad >= L for p in plans)
+        assert plans[0].L_pad - L < g
+        assert sum(p.valid for p in plans) == L
+        assert [p.start for p in plans] == [r * plans[0].Ls for r in range(g)]
+    assert ShardPlan(10530, 8, 0).Ls == 1317
+    assert ShardPlan(10530, 8, 0).heads_per_rank(40) == 5
+    with pytest.raises(Exception):
+        ShardPlan(10530, 8, 0).heads_per_rank(12)
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2512_23379_b200.dist import TorchComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        Ls, hw, L = 3, 4, 5          # L_pad = 6
+        # QKV send layout [dest][Ls][3][hw]; value encodes (src rank, dest, local token, which, d)
+        send = torch.zeros(world, Ls, 3, hw)
+        for dst in range(world):
+            for t in range(Ls):
+                for w in range(3):
+                    send[dst, t, w] = torch.arange(hw, dtype=torch.float32) + 1000 * rank + 100 * dst + 10 * t + w * 0.1
+        recv = torch.empty(world * Ls, 3, hw)
+        comm.all_to_all(recv, send)
+        # full sequence for my head group: token rows in global order
+        for src in range(world):
+            for t in range(Ls):
+                exp = torch.arange(hw, dtype=torch.float32) + 1000 * src + 100 * rank + 10 * t
+                assert torch.allclose(recv[src * Ls + t, 0], exp)
+        out = torch.empty(world * Ls, 2)
+        comm.all_gather(out, torch.full((Ls, 2), float(rank)))
+        assert torch.equal(out[:Ls], torch.zeros(Ls, 2)) and torch.equal(out[Ls:], torch.ones(Ls, 2))
+        q.put((rank, "ok", L))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_collective_layouts():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + os.getpid() % 300
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res

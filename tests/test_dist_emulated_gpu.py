@@ -1,0 +1,87 @@
+"""Ulysses sequence parallelism, g ranks emulated on one B200 (one thread per
+rank, ThreadComm exchanges, no kernel ever waits on another): the sharded step
+must reproduce the single-rank step and the oracle."""
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import wan_oracle as WO
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _setup(heads=4, hd=64, Lc=3, Lm=1, H=12, W=18, layers=2, seed=5):
+    from paper_2512_23379_b200.config import NetConfig
+    from paper_2512_23379_b200.net import ParamStore
+    m = heads * hd
+    cfg = NetConfig(m, layers, heads, 2 * m, 16, mode="wan", patch=(1, 2, 2), audio_dim=16, audio_tokens=2)
+    store = ParamStore.init(cfg, seed)
+    r = np.random.default_rng(seed)
+    x = dict(motion=r.standard_normal((Lm, 16, H, W)), z=r.standard_normal((Lc - Lm, 16, H, W)),
+             ref=r.standard_normal((16, H, W)), audio=r.standard_normal((Lc, 2, 16)))
+    return cfg, store, x, (Lc, Lm, H, W)
+
+
+def _run(cfg, store, x, geo, world, dev):
+    from paper_2512_23379_b200.dist import ThreadComm
+    from paper_2512_23379_b200.model import DeviceDenoiser, DeviceWeights
+    Lc, Lm, H, W = geo
+    w = DeviceWeights.from_host(cfg, store.params, dev)
+    comms = ThreadComm.make(world) if world > 1 else [None]
+    out, errs = [None] * world, []
+    frame_t = np.where(np.arange(Lc) < Lm, 0.0, 0.75)
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(dev)
+            s = torch.cuda.Stream(device=dev)
+            with torch.cuda.stream(s):
+                d = DeviceDenoiser(w, Lc, Lm, (H, W), stream=s, comm=comms[r])
+                md = torch.as_tensor(x["motion"], dtype=torch.float32, device=dev)
+                zd = torch.as_tensor(x["z"], dtype=torch.float32, device=dev)
+                rd = torch.as_tensor(x["ref"], dtype=torch.float32, device=dev)
+                d.prepare_cond(x["audio"], x["ref"])
+                fv = d.frame_vectors(frame_t)
+                x0t = d.step(md, zd, rd, fv)
+                out[r] = d.tokens_to_frames(x0t).double().cpu().numpy()
+                s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            raise
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    return out, frame_t
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ulysses_matches_single_rank(cuda, world):
+    cfg, store, x, geo = _setup()
+    one, frame_t = _run(cfg, store, x, geo, 1, cuda)
+    many, _ = _run(cfg, store, x, geo, world, cuda)
+    for r in range(world):
+        assert rel(many[r], one[0]) < 5e-3, r   # same kernels; short shards may pick the CUDA-core cross-attn
+    ref = WO.denoise(store.bf16_rounded().params, dict(model_dim=cfg.model_dim, layers=cfg.layers, heads=cfg.heads,
+                                                       latent_dim=16, patch=(1, 2, 2), audio_tokens=2, audio_dim=16),
+                     x["motion"], x["z"], x["ref"], x["audio"], frame_t)
+    assert rel(many[0], ref) < 1e-2
+
+
+def test_ulysses_padding_path(cuda):
+    """L = 3*6*9 = 162 tokens: not divisible by 4 -> padded shards, masked keys."""
+    cfg, store, x, geo = _setup(Lc=3, Lm=1, H=12, W=18)
+    assert (geo[0] * (geo[2] // 2) * (geo[3] // 2)) % 4 != 0
+    one, _ = _run(cfg, store, x, geo, 1, cuda)
+    many, _ = _run(cfg, store, x, geo, 4, cuda)
+    assert rel(many[3], one[0]) < 5e-3
