@@ -257,6 +257,276 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
+// ============================================================ tcgen05 flash kernel v2 (2 Q tiles / CTA)
+// One CTA = one head x 256 queries as two 128-row tiles. The MMA warp interleaves the
+// tiles — PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) — so the tensor core works on one tile
+// while the other tile's softmax warpgroup (4 warps, one thread per row) runs. K and V
+// blocks stream through a 3-slot TMA ring; half of the exponentials are evaluated with a
+// degree-3 polynomial on the FMA pipe to offload MUFU (P is stored as bf16 anyway).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;            // 1.5 * 2^23: round-to-nearest integer in the mantissa
+  const float n = t - 12582912.f;
+  const float f = x - n;                     // [-0.5, 0.5]
+  float p = fmaf(f, 0.0555041086648216f, 0.2402265069591007f);
+  p = fmaf(p, f, 0.6931471805599453f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (int)((unsigned)(__float_as_int(t) - 0x4B400000) << 23));
+}
+
+template <int HD>
+struct Fmha2Cfg {
+  static constexpr int BOX = 128 * 64 * 2;               // 128 rows x 64 cols bf16
+  static constexpr int NBOX = HD / 64;
+  static constexpr int TILE = NBOX * BOX;                // 128 rows x HD
+  static constexpr int OFF_Q = 0;                        // 2 tiles
+  static constexpr int OFF_KV = OFF_Q + 2 * TILE;        // 3-slot ring (K or V blocks)
+  static constexpr int OFF_P = OFF_KV + 3 * TILE;        // 2 x (128 x 128 bf16)
+  static constexpr int OFF_BAR = OFF_P + 2 * 2 * BOX;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+    fmha2_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+  using C = Fmha2Cfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [3]
+  uint64_t* kv_empty = bars + 4;  // [3]
+  uint64_t* s_full = bars + 7;    // [2] per tile
+  uint64_t* s_empty = bars + 9;   // [2]
+  uint64_t* p_full = bars + 11;   // [2]
+  uint64_t* o_done = bars + 13;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int qblk = blockIdx.x, head = blockIdx.y;
+  const int n_kv = (p.Lk + 127) / 128;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 3; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&s_empty[t], 4);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&o_done[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int col0 = head * HD;
+      mbar_arrive_expect_tx(q_full, 2 * C::TILE);
+      for (int t = 0; t < 2; ++t)
+        for (int b = 0; b < C::NBOX; ++b)
+          tma_load_2d(smem + C::OFF_Q + t * C::TILE + b * C::BOX, &tmQ, q_full, col0 + 64 * b, qblk * 256 + t * 128);
+      for (int i = 0; i < 2 * n_kv; ++i) {  // item 2j = K_j, 2j+1 = V_j
+        const int slot = i % 3;
+        mbar_wait(&kv_empty[slot], ((i / 3) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[slot], C::TILE);
+        const CUtensorMap* tm = (i & 1) ? &tmV : &tmK;
+        for (int b = 0; b < C::NBOX; ++b)
+          tma_load_2d(smem + C::OFF_KV + slot * C::TILE + b * C::BOX, tm, &kv_full[slot], col0 + 64 * b,
+                      (i >> 1) * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
+      auto wait_item = [&](int i) { mbar_wait(&kv_full[i % 3], (i / 3) & 1); };
+      auto issue_s = [&](int t, int j) {
+        const uint32_t sq = smem_u32(smem + C::OFF_Q + t * C::TILE);
+        const uint32_t sk = smem_u32(smem + C::OFF_KV + ((2 * j) % 3) * C::TILE);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::BOX + (kk & 3) * 32;
+          mma_bf16_ss(tmem + t * 128, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024), idesc_s,
+                      kk > 0);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t sp = smem_u32(smem + C::OFF_P + t * 2 * C::BOX);
+        const uint32_t sv = smem_u32(smem + C::OFF_KV + ((2 * j + 1) % 3) * C::TILE);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t ad = sdesc_sw128(sp + (kk >> 2) * C::BOX + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(sv + kk * 16 * 128, C::BOX, 1024);
+          mma_bf16_ss(tmem + 256 + t * 128, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&o_done[t]);
+      };
+      mbar_wait(q_full, 0);
+      wait_item(0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      mma_commit(&kv_empty[0]);  // K_0 consumed by both tiles
+      for (int j = 0; j < n_kv; ++j) {
+        wait_item(2 * j + 1);  // V_j
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        if (j + 1 < n_kv) {
+          wait_item(2 * j + 2);  // K_{j+1}
+          mbar_wait(&s_empty[0], j & 1);
+          tc_fence_after();
+          issue_s(0, j + 1);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, j);
+        mma_commit(&kv_empty[(2 * j + 1) % 3]);  // V_j consumed
+        if (j + 1 < n_kv) {
+          mbar_wait(&s_empty[1], j & 1);
+          tc_fence_after();
+          issue_s(1, j + 1);
+          mma_commit(&kv_empty[(2 * j + 2) % 3]);  // K_{j+1} consumed
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = (warp - 4) >> 2;  // tile handled by this warpgroup
+    const int qw = warp & 3;
+    const int row = qw * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qw * 32) << 16;
+    const uint32_t tS = tmem + lane_off + t * 128;
+    const uint32_t tO = tmem + lane_off + 256 + t * 128;
+    uint8_t* prow = smem + C::OFF_P + t * 2 * C::BOX + row * 128;
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t sr[128];
+      tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
+      tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+      tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
+      tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[t]);
+      const int valid = p.Lk - j * 128;
+      if (valid < 128) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
+      }
+      float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; c += 8) {
+        m0 = fmax3(m0, __uint_as_float(sr[c + 0]), __uint_as_float(sr[c + 1]));
+        m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
+        m2 = fmax3(m2, __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
+        m3 = fmax3(m3, __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
+      }
+      const float mx = fmax3(m0, m1, fmaxf(m2, m3)) * p.scale_log2;
+      float m_use = m_ref;
+      bool rescale = false;
+      if (j == 0) {
+        m_use = mx;
+      } else if (mx > m_ref + 8.f) {
+        m_use = mx;
+        rescale = true;
+      }
+      const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
+      const float2 nm2 = make_float2(-m_use, -m_use);
+      float2 rs2 = make_float2(0.f, 0.f);
+      if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        float2 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float2 x = ffma2(make_float2(__uint_as_float(sr[ch * 8 + 2 * u]), __uint_as_float(sr[ch * 8 + 2 * u + 1])),
+                           sc2, nm2);
+          if (u == 3) {  // one pair in four on the FMA pipe (offloads MUFU)
+            x.x = fmaxf(x.x, -126.f);
+            x.y = fmaxf(x.y, -126.f);
+            e[u] = ex2_poly2(x);
+          } else {
+            e[u] = make_float2(ex2(x.x), ex2(x.y));
+          }
+          rs2 = fadd2(rs2, e[u]);
+        }
+        uint4 w;
+        w.x = pack_bf16(e[0].x, e[0].y);
+        w.y = pack_bf16(e[1].x, e[1].y);
+        w.z = pack_bf16(e[2].x, e[2].y);
+        w.w = pack_bf16(e[3].x, e[3].y);
+        const int atom = ch >> 3, c16 = ch & 7;
+        *reinterpret_cast<uint4*>(prow + atom * C::BOX + ((c16 ^ (row & 7)) << 4)) = w;
+      }
+      const float rs = rs2.x + rs2.y;
+      if (__any_sync(0xffffffffu, rescale)) {
+        const float f = rescale ? ex2(m_ref - m_use) : 1.f;
+        l *= f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld32(tO + c0, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * f);
+          tmem_st32(tO + c0, o);
+        }
+        tmem_st_wait();
+      }
+      l += rs;
+      m_ref = m_use;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    mbar_wait(&o_done[t], (n_kv - 1) & 1);
+    tc_fence_after();
+    const int grow = qblk * 256 + t * 128 + row;
+    const float inv = 1.f / l;
+#pragma unroll 1
+    for (int c0 = 0; c0 < HD; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld32(tO + c0, o);
+      tmem_ld_wait();
+      if (grow < p.Lq) {
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (long long)grow * p.ldo + head * HD + c0);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(o[8 * qq + 0]) * inv, __uint_as_float(o[8 * qq + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv);
+          dst[qq] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // ============================================================ short-KV CUDA-core kernel
 // grid (ceil(Lq/16), heads), 128 threads: warp w owns query rows 4w..4w+3 of the block.
 // HDMAX bounds the shared-memory tile; the head width itself is runtime (any hd <= HDMAX).
@@ -367,6 +637,31 @@ static int launch_fmha(const AttnParams& p, cudaStream_t s) {
   return check_launch("fmha_tc_kernel");
 }
 
+template <int HD>
+static int launch_fmha2(const AttnParams& p, cudaStream_t s) {
+  using C = Fmha2Cfg<HD>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fmha2_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "fmha2 smem attribute");
+    configured = true;
+  }
+  CUtensorMap tq, tk, tv;
+  auto mk = [&](CUtensorMap* m, const void* ptr, long long ld, int rows) {
+    uint64_t dims[2] = {(uint64_t)ld, (uint64_t)rows};
+    uint64_t strides[1] = {(uint64_t)ld * 2};
+    uint32_t box[2] = {64, 128};
+    return make_tmap_bf16(m, ptr, 2, dims, strides, box);
+  };
+  int rc;
+  if ((rc = mk(&tq, p.q, p.ldq, p.Lq))) return rc;
+  if ((rc = mk(&tk, p.k, p.ldk, p.Lk))) return rc;
+  if ((rc = mk(&tv, p.v, p.ldv, p.Lk))) return rc;
+  dim3 grid((p.Lq + 255) / 256, p.heads);
+  fmha2_tc_kernel<HD><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
+  return check_launch("fmha2_tc_kernel");
+}
+
 template <int HDMAX>
 static int launch_small(const AttnParams& p, cudaStream_t s) {
   dim3 grid((p.Lq + 15) / 16, p.heads);
@@ -387,10 +682,15 @@ extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, cons
   AttnParams p{(const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (__nv_bfloat16*)o,
                ldq, ldk, ldv, ldo, Lq, Lk, heads, head_dim, scale * 1.4426950408889634f};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (impl == 0) {
+  if (impl == 0 || impl == 2) {
     if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
-    if (head_dim == 128) return launch_fmha<128>(p, s);
-    if (head_dim == 64) return launch_fmha<64>(p, s);
+    if (impl == 0) {  // 2 Q tiles per CTA, ping-pong softmax warpgroups
+      if (head_dim == 128) return launch_fmha2<128>(p, s);
+      if (head_dim == 64) return launch_fmha2<64>(p, s);
+    } else {          // v1: 1 Q tile per CTA
+      if (head_dim == 128) return launch_fmha<128>(p, s);
+      if (head_dim == 64) return launch_fmha<64>(p, s);
+    }
     return set_error(FTB_EINVAL, "fmha: head_dim must be 64 or 128");
   }
   if (head_dim <= 16) return launch_small<16>(p, s);

@@ -221,6 +221,46 @@ FTB_DEV void tmem_dealloc_pair(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
 }
 
+// ------------------------------------------------------------------ packed fp32x2 (FFMA2 / FADD2) and 3-input max
+FTB_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 A, B, C, D;\n\t"
+      "mov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\tmov.b64 C, {%6, %7};\n\t"
+      "fma.rn.f32x2 D, A, B, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+FTB_DEV float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 A, B, D;\n\t"
+      "mov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\t"
+      "add.rn.f32x2 D, A, B;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+FTB_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for a pair on the FMA pipe: round-to-nearest split x = n + f, f in [-0.5, 0.5],
+// degree-3 polynomial, exponent add folded into one IMAD per element
+// ((t_bits - 0x4B400000) << 23 == t_bits << 23 mod 2^32). Requires x >= -126.
+FTB_DEV float2 ex2_poly2(float2 x) {
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(f, make_float2(0.0555041086648216f, 0.0555041086648216f),
+                   make_float2(0.2402265069591007f, 0.2402265069591007f));
+  p = ffma2(p, f, make_float2(0.6931471805599453f, 0.6931471805599453f));
+  p = ffma2(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (int)((unsigned)__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (int)((unsigned)__float_as_int(t.y) << 23)));
+}
+
 // ------------------------------------------------------------------ math
 FTB_DEV float ex2(float x) {
   float y;
