@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--detail", action="store_true", help="per-shape kernel breakdown on stderr")
     return ap.parse_args()
 
 
@@ -279,12 +280,24 @@ def main():
 
     # ---------------- instrumented chunk: per-kernel durations for the roofline
     ops.PROFILER = []
+    ops.PROFILE_DETAIL = True if args.detail else None
     chunk(nsteps - 1)
     torch.cuda.synchronize()
     prof = ops.PROFILER
     ops.PROFILER = None
     agg = {}
+    if args.detail:
+        det = {}
+        for kind, a, b, fl, nb in prof:
+            g = det.setdefault(kind, [0.0, 0.0, 0])
+            g[0] += a.elapsed_time(b)
+            g[1] += fl
+            g[2] += 1
+        for k, v in sorted(det.items(), key=lambda kv: -kv[1][0]):
+            sys.stderr.write("%-50s %9.3f ms %5d launches %8.1f TFLOP/s\n" % (
+                k, v[0], v[2], v[1] / (v[0] * 1e-3) / 1e12 if v[1] else 0.0))
     for kind, a, b, fl, nb in prof:
+        kind = "gemm" if kind.startswith("gemm") else kind
         t = a.elapsed_time(b)
         g = agg.setdefault(kind, [0.0, 0.0, 0.0, 0])
         g[0] += t

@@ -52,15 +52,12 @@ enum {
   FTB_EPI_QKV_ROPE = 5    /* bf16 q|k|v with 3D RoPE on q,k; Ulysses send layout    */
 };
 
-/* 3D rotary tables (wan mode). Pair p of a head: p < pairs_t -> frame axis,
- * p < pairs_t+pairs_h -> row axis, else column axis. cos/sin are float32
- * [positions][pairs_axis] row-major, computed on the host in float64. */
+/* 3D rotary tables (wan mode): per-token float32 cos/sin [token][head_dim/2]
+ * (token = row + row_offset, frame-major), composed on the host from the float64
+ * per-axis tables (pairs [0,pt) frame axis, [pt,pt+ph) row axis, rest column axis). */
 typedef struct ftb_rope3d {
-  const float* cos_t; const float* sin_t;
-  const float* cos_h; const float* sin_h;
-  const float* cos_w; const float* sin_w;
-  int32_t pairs_t, pairs_h, pairs_w;
-  int32_t grid_h, grid_w; /* token grid of one latent frame */
+  const float* cos_full;
+  const float* sin_full;
 } ftb_rope3d;
 
 typedef struct ftb_epilogue {

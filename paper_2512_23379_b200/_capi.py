@@ -22,8 +22,7 @@ vp, i32, i64, f32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint64
 
 
 class Rope3D(C.Structure):
-    _fields_ = [("cos_t", vp), ("sin_t", vp), ("cos_h", vp), ("sin_h", vp), ("cos_w", vp), ("sin_w", vp),
-                ("pairs_t", i32), ("pairs_h", i32), ("pairs_w", i32), ("grid_h", i32), ("grid_w", i32)]
+    _fields_ = [("cos_full", vp), ("sin_full", vp)]
 
 
 class Epilogue(C.Structure):

@@ -48,32 +48,6 @@ struct GemmCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-__device__ __forceinline__ void rope_rotate(const GemmParams& p, long long token, int pair, float& x0, float& x1) {
-  const ftb_rope3d& r = p.rope;
-  int tpf = r.grid_h * r.grid_w;
-  int f = (int)(token / tpf);
-  int rem = (int)(token - (long long)f * tpf);
-  int y = rem / r.grid_w;
-  int x = rem - y * r.grid_w;
-  float c, s;
-  if (pair < r.pairs_t) {
-    c = __ldg(r.cos_t + (long long)f * r.pairs_t + pair);
-    s = __ldg(r.sin_t + (long long)f * r.pairs_t + pair);
-  } else if (pair < r.pairs_t + r.pairs_h) {
-    int q = pair - r.pairs_t;
-    c = __ldg(r.cos_h + (long long)y * r.pairs_h + q);
-    s = __ldg(r.sin_h + (long long)y * r.pairs_h + q);
-  } else {
-    int q = pair - r.pairs_t - r.pairs_h;
-    c = __ldg(r.cos_w + (long long)x * r.pairs_w + q);
-    s = __ldg(r.sin_w + (long long)x * r.pairs_w + q);
-  }
-  float a = x0 * c - x1 * s;
-  float b = x0 * s + x1 * c;
-  x0 = a;
-  x1 = b;
-}
-
 // Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int gc0, float (&v)[32]) {
   const int N = p.N;
@@ -150,6 +124,46 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
       const int m = p.heads * p.head_dim;
       const long long token = gr + p.row_offset;
       __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(p.out);
+      if (full && (p.head_dim & 31) == 0) {
+        // fast path: the 32 columns lie in one head -> one destination run of 64 bytes
+        const int which = gc0 / m;
+        const int cm = gc0 - which * m;
+        const int h = cm / p.head_dim;
+        const int d0 = cm - h * p.head_dim;
+        if (which < 2 && p.has_rope) {
+          const int half = p.head_dim >> 1;
+          const float4* cs = reinterpret_cast<const float4*>(p.rope.cos_full + token * half + (d0 >> 1));
+          const float4* sn = reinterpret_cast<const float4*>(p.rope.sin_full + token * half + (d0 >> 1));
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 c4 = __ldg(cs + q4), s4 = __ldg(sn + q4);
+            const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = 8 * q4 + 2 * e;
+              const float a = v[j] * cc[e] - v[j + 1] * ss[e];
+              const float b = v[j] * ss[e] + v[j + 1] * cc[e];
+              v[j] = a;
+              v[j + 1] = b;
+            }
+          }
+        }
+        const int dest = h / p.hpr;
+        const int hl = h - dest * p.hpr;
+        uint4* o4 = reinterpret_cast<uint4*>(base + (((long long)dest * p.M + gr) * 3 + which) *
+                                                        ((long long)p.hpr * p.head_dim) +
+                                             (long long)hl * p.head_dim + d0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+          w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+          w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+          w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+          o4[q] = w;
+        }
+        break;
+      }
 #pragma unroll 4
       for (int j = 0; j < 32; j += 2) {
         int c = gc0 + j;
@@ -159,7 +173,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
         int h = cm / p.head_dim;
         int d = cm - h * p.head_dim;
         float x0 = v[j], x1 = v[j + 1];
-        if (which < 2 && p.has_rope) rope_rotate(p, token, d >> 1, x0, x1);
+        if (which < 2 && p.has_rope) {
+          const long long ix = token * (p.head_dim >> 1) + (d >> 1);
+          const float cr = __ldg(p.rope.cos_full + ix), sr = __ldg(p.rope.sin_full + ix);
+          const float a = x0 * cr - x1 * sr;
+          x1 = x0 * sr + x1 * cr;
+          x0 = a;
+        }
         int dest = h / p.hpr;
         int hl = h - dest * p.hpr;
         long long idx = (((long long)dest * p.M + gr) * 3 + which) * ((long long)p.hpr * p.head_dim) +

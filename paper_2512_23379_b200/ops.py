@@ -17,6 +17,7 @@ from .errors import ConfigError
 # Optional per-launch profiler (bench.py roofline pass): list of
 # (kind, start_event, end_event, flops, bytes) or None.
 PROFILER = None
+PROFILE_DETAIL = None  # set to True: per-shape GEMM buckets
 
 
 class _Prof:
@@ -55,14 +56,15 @@ def _need(t, dtype, name):
 
 
 class RopeTables:
-    """Device copy of host-computed 3D RoPE cos/sin tables (see rope.py)."""
+    """Device copy of the host-computed 3D RoPE tables (rope.py), expanded per
+    token: cos/sin [frames*grid_h*grid_w][head_dim/2] float32."""
 
     def __init__(self, tables, grid_h, grid_w, device):
-        self.t = {k: torch.as_tensor(v, dtype=torch.float32).contiguous().to(device) for k, v in tables.items()}
-        self.struct = A.Rope3D(A.ptr(self.t["cos_t"]), A.ptr(self.t["sin_t"]), A.ptr(self.t["cos_h"]),
-                               A.ptr(self.t["sin_h"]), A.ptr(self.t["cos_w"]), A.ptr(self.t["sin_w"]),
-                               self.t["cos_t"].shape[1], self.t["cos_h"].shape[1], self.t["cos_w"].shape[1],
-                               grid_h, grid_w)
+        from .rope import per_token_tables
+        cos, sin = per_token_tables(tables, grid_h, grid_w)
+        self.cos = torch.as_tensor(cos).contiguous().to(device)
+        self.sin = torch.as_tensor(sin).contiguous().to(device)
+        self.struct = A.Rope3D(A.ptr(self.cos), A.ptr(self.sin))
 
 
 def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=0, row_offset=0,
@@ -92,7 +94,7 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
         _need(bias, torch.float32, "bias")
     epi = A.Epilogue(k, rows_per_group, row_offset, A.ptr(bias), A.ptr(group_vec), group_ld, A.ptr(out), ldc,
                      heads, head_dim, heads_per_rank, C.pointer(rope.struct) if rope is not None else None)
-    with _Prof("gemm", 2.0 * M * N * K, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
+    with _Prof("gemm" if PROFILE_DETAIL is None else "gemm:%s:%dx%dx%d" % (kind, M, N, K), 2.0 * M * N * K, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
         A.call("ftb_gemm_bf16", A.ptr(a), lda, a_chunks, a_chunk_stride, A.ptr(w_t), _ld(w_t), M, N, K,
                C.byref(epi), A.stream_ptr(stream))
     return out
@@ -125,7 +127,7 @@ def attention(q, k, v, out, heads, head_dim, Lq, Lk, scale, *, impl=None, stream
             Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))
     if impl is None:
         impl = 0 if (head_dim in (64, 128) and Lq >= 64) else 1
-    kind = "fmha" if impl == 0 else "attn_small"
+    kind = ("fmha" if Lk > 256 else "fmha_short_kv") if impl in (0, 2) else "attn_small"
     with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
         A.call("ftb_attention_impl", int(impl), *args)
     return out

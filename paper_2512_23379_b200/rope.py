@@ -34,3 +34,16 @@ def rope3d_tables(frames: int, grid_h: int, grid_w: int, hd: int, theta: float =
         out["cos_" + ax] = np.cos(ang).astype(np.float32)
         out["sin_" + ax] = np.sin(ang).astype(np.float32)
     return out
+
+
+def per_token_tables(tables: dict, grid_h: int, grid_w: int):
+    """Per-axis tables -> per-token float32 [frames*grid_h*grid_w][hd/2] cos and sin
+    (token order frame-major, then row, then column); a pure gather of the
+    float32-rounded per-axis values, so it stays bit-identical to them."""
+    frames = tables["cos_t"].shape[0]
+    f = np.repeat(np.arange(frames), grid_h * grid_w)
+    y = np.tile(np.repeat(np.arange(grid_h), grid_w), frames)
+    x = np.tile(np.arange(grid_w), frames * grid_h)
+    cos = np.concatenate([tables["cos_t"][f], tables["cos_h"][y], tables["cos_w"][x]], axis=1)
+    sin = np.concatenate([tables["sin_t"][f], tables["sin_h"][y], tables["sin_w"][x]], axis=1)
+    return np.ascontiguousarray(cos, dtype=np.float32), np.ascontiguousarray(sin, dtype=np.float32)

@@ -126,3 +126,20 @@ def test_product_chunk_noise_bit_exact(golden, steps):
     from paper_2512_23379_b200.seeding import chunk_noise
     z = chunk_noise(5, 3, golden["s_steps%d_z" % steps][0].shape)
     assert np.array_equal(z, golden["s_steps%d_z" % steps][0])
+
+
+def test_rope_tables_bit_exact():
+    """Product RoPE tables (host float64 -> float32) equal the oracle's, byte for byte,
+    and the per-token expansion is an exact gather of them."""
+    from oracle import wan_oracle as WO
+    from paper_2512_23379_b200.rope import per_token_tables, rope3d_tables
+    for hd, F, gh, gw in [(128, 10, 26, 45), (64, 4, 6, 9), (16, 3, 2, 2)]:
+        a, b = rope3d_tables(F, gh, gw, hd), WO.rope_tables(F, gh, gw, hd)
+        for k in a:
+            assert a[k].dtype == np.float32 and a[k].tobytes() == b[k].tobytes(), (hd, k)
+        cos, sin = per_token_tables(a, gh, gw)
+        assert cos.shape == (F * gh * gw, hd // 2)
+        r, c = min(5, gh - 1), min(3, gw - 1)
+        t = gh * gw + r * gw + c  # frame 1, row r, col c
+        assert np.array_equal(cos[t], np.concatenate([a["cos_t"][1], a["cos_h"][r], a["cos_w"][c]]))
+        assert np.array_equal(sin[t], np.concatenate([a["sin_t"][1], a["sin_h"][r], a["sin_w"][c]]))
