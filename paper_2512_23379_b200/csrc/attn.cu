@@ -279,29 +279,31 @@ struct Fmha2Cfg {
   static constexpr int BOX = 128 * 64 * 2;               // 128 rows x 64 cols bf16
   static constexpr int NBOX = HD / 64;
   static constexpr int TILE = NBOX * BOX;                // 128 rows x HD
+  static constexpr int SLOTS = (HD == 128) ? 4 : 6;      // K/V ring depth
   static constexpr int OFF_Q = 0;                        // 2 tiles
-  static constexpr int OFF_KV = OFF_Q + 2 * TILE;        // 3-slot ring (K or V blocks)
-  static constexpr int OFF_P = OFF_KV + 3 * TILE;        // 2 x (128 x 128 bf16)
-  static constexpr int OFF_BAR = OFF_P + 2 * 2 * BOX;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_KV = OFF_Q + 2 * TILE;
+  static constexpr int OFF_BAR = OFF_KV + SLOTS * TILE;
+  static constexpr int SMEM = OFF_BAR + 512 + 1024;
 };
 
+// TMEM map (512 columns): S_t fp32 at [128t, 128t+128) with P_t (bf16 pairs) aliased onto
+// its first 64 columns; O_t fp32 at [256 + 128t, 256 + 128t + HD).
 template <int HD>
 __global__ void __launch_bounds__(384, 1)
     fmha2_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
   using C = Fmha2Cfg<HD>;
+  constexpr int NS = C::SLOTS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [3]
-  uint64_t* kv_empty = bars + 4;  // [3]
-  uint64_t* s_full = bars + 7;    // [2] per tile
-  uint64_t* s_empty = bars + 9;   // [2]
-  uint64_t* p_full = bars + 11;   // [2]
-  uint64_t* o_done = bars + 13;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* kv_full = bars + 1;         // [NS]
+  uint64_t* kv_empty = bars + 1 + NS;   // [NS]
+  uint64_t* s_full = bars + 1 + 2 * NS; // [2] per tile
+  uint64_t* p_full = s_full + 2;        // [2]
+  uint64_t* o_done = s_full + 4;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
 
   const int warp = warp_id(), lane = lane_id();
   const int qblk = blockIdx.x, head = blockIdx.y;
@@ -312,13 +314,12 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 3; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&s_empty[t], 4);
       mbar_init(&p_full[t], 4);
       mbar_init(&o_done[t], 1);
     }
@@ -338,8 +339,8 @@ __global__ void __launch_bounds__(384, 1)
         for (int b = 0; b < C::NBOX; ++b)
           tma_load_2d(smem + C::OFF_Q + t * C::TILE + b * C::BOX, &tmQ, q_full, col0 + 64 * b, qblk * 256 + t * 128);
       for (int i = 0; i < 2 * n_kv; ++i) {  // item 2j = K_j, 2j+1 = V_j
-        const int slot = i % 3;
-        mbar_wait(&kv_empty[slot], ((i / 3) & 1) ^ 1);
+        const int slot = i % NS;
+        mbar_wait(&kv_empty[slot], ((i / NS) & 1) ^ 1);
         mbar_arrive_expect_tx(&kv_full[slot], C::TILE);
         const CUtensorMap* tm = (i & 1) ? &tmV : &tmK;
         for (int b = 0; b < C::NBOX; ++b)
@@ -351,10 +352,10 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
-      auto wait_item = [&](int i) { mbar_wait(&kv_full[i % 3], (i / 3) & 1); };
+      auto wait_item = [&](int i) { mbar_wait(&kv_full[i % NS], (i / NS) & 1); };
       auto issue_s = [&](int t, int j) {
         const uint32_t sq = smem_u32(smem + C::OFF_Q + t * C::TILE);
-        const uint32_t sk = smem_u32(smem + C::OFF_KV + ((2 * j) % 3) * C::TILE);
+        const uint32_t sk = smem_u32(smem + C::OFF_KV + ((2 * j) % NS) * C::TILE);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::BOX + (kk & 3) * 32;
@@ -363,14 +364,12 @@ __global__ void __launch_bounds__(384, 1)
         }
         mma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int j) {
-        const uint32_t sp = smem_u32(smem + C::OFF_P + t * 2 * C::BOX);
-        const uint32_t sv = smem_u32(smem + C::OFF_KV + ((2 * j + 1) % 3) * C::TILE);
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t (TMEM) . V_j (smem, MN-major)
+        const uint32_t sv = smem_u32(smem + C::OFF_KV + ((2 * j + 1) % NS) * C::TILE);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t ad = sdesc_sw128(sp + (kk >> 2) * C::BOX + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = sdesc_sw128(sv + kk * 16 * 128, C::BOX, 1024);
-          mma_bf16_ss(tmem + 256 + t * 128, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&o_done[t]);
       };
@@ -380,6 +379,8 @@ __global__ void __launch_bounds__(384, 1)
       issue_s(0, 0);
       issue_s(1, 0);
       mma_commit(&kv_empty[0]);  // K_0 consumed by both tiles
+      // Per block: PV_0(j), S_0(j+1), PV_1(j), S_1(j+1). S_t(j+1) overwrites the TMEM that
+      // holds P_t(j), so it is issued after PV_t(j) (tcgen05 ops of a CTA execute in order).
       for (int j = 0; j < n_kv; ++j) {
         wait_item(2 * j + 1);  // V_j
         mbar_wait(&p_full[0], j & 1);
@@ -387,19 +388,15 @@ __global__ void __launch_bounds__(384, 1)
         issue_pv(0, j);
         if (j + 1 < n_kv) {
           wait_item(2 * j + 2);  // K_{j+1}
-          mbar_wait(&s_empty[0], j & 1);
-          tc_fence_after();
           issue_s(0, j + 1);
         }
         mbar_wait(&p_full[1], j & 1);
         tc_fence_after();
         issue_pv(1, j);
-        mma_commit(&kv_empty[(2 * j + 1) % 3]);  // V_j consumed
+        mma_commit(&kv_empty[(2 * j + 1) % NS]);  // V_j consumed
         if (j + 1 < n_kv) {
-          mbar_wait(&s_empty[1], j & 1);
-          tc_fence_after();
           issue_s(1, j + 1);
-          mma_commit(&kv_empty[(2 * j + 2) % 3]);  // K_{j+1} consumed
+          mma_commit(&kv_empty[(2 * j + 2) % NS]);  // K_{j+1} consumed by both tiles
         }
       }
     }
@@ -410,7 +407,6 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_off = (uint32_t)(qw * 32) << 16;
     const uint32_t tS = tmem + lane_off + t * 128;
     const uint32_t tO = tmem + lane_off + 256 + t * 128;
-    uint8_t* prow = smem + C::OFF_P + t * 2 * C::BOX + row * 128;
     float m_ref = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
       mbar_wait(&s_full[t], j & 1);
@@ -421,9 +417,6 @@ __global__ void __launch_bounds__(384, 1)
       tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
       tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[t]);
       const int valid = p.Lk - j * 128;
       if (valid < 128) {
 #pragma unroll
@@ -450,8 +443,7 @@ __global__ void __launch_bounds__(384, 1)
       const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
       const float2 nm2 = make_float2(-m_use, -m_use);
       float2 rs2 = make_float2(0.f, 0.f);
-      if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);
-      tc_fence_after();
+      // P_t (bf16 pairs) overwrites the first 64 columns of S_t: pack in place in sr[0..63]
 #pragma unroll
       for (int ch = 0; ch < 16; ++ch) {
         float2 e[4];
@@ -468,15 +460,14 @@ __global__ void __launch_bounds__(384, 1)
           }
           rs2 = fadd2(rs2, e[u]);
         }
-        uint4 w;
-        w.x = pack_bf16(e[0].x, e[0].y);
-        w.y = pack_bf16(e[1].x, e[1].y);
-        w.z = pack_bf16(e[2].x, e[2].y);
-        w.w = pack_bf16(e[3].x, e[3].y);
-        const int atom = ch >> 3, c16 = ch & 7;
-        *reinterpret_cast<uint4*>(prow + atom * C::BOX + ((c16 ^ (row & 7)) << 4)) = w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sr[ch * 4 + u] = pack_bf16(e[u].x, e[u].y);
       }
       const float rs = rs2.x + rs2.y;
+      if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) done: O_t stable
+      tc_fence_after();
+      tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
+      tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
       if (__any_sync(0xffffffffu, rescale)) {
         const float f = rescale ? ex2(m_ref - m_use) : 1.f;
         l *= f;
@@ -489,11 +480,10 @@ __global__ void __launch_bounds__(384, 1)
           for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * f);
           tmem_st32(tO + c0, o);
         }
-        tmem_st_wait();
       }
+      tmem_st_wait();
       l += rs;
       m_ref = m_use;
-      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
