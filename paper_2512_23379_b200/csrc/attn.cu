@@ -330,7 +330,10 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
+  // Register budget: the producer / MMA warpgroup gives registers to the two softmax
+  // warpgroups (128*96 + 256*200 <= 384*168: inc blocks until the pool has them), which keeps a whole 128-column S row resident.
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
   if (warp == 0) {
     if (lane == 0) {
       const int col0 = head * HD;
@@ -400,7 +403,9 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
     const int t = (warp - 4) >> 2;  // tile handled by this warpgroup
     const int qw = warp & 3;
     const int row = qw * 32 + lane;
