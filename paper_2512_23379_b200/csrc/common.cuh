@@ -276,11 +276,17 @@ FTB_DEV float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+FTB_DEV float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));  // MUFU.TANH, rel. err ~2^-11 (output is bf16)
+  return y;
+}
 FTB_DEV float gelu_tanh(float x) {
   // 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))  (backends/reference.py:28-31)
   const float c = 0.7978845608028654f;
-  float u = c * (x + 0.044715f * x * x * x);
-  return 0.5f * x * (1.f + tanhf(u));
+  const float u = c * fmaf(0.044715f * x, x * x, x);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_fast(u), hx);
 }
 FTB_DEV uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
