@@ -229,25 +229,38 @@ class DeviceDenoiser:
         return out
 
     # ------------------------------------------------------------ conditioning (once per chunk)
-    def prepare_cond(self, signal, reference):
-        """cond = [sig tokens + frame pos ; ref token] (net.py:233-237) and the
-        per-layer cross-attention K|V projections of it (cond does not change
-        across the sampler's steps, so K/V are computed once per chunk)."""
-        cfg, B, W = self.cfg, self.buf, self.w
+    def stage_cond(self, signal, reference, k=0):
+        """Host half of the conditioning: driving window + reference token written
+        (bf16) into pinned staging buffer k (two, so chunk c+1 stages while c copies)."""
+        cfg = self.cfg
         nsig = self.n_cond - 1
-        ci = B["cond_in"]
-        ci.zero_()
+        stages = getattr(self, "_cond_stage", None)
+        if stages is None:
+            stages = [torch.zeros(self.buf["cond_in"].shape, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+            self._cond_stage = stages
+        st = stages[k]
         if cfg.mode == "ftlk":
             sig = torch.as_tensor(np.asarray(signal, dtype=np.float64).reshape(self.Lc, 1), dtype=torch.float32)
             ref = torch.as_tensor(np.asarray(reference, dtype=np.float64).reshape(1, -1), dtype=torch.float32)
-            A = 1
         else:
             sig = torch.as_tensor(np.asarray(signal, dtype=np.float32).reshape(nsig, cfg.audio_dim))
             ref_lat = np.asarray(reference, dtype=np.float64).reshape(cfg.latent_dim, -1)
             ref = torch.as_tensor(ref_lat.mean(axis=1).reshape(1, -1), dtype=torch.float32)
-            A = cfg.audio_tokens
-        ci[:nsig, :sig.shape[1]].copy_(sig.to(torch.bfloat16))
-        ci[nsig:, :ref.shape[1]].copy_(ref.to(torch.bfloat16))
+        st.zero_()
+        st[:nsig, :sig.shape[1]].copy_(sig.to(torch.bfloat16))
+        st[nsig:, :ref.shape[1]].copy_(ref.to(torch.bfloat16))
+
+    def copy_cond_in(self, k=0):
+        """H2D of staging buffer k into the device cond input (stream-ordered)."""
+        self.buf["cond_in"].copy_(self._cond_stage[k], non_blocking=True)
+
+    def upload_cond(self):
+        """Device half: cond input -> cond tokens (sig + frame pos ; ref) and the
+        per-layer cross-attention K|V (net.py:233-237). Capturable in a CUDA graph."""
+        cfg, B, W = self.cfg, self.buf, self.w
+        nsig = self.n_cond - 1
+        ci = B["cond_in"]
+        A = cfg.audio_tokens if cfg.mode == "wan" else 1
         ops.gemm(ci[:nsig], W.mats["sig.w"][0], B["cond"][:nsig], "rowadd_f32", bias=W.vecs["sig.b"],
                  group_vec=self.pos, rows_per_group=A, M=nsig, K=W.mats["sig.w"][1], lda=ci.stride(0),
                  stream=self.stream)
@@ -256,6 +269,13 @@ class DeviceDenoiser:
         ops.cast_f32_bf16(B["cond"], B["cond_bf"], stream=self.stream)
         for i in range(cfg.layers):
             ops.gemm(B["cond_bf"], W.mats["layers.%d.cross.wkv" % i][0], B["ckv"][i], "bf16", stream=self.stream)
+
+    def prepare_cond(self, signal, reference):
+        """cond = [sig tokens + frame pos ; ref token] and per-layer cross K|V
+        (once per chunk: cond does not change across the sampler's steps)."""
+        self.stage_cond(signal, reference, 0)
+        self.copy_cond_in(0)
+        self.upload_cond()
 
     # ------------------------------------------------------------ one denoise step
     def step(self, motion, z, reference, fv, x0_out=None, ddim=None):

@@ -70,7 +70,7 @@ class DeviceStreamer:
     """Device state of one stream: denoiser at the stream geometry, motion
     cache, sampler state, and the codec. Used by StreamSession and generate()."""
 
-    def __init__(self, runner, cfg: StreamConfig, codec, reference_latent, latent_hw=(1, 1)):
+    def __init__(self, runner, cfg: StreamConfig, codec, reference_latent, latent_hw=(1, 1), use_graph=True):
         self.runner, self.scfg, self.codec = runner, cfg, codec
         self.ncfg = runner.cfg
         self.dev = runner.device
@@ -84,35 +84,99 @@ class DeviceStreamer:
         self.motion = self.ref.unsqueeze(0).repeat(lm, 1, 1, 1).contiguous() if lm else None
         nt = cfg.stride
         self.z = torch.empty((nt,) + self.fshape, dtype=torch.float32, device=self.dev)
-        self.noise_host = torch.empty((nt,) + self.fshape, dtype=torch.float32).pin_memory()
+        self.noise_host = [torch.empty((nt,) + self.fshape, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.x0_static = torch.empty((nt,) + self.fshape, dtype=torch.float32, device=self.dev)
         self.slots = [torch.empty((nt,) + self.fshape, dtype=torch.float32, device=self.dev) for _ in range(4)]
         self.slot = 0
+        self._k = 0
+        self._h2d_ev = [None, None]
+        self.use_graph = use_graph and self.d.comm.world == 1
+        self.graph = None
+        self.graph_launches = 0
+        self._eager_runs = 0
 
     def reset(self):
         lm = self.scfg.motion_len
         if lm:
             self.motion.copy_(self.ref.unsqueeze(0).expand(lm, *self.fshape))
 
+    def _device_chunk(self):
+        """All device work of one chunk after the H2D of its inputs: cond tokens and
+        cross K/V, the 4-step ladder, the motion-cache update. CUDA-graph capturable."""
+        cfg = self.scfg
+        nt, lm = cfg.stride, cfg.motion_len
+        self.d.upload_cond()
+        self.d.sample(self.motion, self.ref, self.z, cfg.sampler, self.x0_static)
+        if lm:
+            if lm <= nt:
+                self.motion.copy_(self.x0_static[nt - lm:])
+            else:  # carried rows still include older motion rows
+                keep = lm - nt
+                self.motion.copy_(torch.cat([self.motion[lm - keep:], self.x0_static], 0))
+
+    def _capture(self):
+        """Capture _device_chunk once (after an eager warm-up filled the per-ladder
+        caches); later chunks replay it: one launch instead of ~450 per step."""
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream())
+        keep = self.d.stream
+        self.d.stream = None
+        g = torch.cuda.CUDAGraph()
+        from . import _capi
+        n0 = _capi.LAUNCHES[0]
+        try:
+            with torch.cuda.graph(g, stream=s):
+                self._device_chunk()
+        finally:
+            self.d.stream = keep
+        self.graph_launches = _capi.LAUNCHES[0] - n0   # kernels per replay (bench gpu_launches)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+
+    def run_resident(self, z_dev, cond_in_dev):
+        """Chunk with inputs already in HBM (benchmark `value`): D2D into the static
+        input buffers, then the captured graph (or the eager path before capture)."""
+        self.z.copy_(z_dev)
+        self.d.buf["cond_in"].copy_(cond_in_dev)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._device_chunk()
+            self._eager_runs += 1
+            if self.use_graph and self._eager_runs == 1:
+                self._capture()
+        return self.x0_static
+
     def denoise_chunk(self, c, window, noise=None):
         """Runs chunk c on the current stream; returns the device x0 slot
-        (targets). `noise` (host f64) defaults to the reference draw."""
+        (targets). `noise` (host f64) defaults to the reference draw. Inputs are
+        staged in pinned memory (double-buffered) and copied H2D in stream order."""
         cfg = self.scfg
         nt = cfg.stride
         if noise is None:
             noise = chunk_noise(cfg.seed, c, (nt,) + self.ref_host.shape)
-        self.noise_host.copy_(torch.from_numpy(np.asarray(noise, dtype=np.float32).reshape(self.noise_host.shape)))
-        self.z.copy_(self.noise_host, non_blocking=True)
-        self.d.prepare_cond(window, self.ref_host)
+        k = self._k
+        self._k ^= 1
+        if self._h2d_ev[k] is not None:
+            self._h2d_ev[k].synchronize()   # staging buffer k no longer read by chunk c-2's copy
+        self.noise_host[k].copy_(torch.from_numpy(np.asarray(noise, dtype=np.float32).reshape(self.fshape[:0] + (
+            nt,) + self.fshape)))
+        self.d.stage_cond(window, self.ref_host, k)
+        self.z.copy_(self.noise_host[k], non_blocking=True)
+        self.d.copy_cond_in(k)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self._h2d_ev[k] = ev
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._device_chunk()
+            self._eager_runs += 1
+            if self.use_graph and self._eager_runs == 1:
+                self._capture()
         x0 = self.slots[self.slot]
         self.slot = (self.slot + 1) % len(self.slots)
-        self.d.sample(self.motion, self.ref, self.z, cfg.sampler, x0)
-        lm = cfg.motion_len
-        if lm:
-            if lm <= nt:
-                self.motion.copy_(x0[nt - lm:])
-            else:  # carried rows still include older motion rows
-                keep = lm - nt
-                self.motion.copy_(torch.cat([self.motion[lm - keep:], x0], 0))
+        x0.copy_(self.x0_static)
         return x0
 
 
