@@ -268,9 +268,202 @@ static int launch_conv(const void* in, int T_in, const void* w_t, const ConvPara
   return check_launch("conv_tc_kernel");
 }
 
+// ---------------------------------------------------------------------------------------
+// 3x3 (x KT) variant with dx reuse: per (dt, dy, channel block) ONE haloed TMA box of 130
+// pixels (x0-1 .. x0+128) feeds the three dx taps as row-shifted smem views (UMMA
+// descriptor start + dx*128 B; the 128B-swizzle XOR follows absolute smem address bits, so
+// the shifted views need no base offset — verified on B200), cutting
+// the A-operand L2 traffic 3x. BK = 64 (SWIZZLE_128B); B holds the three taps' weights.
+constexpr int DXR_AROWS = 130;
+
+template <int BN, int BK>
+struct DxrCfg {
+  static constexpr int ROW = BK * 2;                      // bytes per pixel row of a k-block
+  static constexpr int A_BYTES = (DXR_AROWS * ROW + 1023) / 1024 * 1024;
+  static constexpr int B_TAP = BN * ROW;
+  static constexpr int STAGE_BYTES = A_BYTES + 3 * B_TAP;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 4u;  // SWIZZLE_128B / SWIZZLE_64B
+  static constexpr uint32_t SBO = 8 * ROW;
+};
+
+
+template <int BN, int BK>
+__global__ void __launch_bounds__(256, 1)
+    conv_dxr_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const ConvParams p) {
+  using C = DxrCfg<BN, BK>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int num_m = p.T * p.H * p.num_xt;
+  const int num_n = (p.Cout + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int rows = p.KT * 3;                  // (dt, dy) pairs
+  const int num_kb = rows * p.kb_per_tap;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+        const int xt = m_blk % p.num_xt;
+        const int ty = m_blk / p.num_xt;
+        const int y = ty % p.H, t = ty / p.H;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int r = kb / p.kb_per_tap, cb = kb - r * p.kb_per_tap;
+          const int dy = r % 3, dt = r / 3;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], DXR_AROWS * C::ROW + 3 * C::B_TAP);
+          tma_load_4d(sa, &tmA, &full_bar[stage], cb * BK, xt * 128 - 1, y + dy - 1, t + dt + p.t0);
+          const int tap0 = (dt * 3 + dy) * 3;
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx)
+            tma_load_2d(sb + dx * C::B_TAP, &tmB, &full_bar[stage], (tap0 + dx) * p.Cin + cb * BK, n_blk * BN);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss(tmem_d, sdesc(sa + dx * C::ROW + k * 32, 16, C::SBO, C::LAYOUT),
+                          sdesc(sb + dx * C::B_TAP + k * 32, 16, C::SBO, C::LAYOUT), idesc, (kb | dx | k) ? 1u : 0u);
+          mma_commit(&empty_bar[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull_bar[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+      const int xt = m_blk % p.num_xt;
+      const int ty = m_blk / p.num_xt;
+      const int y = ty % p.H, t = ty / p.H;
+      const int x = xt * 128 + q * 32 + lane;
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int gc0 = n_blk * BN + c0;
+        if (gc0 >= p.Cout) break;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (x < p.W) conv_epilogue(p, t, y, x, gc0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+template <int BN, int BK>
+static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s) {
+  using C = DxrCfg<BN, BK>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(conv_dxr_kernel<BN, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "conv_dxr smem attribute");
+    configured = true;
+  }
+  CUtensorMap ta, tb;
+  {
+    uint64_t dims[4] = {(uint64_t)p.Cin, (uint64_t)p.W, (uint64_t)p.H, (uint64_t)T_in};
+    uint64_t strides[3] = {(uint64_t)p.Cin * 2, (uint64_t)p.W * p.Cin * 2, (uint64_t)p.H * p.W * p.Cin * 2};
+    uint32_t box[4] = {BK, DXR_AROWS, 1, 1};
+    int rc = make_tmap_bf16(&ta, in, 4, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  {
+    const long long ktot = (long long)p.taps * p.Cin;
+    uint64_t dims[2] = {(uint64_t)ktot, (uint64_t)p.Cout};
+    uint64_t strides[1] = {(uint64_t)ktot * 2};
+    uint32_t box[2] = {BK, BN};
+    int rc = make_tmap_bf16(&tb, w_t, 2, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  const int tiles = p.T * p.H * p.num_xt * ((p.Cout + BN - 1) / BN);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  conv_dxr_kernel<BN, BK><<<grid, 256, C::SMEM, s>>>(ta, tb, p);
+  return check_launch("conv_dxr_kernel");
+}
+
 }  // namespace ftb
 
 using namespace ftb;
+
+static int g_conv_variant = 0;  // 0 auto (dx reuse for 3x3 taps), 1 per-tap kernel
+extern "C" int ftb_set_conv_variant(int32_t v) {
+  if (v < 0 || v > 1) return set_error(FTB_EINVAL, "conv variant must be 0 (auto) or 1 (per-tap)");
+  g_conv_variant = v;
+  return FTB_OK;
+}
 
 extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t W, int32_t Cin, const void* w_t,
                                int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0, const float* bias,
@@ -310,6 +503,19 @@ extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t 
   p.mode = mode;
   p.out_f32 = out_f32;
   p.resid_f32 = resid_f32;
+  if (g_conv_variant != 1 && KH == 3 && KW == 3 && Cin % 32 == 0) {
+    cudaStream_t s0 = reinterpret_cast<cudaStream_t>(stream);
+    if (Cin % 64 == 0) {
+      p.kb_per_tap = Cin / 64;
+      if (Cout <= 32) return launch_conv_dxr<32, 64>(in, T_in, w_t, p, s0);
+      if (Cout <= 96) return launch_conv_dxr<96, 64>(in, T_in, w_t, p, s0);
+      return launch_conv_dxr<192, 64>(in, T_in, w_t, p, s0);
+    }
+    p.kb_per_tap = Cin / 32;
+    if (Cout <= 32) return launch_conv_dxr<32, 32>(in, T_in, w_t, p, s0);
+    if (Cout <= 96) return launch_conv_dxr<96, 32>(in, T_in, w_t, p, s0);
+    return launch_conv_dxr<192, 32>(in, T_in, w_t, p, s0);
+  }
   const bool bk32 = (Cin % 64) != 0 && (Cin % 32) == 0;
   const int BK = (Cin <= 32 || bk32) ? 32 : 64;
   p.kb_per_tap = (Cin + BK - 1) / BK;

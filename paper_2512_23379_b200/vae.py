@@ -232,7 +232,8 @@ class DeviceVAEDecoder:
     def _conv(self, inp, T_in, H, W, Cin, cw, out, out_ld, t0, mode, resid, resid_ld, T_out, stream):
         kt, kh, kw = cw.k
         cout = cw.cout if (mode & 15) != 0 or cw.cout % 32 == 0 else cw.wt.shape[0]
-        with ops._Prof("conv", 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
+        tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%dx%d %d->%d k%d%d%d" % (T_out, H, W, 0, Cin, cw.cout, kt, kh, kw)
+        with ops._Prof(tag, 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
             A.call("ftb_conv3d_bf16", A.ptr(inp), T_in, H, W, Cin, A.ptr(cw.wt), cout, kt, kh, kw, t0,
                    A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld, T_out, mode, A.stream_ptr(stream))
 

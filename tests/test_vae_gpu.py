@@ -26,12 +26,17 @@ CONV_CASES = [  # T_out, H, W, Cin, Cout, k
     (3, 6, 9, 64, 128, (3, 1, 1)),
     (2, 5, 260, 32, 64, (1, 3, 3)),
     (2, 4, 33, 128, 64, (1, 1, 1)),
+    (3, 6, 150, 64, 96, (3, 3, 3)),      # dx-reuse kernel (Cin % 64 == 0, 3x3 taps)
+    (2, 4, 90, 128, 192, (1, 3, 3)),
+    (2, 3, 33, 384, 384, (3, 3, 3)),
 ]
 
 
+@pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("T,H,W,Cin,Cout,k", CONV_CASES)
-def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k):
+def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k, variant):
     from paper_2512_23379_b200 import _capi as A
+    A.call("ftb_set_conv_variant", variant)
     r = np.random.default_rng(T * 100 + W)
     kt = k[0]
     x = bfr(r.standard_normal((T + kt - 1, H, W, Cin)))
@@ -46,6 +51,7 @@ def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k):
     out = torch.empty(T, H, W, Cout, dtype=torch.bfloat16, device=cuda)
     A.call("ftb_conv3d_bf16", A.ptr(xd), T + kt - 1, H, W, Cin, A.ptr(wt), Cout, *k, 0, A.ptr(bd), A.ptr(rd),
            Cout, A.ptr(out), Cout, T, 0, A.stream_ptr())
+    A.call("ftb_set_conv_variant", 0)
     assert rel(out.float().cpu().numpy(), want) < 8e-3
 
 
