@@ -197,9 +197,9 @@ def main():
     windows = [rng.standard_normal((Lc, A, adim)) if cfg.mode == "wan" else rng.uniform(-1, 1, Lc)
                for _ in range(nsteps)]
     vae = None
-    if cfg.mode == "wan" and not args.no_decode and rank == 0:   # decode on rank 0 (spatial split: DESIGN 7)
+    if cfg.mode == "wan" and not args.no_decode:   # N > 1: spatially split decode with halo exchange
         from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig
-        vae = DeviceVAEDecoder(VAEConfig(z_dim=cfg.latent_dim), dev, params=None, seed=201, rgb8=True)
+        vae = DeviceVAEDecoder(VAEConfig(z_dim=cfg.latent_dim), dev, params=None, seed=201, rgb8=True, comm=comm)
 
     from paper_2512_23379_b200.streaming import DeviceStreamer
 

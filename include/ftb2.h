@@ -147,6 +147,13 @@ int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t W, int32_t 
                     const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0,
                     const float* bias, const void* resid, int64_t resid_ld,
                     void* out, int64_t out_ld, int32_t T_out, int32_t mode, void* stream);
+/* Spatially split decode: as ftb_conv3d_bf16 (3x3 spatial kernels) but input rows -1 and H come
+ * from halo_top / halo_bot, each [T_in][1][W][Cin] bf16 (the neighbour ranks' edge rows, or zeros
+ * at the global edge) instead of zero padding. */
+int ftb_conv3d_halo_bf16(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in, int32_t H,
+                         int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW,
+                         int32_t t0, const float* bias, const void* resid, int64_t resid_ld, void* out,
+                         int64_t out_ld, int32_t T_out, int32_t mode, void* stream);
 /* Conv kernel variant: 0 auto (one haloed TMA box per (dt,dy) feeds the 3 dx taps when KH=KW=3 and
  * Cin % 64 == 0), 1 per-tap boxes. */
 int ftb_set_conv_variant(int32_t variant);

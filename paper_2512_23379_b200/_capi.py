@@ -54,6 +54,8 @@ _SIGS = {
     "ftb_add_bcast_f32": ([vp, i64, i64, vp, i64, vp, vp], i32),
     "ftb_conv3d_bf16": ([vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, vp, vp, i64, vp, i64, i32, i32, vp],
                         i32),
+    "ftb_conv3d_halo_bf16": ([vp, vp, vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, vp, vp, i64, vp, i64, i32,
+                              i32, vp], i32),
     "ftb_rmsnorm_silu_bf16": ([vp, i64, i32, vp, f32, i32, vp, vp], i32),
     "ftb_upsample2x_bf16": ([vp, i32, i32, i32, i32, vp, vp], i32),
     "ftb_nchw_to_nhwc_bf16": ([vp, i32, i32, i32, i32, vp, i32, vp], i32),

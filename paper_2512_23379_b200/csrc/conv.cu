@@ -29,6 +29,7 @@ struct ConvParams {
   int mode;       // 0 store, 1 time split, 2 RGB8
   int out_f32;    // mode bit 4: fp32 output
   int resid_f32;  // mode bit 5: fp32 residual
+  int halo;       // dx-reuse kernel: rows -1 / H come from the halo maps (spatial split)
 };
 
 template <int BN, int BK>
@@ -293,6 +294,7 @@ struct DxrCfg {
 template <int BN, int BK>
 __global__ void __launch_bounds__(256, 1)
     conv_dxr_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmTop, const __grid_constant__ CUtensorMap tmBot,
                     const ConvParams p) {
   using C = DxrCfg<BN, BK>;
   extern __shared__ uint8_t smem_raw[];
@@ -345,7 +347,13 @@ __global__ void __launch_bounds__(256, 1)
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
           mbar_arrive_expect_tx(&full_bar[stage], DXR_AROWS * C::ROW + 3 * C::B_TAP);
-          tma_load_4d(sa, &tmA, &full_bar[stage], cb * BK, xt * 128 - 1, y + dy - 1, t + dt + p.t0);
+          const int row = y + dy - 1;
+          if (p.halo && row < 0)          // neighbour's last row (or zeros at the global edge)
+            tma_load_4d(sa, &tmTop, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
+          else if (p.halo && row >= p.H)  // neighbour's first row
+            tma_load_4d(sa, &tmBot, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
+          else
+            tma_load_4d(sa, &tmA, &full_bar[stage], cb * BK, xt * 128 - 1, row, t + dt + p.t0);
           const int tap0 = (dt * 3 + dy) * 3;
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx)
@@ -424,7 +432,8 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 template <int BN, int BK>
-static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s) {
+static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s,
+                           const void* halo_top = nullptr, const void* halo_bot = nullptr) {
   using C = DxrCfg<BN, BK>;
   static bool configured = false;
   if (!configured) {
@@ -450,7 +459,16 @@ static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const Conv
   }
   const int tiles = p.T * p.H * p.num_xt * ((p.Cout + BN - 1) / BN);
   const int grid = tiles < sm_count() ? tiles : sm_count();
-  conv_dxr_kernel<BN, BK><<<grid, 256, C::SMEM, s>>>(ta, tb, p);
+  CUtensorMap ttop = ta, tbot = ta;
+  if (p.halo) {  // halo rows: [T_in][1][W][Cin] each
+    uint64_t dims[4] = {(uint64_t)p.Cin, (uint64_t)p.W, 1, (uint64_t)T_in};
+    uint64_t strides[3] = {(uint64_t)p.Cin * 2, (uint64_t)p.W * p.Cin * 2, (uint64_t)p.W * p.Cin * 2};
+    uint32_t box[4] = {BK, DXR_AROWS, 1, 1};
+    int rc = make_tmap_bf16(&ttop, halo_top, 4, dims, strides, box, BK * 2);
+    if (!rc) rc = make_tmap_bf16(&tbot, halo_bot, 4, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  conv_dxr_kernel<BN, BK><<<grid, 256, C::SMEM, s>>>(ta, tb, ttop, tbot, p);
   return check_launch("conv_dxr_kernel");
 }
 
@@ -465,7 +483,8 @@ extern "C" int ftb_set_conv_variant(int32_t v) {
   return FTB_OK;
 }
 
-extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t W, int32_t Cin, const void* w_t,
+static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in, int32_t H,
+                       int32_t W, int32_t Cin, const void* w_t,
                                int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0, const float* bias,
                                const void* resid, int64_t resid_ld, void* out, int64_t out_ld, int32_t T_out,
                                int32_t mode, void* stream) {
@@ -503,18 +522,22 @@ extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t 
   p.mode = mode;
   p.out_f32 = out_f32;
   p.resid_f32 = resid_f32;
-  if (g_conv_variant != 1 && KH == 3 && KW == 3 && Cin % 32 == 0) {
+  p.halo = halo_top != nullptr;
+  if (p.halo && (!halo_bot || KH != 3 || KW != 3 || Cin % 32))
+    return set_error(FTB_EINVAL, "conv3d: halo rows need a 3x3 kernel, both halo buffers and Cin % 32 == 0");
+  if ((g_conv_variant != 1 || p.halo) && KH == 3 && KW == 3 && Cin % 32 == 0) {
     cudaStream_t s0 = reinterpret_cast<cudaStream_t>(stream);
+    const void *ht = halo_top, *hb = halo_bot;
     if (Cin % 64 == 0) {
       p.kb_per_tap = Cin / 64;
-      if (Cout <= 32) return launch_conv_dxr<32, 64>(in, T_in, w_t, p, s0);
-      if (Cout <= 96) return launch_conv_dxr<96, 64>(in, T_in, w_t, p, s0);
-      return launch_conv_dxr<192, 64>(in, T_in, w_t, p, s0);
+      if (Cout <= 32) return launch_conv_dxr<32, 64>(in, T_in, w_t, p, s0, ht, hb);
+      if (Cout <= 96) return launch_conv_dxr<96, 64>(in, T_in, w_t, p, s0, ht, hb);
+      return launch_conv_dxr<192, 64>(in, T_in, w_t, p, s0, ht, hb);
     }
     p.kb_per_tap = Cin / 32;
-    if (Cout <= 32) return launch_conv_dxr<32, 32>(in, T_in, w_t, p, s0);
-    if (Cout <= 96) return launch_conv_dxr<96, 32>(in, T_in, w_t, p, s0);
-    return launch_conv_dxr<192, 32>(in, T_in, w_t, p, s0);
+    if (Cout <= 32) return launch_conv_dxr<32, 32>(in, T_in, w_t, p, s0, ht, hb);
+    if (Cout <= 96) return launch_conv_dxr<96, 32>(in, T_in, w_t, p, s0, ht, hb);
+    return launch_conv_dxr<192, 32>(in, T_in, w_t, p, s0, ht, hb);
   }
   const bool bk32 = (Cin % 64) != 0 && (Cin % 32) == 0;
   const int BK = (Cin <= 32 || bk32) ? 32 : 64;
@@ -531,4 +554,22 @@ extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t 
   if (bn == 32) return launch_conv<32, 64>(in, T_in, w_t, p, s);
   if (bn == 96) return launch_conv<96, 64>(in, T_in, w_t, p, s);
   return launch_conv<192, 64>(in, T_in, w_t, p, s);
+}
+
+extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t W, int32_t Cin, const void* w_t,
+                               int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0, const float* bias,
+                               const void* resid, int64_t resid_ld, void* out, int64_t out_ld, int32_t T_out,
+                               int32_t mode, void* stream) {
+  return conv3d_impl(in, nullptr, nullptr, T_in, H, W, Cin, w_t, Cout, KT, KH, KW, t0, bias, resid, resid_ld, out,
+                     out_ld, T_out, mode, stream);
+}
+
+extern "C" int ftb_conv3d_halo_bf16(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in,
+                                    int32_t H, int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT,
+                                    int32_t KH, int32_t KW, int32_t t0, const float* bias, const void* resid,
+                                    int64_t resid_ld, void* out, int64_t out_ld, int32_t T_out, int32_t mode,
+                                    void* stream) {
+  if (!halo_top || !halo_bot) return set_error(FTB_EINVAL, "conv3d_halo: halo buffers required");
+  return conv3d_impl(in, halo_top, halo_bot, T_in, H, W, Cin, w_t, Cout, KT, KH, KW, t0, bias, resid, resid_ld, out,
+                     out_ld, T_out, mode, stream);
 }

@@ -50,6 +50,10 @@ class ShardPlan:
 class LocalComm:
     world, rank = 1, 0
 
+    def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
+        recv_top.zero_()
+        recv_bot.zero_()
+
     def all_to_all(self, out, inp, stream=None):
         out.copy_(inp)
 
@@ -72,6 +76,25 @@ class TorchComm:
 
     def all_gather(self, out, inp, stream=None):
         self.dist.all_gather_into_tensor(out.reshape(-1), inp.reshape(-1), group=self.group)
+
+    def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
+        """Spatial-split halo swap: my first row -> rank-1 (its bottom halo), my last
+        row -> rank+1 (its top halo); global edges receive zeros."""
+        d, r, g = self.dist, self.rank, self.world
+        ops = []
+        if r > 0:
+            ops += [d.P2POp(d.isend, send_first.contiguous(), r - 1, self.group),
+                    d.P2POp(d.irecv, recv_top, r - 1, self.group)]
+        if r + 1 < g:
+            ops += [d.P2POp(d.isend, send_last.contiguous(), r + 1, self.group),
+                    d.P2POp(d.irecv, recv_bot, r + 1, self.group)]
+        if ops:
+            for w in d.batch_isend_irecv(ops):
+                w.wait()
+        if r == 0:
+            recv_top.zero_()
+        if r + 1 == g:
+            recv_bot.zero_()
 
 
 class _ThreadHub:
@@ -122,3 +145,20 @@ class ThreadComm:
             for src in range(g):
                 ov[src].copy_(self.hub.slots[src].reshape(-1))
         self._exchange(out, inp, stream, pick)
+
+    def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        s.synchronize()
+        self.hub.slots[self.rank] = (send_first, send_last)
+        self.hub.barrier.wait()
+        with torch.cuda.stream(s):
+            if self.rank > 0:
+                recv_top.copy_(self.hub.slots[self.rank - 1][1])
+            else:
+                recv_top.zero_()
+            if self.rank + 1 < self.world:
+                recv_bot.copy_(self.hub.slots[self.rank + 1][0])
+            else:
+                recv_bot.zero_()
+        s.synchronize()
+        self.hub.barrier.wait()

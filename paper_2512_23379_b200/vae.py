@@ -144,14 +144,25 @@ class _ConvW:
 
 class DeviceVAEDecoder:
     """Streaming causal decoder on one device. `decode_device(z)` decodes one
-    chunk of target latents [T, z_dim, h, w] and advances the causal caches."""
+    chunk of target latents [T, z_dim, h, w] and advances the causal caches.
 
-    def __init__(self, cfg: VAEConfig, device, params=None, seed=0, rgb8=True):
+    With a communicator of world g > 1 the decode is split spatially along the
+    latent rows: conv_in runs on the full (replicated) latent, then
+    rank r owns a contiguous slab of rows at every level (slabs double with each
+    2x upsample). Before every 3x3 convolution the ranks swap their edge rows
+    (one row per side at that level's resolution, all frames) with their
+    neighbours; the conv kernel reads rows -1 / H_local from those halo buffers
+    (zeros at the global edges), so the split decode equals the unsplit one.
+    The causal caches of the halo rows travel with the caches of the slabs."""
+
+    def __init__(self, cfg: VAEConfig, device, params=None, seed=0, rgb8=True, comm=None):
+        from .dist import LocalComm
         self.cfg = cfg
         self.dev = torch.device(device)
         self.prog, shapes = vae_program(cfg)
         self.rgb8 = rgb8
         self.frames_per_latent = cfg.time_factor
+        self.comm = comm if comm is not None else LocalComm()
         self.W, self.G = {}, {}
         for idx, (name, shape) in enumerate(shapes):
             if name.endswith(".g"):
@@ -167,13 +178,22 @@ class DeviceVAEDecoder:
         self._geo = None
         self._host = {}
 
+    @property
+    def split(self):
+        return self.comm.world > 1
+
     # ------------------------------------------------------------ buffers
     def _setup(self, T, h, w):
         key = (T, h, w)
         if self._geo == key:
             return
         self._geo = key
-        geo = [dict(T=T, H=h, W=w, C=0)]
+        g, r = self.comm.world, self.comm.rank
+        if h < g:
+            raise ConfigError("latent height %d cannot be split over %d ranks" % (h, g))
+        sizes = [h // g + (1 if i < h % g else 0) for i in range(g)]
+        self.row0, self.rows = sum(sizes[:r]), sizes[r]
+        geo = [dict(T=T, H=self.rows, W=w, C=0)]
         ups = 1
         for op, name, cin, cout in self.prog:
             cur = geo[-1]
@@ -187,24 +207,33 @@ class DeviceVAEDecoder:
             elif op == "resample":
                 cur["C"] = max(cur["C"], cin)
                 ups = max(ups, cur["T"] * 4 * cur["H"] * cur["W"] * cin)
-                geo.append(dict(T=cur["T"], H=2 * cur["H"], W=2 * cur["W"], C=cout))
+                geo.append(dict(T=cur["T"], H=2 * cur["H"], W=2 * cur["W"], C=cout, HC=cin))
         bf, f32 = torch.bfloat16, torch.float32
         levels = {}
-        for l, g in enumerate(geo):
-            px, C = g["T"] * g["H"] * g["W"], g["C"]
-            levels[l] = dict(g, x=torch.empty(px * C, dtype=f32, device=self.dev),      # residual stream
+        for l, gg in enumerate(geo):
+            px, C = gg["T"] * gg["H"] * gg["W"], gg["C"]
+            Tp = gg["T"] + 2
+            levels[l] = dict(gg, x=torch.empty(px * C, dtype=f32, device=self.dev),      # residual stream
                              sc=torch.empty(px * C, dtype=f32, device=self.dev),     # 1x1 shortcut
                              h=torch.empty(px * C, dtype=bf, device=self.dev),       # conv1 output
                              xb=torch.empty(px * C, dtype=bf, device=self.dev),      # bf16 view of x
-                             work=torch.empty((g["T"] + 2) * g["H"] * g["W"] * C, dtype=bf, device=self.dev))
+                             work=torch.empty(Tp * gg["H"] * gg["W"] * C, dtype=bf, device=self.dev))
+            if self.split:  # halo rows (+2 cache frames) and contiguous edge-row send buffers
+                row = gg["W"] * max(C, gg.get("HC", 0))
+                levels[l].update(top=torch.zeros(Tp * row, dtype=bf, device=self.dev),
+                                 bot=torch.zeros(Tp * row, dtype=bf, device=self.dev),
+                                 s_first=torch.empty(Tp * row, dtype=bf, device=self.dev),
+                                 s_last=torch.empty(Tp * row, dtype=bf, device=self.dev))
         self.levels = levels
         self.upbuf = torch.empty(ups, dtype=bf, device=self.dev)
+        self.full0 = torch.empty(T * h * w * geo[0]["C"], dtype=f32, device=self.dev) if self.split else None
         last = levels[len(geo) - 1]
         npx = last["T"] * last["H"] * last["W"]
         self.out_rgb = torch.empty(npx * 3, dtype=torch.uint8, device=self.dev)
         self.out_f = torch.empty(npx * 32, dtype=f32, device=self.dev)
         for cw in self.W.values():
             cw.cache = None
+            cw.hcache = None
         self.reset()
 
     def reset(self):
@@ -212,13 +241,30 @@ class DeviceVAEDecoder:
         for cw in self.W.values():
             if cw.cache is not None:
                 cw.cache.zero_()
+            if getattr(cw, "hcache", None) is not None:
+                cw.hcache.zero_()
 
     # ------------------------------------------------------------ primitive wrappers
     OUT_F32, RESID_F32 = 16, 32
 
-    def _causal(self, cw, L, Cin, producer, out, out_ld, mode, resid=None, resid_ld=0, stream=None):
+    def _exchange_halos(self, L, src, T_in, Cin, off=0):
+        """Edge rows of `src` frames [0, T_in) -> neighbours; the neighbours' edge rows
+        land in L['top'] / L['bot'] frames [off, off + T_in) (zeros at the global edges)."""
+        H, W = L["H"], L["W"]
+        row = W * Cin
+        v = src[:T_in * H * row].view(T_in, H, row)
+        first, last = L["s_first"][:T_in * row].view(T_in, row), L["s_last"][:T_in * row].view(T_in, row)
+        first.copy_(v[:, 0])
+        last.copy_(v[:, H - 1])
+        top = L["top"][off * row:(off + T_in) * row].view(T_in, row)
+        bot = L["bot"][off * row:(off + T_in) * row].view(T_in, row)
+        self.comm.neighbor_exchange(first, last, top, bot)
+        return L["top"][:(off + T_in) * row], L["bot"][:(off + T_in) * row]
+
+    def _causal(self, cw, L, Cin, producer, out, out_ld, mode, resid=None, resid_ld=0, stream=None, halo=True):
         """KT=3 causal conv on level L: cache -> work[0:2], producer fills
-        work[2:], conv, last 2 input frames -> cache (for the next chunk)."""
+        work[2:], (split: halo exchange of the new frames), conv, last 2 input
+        frames -> cache (for the next chunk)."""
         T, H, W = L["T"], L["H"], L["W"]
         fr = H * W * Cin
         work = L["work"][:(T + 2) * fr]
@@ -226,16 +272,39 @@ class DeviceVAEDecoder:
             cw.cache = torch.zeros(2 * fr, dtype=torch.bfloat16, device=self.dev)
         work[:2 * fr].copy_(cw.cache)
         producer(work[2 * fr:])
-        self._conv(work, T + 2, H, W, Cin, cw, out, out_ld, 0, mode, resid, resid_ld, T, stream)
+        halos = None
+        if self.split and halo and cw.k[1] == 3:
+            row = W * Cin
+            if cw.hcache is None:
+                cw.hcache = torch.zeros(2, 2 * row, dtype=torch.bfloat16, device=self.dev)
+            # exchange the T new frames; the 2 cached halo frames come from this conv's halo cache
+            tv, bv = self._exchange_halos(L, work[2 * fr:], T, Cin, off=2)
+            tv[:2 * row].copy_(cw.hcache[0])
+            bv[:2 * row].copy_(cw.hcache[1])
+            cw.hcache[0].copy_(tv[T * row:(T + 2) * row])
+            cw.hcache[1].copy_(bv[T * row:(T + 2) * row])
+            halos = (tv, bv)
+        self._conv(work, T + 2, H, W, Cin, cw, out, out_ld, 0, mode, resid, resid_ld, T, stream, halos,
+                   allow_halo=halo)
         cw.cache.copy_(work[T * fr:(T + 2) * fr])
 
-    def _conv(self, inp, T_in, H, W, Cin, cw, out, out_ld, t0, mode, resid, resid_ld, T_out, stream):
+    def _conv(self, inp, T_in, H, W, Cin, cw, out, out_ld, t0, mode, resid, resid_ld, T_out, stream, halos=None,
+              allow_halo=True):
         kt, kh, kw = cw.k
         cout = cw.cout if (mode & 15) != 0 or cw.cout % 32 == 0 else cw.wt.shape[0]
-        tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%dx%d %d->%d k%d%d%d" % (T_out, H, W, 0, Cin, cw.cout, kt, kh, kw)
+        if self.split and allow_halo and kh == 3 and halos is None:   # non-causal 3x3 (resample)
+            L = next(lv for lv in self.levels.values() if lv["H"] == H and lv["W"] == W and lv["T"] == T_in)
+            halos = self._exchange_halos(L, inp, T_in, Cin)
+        tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%d %d->%d k%d%d%d" % (
+            T_out, H, W, Cin, cw.cout, kt, kh, kw)
         with ops._Prof(tag, 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
-            A.call("ftb_conv3d_bf16", A.ptr(inp), T_in, H, W, Cin, A.ptr(cw.wt), cout, kt, kh, kw, t0,
-                   A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld, T_out, mode, A.stream_ptr(stream))
+            if halos is not None:
+                A.call("ftb_conv3d_halo_bf16", A.ptr(inp), A.ptr(halos[0]), A.ptr(halos[1]), T_in, H, W, Cin,
+                       A.ptr(cw.wt), cout, kt, kh, kw, t0, A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld,
+                       T_out, mode, A.stream_ptr(stream))
+            else:
+                A.call("ftb_conv3d_bf16", A.ptr(inp), T_in, H, W, Cin, A.ptr(cw.wt), cout, kt, kh, kw, t0,
+                       A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld, T_out, mode, A.stream_ptr(stream))
 
     def _rms(self, x, npix, C, g, y, stream):
         fn = "ftb_rmsnorm_silu_f32" if x.dtype == torch.float32 else "ftb_rmsnorm_silu_bf16"
@@ -244,7 +313,8 @@ class DeviceVAEDecoder:
     # ------------------------------------------------------------ decode
     def decode_device_tensor(self, z, stream=None):
         """z: device f32 [T, z_dim, h, w] -> device output (uint8 [T*tf, H, W, 3] if
-        rgb8 else f32 [T*tf, H, W, 32] with channels 0..2 valid)."""
+        rgb8 else f32 [T*tf, H, W, 32] with channels 0..2 valid). With a split
+        communicator the output is this rank's row slab [T*tf, H_local, W, .]."""
         if z.dim() != 4 or z.shape[1] != self.cfg.z_dim:
             raise ConfigError("VAE input must be [T, z_dim, h, w]")
         T, _, h, w = z.shape
@@ -255,10 +325,20 @@ class DeviceVAEDecoder:
         l = 0
         cw = self.W["conv_in"]
         zc = self.cfg.z_dim
-        self._causal(cw, lv[0], zc,
-                     lambda dst: A.call("ftb_nchw_to_nhwc_bf16", A.ptr(z), T, zc, h, w, A.ptr(dst), zc,
-                                        A.stream_ptr(s)),
-                     lv[0]["x"], cw.cout, F32, stream=s)
+        if not self.split:
+            self._causal(cw, lv[0], zc,
+                         lambda dst: A.call("ftb_nchw_to_nhwc_bf16", A.ptr(z), T, zc, h, w, A.ptr(dst), zc,
+                                            A.stream_ptr(s)),
+                         lv[0]["x"], cw.cout, F32, stream=s)
+        else:   # conv_in on the full (replicated) latent, then keep this rank's rows
+            full = dict(T=T, H=h, W=w, work=self._full_work(T, h, w, zc))
+            self._causal(cw, full, zc,
+                         lambda dst: A.call("ftb_nchw_to_nhwc_bf16", A.ptr(z), T, zc, h, w, A.ptr(dst), zc,
+                                            A.stream_ptr(s)),
+                         self.full0, cw.cout, F32, stream=s, halo=False)
+            C0 = cw.cout
+            lv[0]["x"][:T * self.rows * w * C0].view(T, self.rows, w, C0).copy_(
+                self.full0.view(T, h, w, C0)[:, self.row0:self.row0 + self.rows])
         for op, name, cin, cout in self.prog[1:]:
             L = lv[l]
             T_, H_, W_ = L["T"], L["H"], L["W"]
@@ -299,6 +379,14 @@ class DeviceVAEDecoder:
                 self._causal(hw_, L, cin, prod, self.out_f, 32, F32, stream=s)
                 return self.out_f[:npx * 32].view(T_, H_, W_, 32)
         raise ConfigError("VAE program has no head")
+
+    def _full_work(self, T, h, w, zc):
+        buf = getattr(self, "_fw", None)
+        n = (T + 2) * h * w * zc
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(n, dtype=torch.bfloat16, device=self.dev)
+            self._fw = buf
+        return buf
 
     def decode_device(self, z, stream):
         """Codec interface of the streaming engine: device latents -> host frames."""

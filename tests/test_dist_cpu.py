@@ -68,3 +68,40 @@ def test_gloo_world2_collective_layouts():
     for p in ps:
         p.join(timeout=60)
     assert all(r[1] == "ok" for r in res), res
+
+
+def _halo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2512_23379_b200.dist import TorchComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        first = torch.full((4, 6), 10.0 * rank + 1)
+        last = torch.full((4, 6), 10.0 * rank + 2)
+        top, bot = torch.empty(4, 6), torch.empty(4, 6)
+        comm.neighbor_exchange(first, last, top, bot)
+        exp_top = 0.0 if rank == 0 else 10.0 * (rank - 1) + 2
+        exp_bot = 0.0 if rank == world - 1 else 10.0 * (rank + 1) + 1
+        assert torch.all(top == exp_top) and torch.all(bot == exp_bot), (rank, top[0, 0], bot[0, 0])
+        q.put((rank, "ok", 0))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_halo_exchange_world3():
+    """Spatially split VAE: edge-row swap with neighbours, zeros at the global edges."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + os.getpid() % 90
+    ps = [ctx.Process(target=_halo_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res

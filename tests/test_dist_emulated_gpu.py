@@ -85,3 +85,48 @@ def test_ulysses_padding_path(cuda):
     one, _ = _run(cfg, store, x, geo, 1, cuda)
     many, _ = _run(cfg, store, x, geo, 4, cuda)
     assert rel(many[3], one[0]) < 5e-3
+
+
+SMALL_VAE = dict(z_dim=16, base_dim=32, dim_mult=(1, 2, 4, 4), num_res_blocks=2, temporal_upsample=(True, True, False))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_vae_matches_unsplit(cuda, world):
+    """Spatially split causal VAE decode (row slabs + per-conv halo exchange, two
+    chunks so the causal caches of slabs and halos are exercised) == unsplit decode."""
+    from paper_2512_23379_b200.dist import ThreadComm
+    from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig, init_vae_params
+    cfg = VAEConfig(**SMALL_VAE)
+    P = init_vae_params(cfg, 4)
+    r = np.random.default_rng(1)
+    zs = [r.standard_normal((3, 16, 6, 8)) for _ in range(2)]
+    ref_dec = DeviceVAEDecoder(cfg, cuda, params=P, rgb8=False)
+    want = [ref_dec.decode_device(torch.as_tensor(z, dtype=torch.float32, device=cuda), torch.cuda.current_stream())
+            for z in zs]
+    comms = ThreadComm.make(world)
+    got, errs = [[None] * world for _ in zs], []
+
+    def worker(rk):
+        try:
+            torch.cuda.set_device(cuda)
+            s = torch.cuda.Stream(device=cuda)
+            dec = DeviceVAEDecoder(cfg, cuda, params=P, rgb8=False, comm=comms[rk])
+            for i, z in enumerate(zs):
+                with torch.cuda.stream(s):
+                    zd = torch.as_tensor(z, dtype=torch.float32, device=cuda)
+                out = dec.decode_device(zd, s)
+                got[i][rk] = (dec.row0, out)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            raise
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    for i in range(2):
+        slabs = sorted(got[i], key=lambda x: x[0])
+        full = np.concatenate([sl for _, sl in slabs], axis=1)[..., :3]
+        assert full.shape == want[i][..., :3].shape
+        assert rel(full, want[i][..., :3]) < 2e-3, i
