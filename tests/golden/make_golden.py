@@ -140,6 +140,12 @@ def main():
         g["w_%d_%d" % (lc, lm)] = np.array(wins)
     g["w_signal"] = sig
 
+    # ---- FTLK checkpoint written by the reference writer (checkpoint.py:31-53)
+    from ftlk.checkpoint import save as ref_save
+    ref_save(os.path.join(os.path.dirname(OUT), "tiny.ftlk"), stores["tiny"], "generator_student",
+             cfgs["tiny"][0])
+    g["c_tiny_checksum"] = np.array(stores["tiny"].checksum())
+
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, len(g), "arrays")
 
