@@ -160,7 +160,7 @@ def load_device_weights(path, device="cuda"):
                 if arr.ndim == 2 and not name.endswith(".mod"):
                     K, N = arr.shape
                     wt = torch.zeros(N, round8(K), dtype=torch.bfloat16, device=w.device)
-                    wt[:, :K] = torch.from_numpy(np.ascontiguousarray(arr.T)).to(w.device).to(torch.bfloat16)
+                    wt[:, :K] = torch.from_numpy(np.array(arr.T)).to(w.device).to(torch.bfloat16)
                     w.mats[name] = (wt, K)
                 else:
                     w.vecs[name] = torch.from_numpy(np.array(arr)).to(torch.float32).to(w.device)

@@ -6,6 +6,7 @@ import time
 
 import numpy as np
 import pytest
+import torch
 
 pytestmark = pytest.mark.gpu
 BUDGET = 1e-2
@@ -129,3 +130,52 @@ def test_session_memory_flat(golden, cuda, setup):
     sess.close()
     assert got == len(sig)
     assert marks[60] <= marks[10] * 1.02, marks
+
+
+def test_wan_stream_with_vae_decoder(cuda):
+    """Wan-shaped engine end to end: threaded session with the causal VAE as codec;
+    emitted RGB8 frames equal the synchronous twin; decoded float frames of chunk 0
+    match the float64 oracle pipeline (DiT sampler -> VAE decode)."""
+    from oracle import vae_oracle as VO
+    from oracle import wan_oracle as WO
+    from paper_2512_23379_b200.config import NetConfig, StreamConfig
+    from paper_2512_23379_b200.net import ParamStore
+    from paper_2512_23379_b200.seeding import chunk_noise
+    from paper_2512_23379_b200.streaming import generate, start_stream
+    from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig, init_vae_params
+    cfg = NetConfig(128, 1, 2, 256, 16, mode="wan", patch=(1, 2, 2), audio_dim=8, audio_tokens=2)
+    store = ParamStore.init(cfg, 5)
+    vcfg = dict(z_dim=16, base_dim=32, dim_mult=(1, 2, 4, 4), num_res_blocks=1, temporal_upsample=(True, True, False))
+    VP = init_vae_params(VAEConfig(**vcfg), 6)
+    r = np.random.default_rng(2)
+    H, W = 4, 6
+    ref_lat = r.standard_normal((16, H, W))
+    audio = r.standard_normal((14, 2, 8))
+    scfg = StreamConfig(chunk_len=5, motion_len=1, seed=9)
+    # threaded session, RGB8 output
+    vae8 = DeviceVAEDecoder(VAEConfig(**vcfg), cuda, params=VP, rgb8=True)
+    sess = start_stream(store, cfg, vae8, None, scfg, reference_latent=ref_lat, latent_hw=(H, W))
+    sess.push_signal((i, audio[i]) for i in range(8))
+    got = []
+    deadline = time.time() + 120
+    while len(got) < 32 and time.time() < deadline:
+        fr, _ = sess.next_frames(wait=True, timeout=0.2)
+        got.extend(fr)
+    sess.close()
+    assert [f.index for f in got] == list(range(32)) and [f.chunk for f in got] == [i // 16 for i in range(32)]
+    assert got[0].state.shape == (32, 48, 3) and got[0].state.dtype == np.uint8
+    vae8b = DeviceVAEDecoder(VAEConfig(**vcfg), cuda, params=VP, rgb8=True)
+    _, _, fr = generate(store, cfg, vae8b, ref_lat, audio[:8], 8, cfg=scfg, latent_hw=(H, W))
+    assert np.array_equal(np.stack([f.state for f in got]), fr)
+    # float frames of chunk 0 vs the oracle pipeline
+    vaef = DeviceVAEDecoder(VAEConfig(**vcfg), cuda, params=VP, rgb8=False)
+    tg, _, frf = generate(store, cfg, vaef, ref_lat, audio[:4], 4, cfg=scfg, latent_hw=(H, W))
+    P = store.bf16_rounded().params
+    ocfg = dict(model_dim=128, layers=1, heads=2, latent_dim=16, patch=(1, 2, 2), audio_tokens=2, audio_dim=8)
+    win = np.concatenate([np.zeros((1, 2, 8)), audio[:4]], 0)
+    lat = WO.sample_chunk(P, ocfg, (1.0, 0.75, 0.5, 0.25), ref_lat[None], ref_lat, win,
+                          chunk_noise(9, 0, (4, 16, H, W)))
+    assert rel(tg[:4], lat[1:]) < BUDGET
+    VPb = {k: (torch.as_tensor(v).to(torch.bfloat16).double().numpy() if k.endswith(".w") else v) for k, v in VP.items()}
+    want = VO.VAEOracle(VPb, **vcfg).decode(tg[:4])
+    assert rel(frf[..., :3], want) < BUDGET
