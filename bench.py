@@ -336,7 +336,8 @@ def main():
                "chunk_seconds": chunk_s}
 
     if rank == 0:
-        line = {"metric": "streaming FPS (14B-shape DiT, 4-step chunk, 28 frames/chunk)", "value": fps,
+        line = {"metric": "streaming FPS (%s-shape DiT, 4-step chunk, %d frames/chunk)" % (
+                    {"14b": "14B", "1.3b": "1.3B", "tiny": "tiny ftlk"}[args.model], frames_per_chunk), "value": fps,
                 "unit": "FPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "chunk_latency_ms": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) audio)",
