@@ -21,6 +21,9 @@
  *   ftb_unpatch_ddim ..... diffusion.py:229-236 x0 slice + DDIM update; streaming.py:298-299 tail
  *   ftb_codec_decode ..... world.py:206-210 Codec.decode (latents @ Q)
  *   ftb_vae_* ............ wan-mode causal VAE decoder (build-defined)
+ *   ftb_sym_* / ftb_ipc_* / ftb_peer_barrier / peer epilogues
+ *                          Ulysses sequence parallel over NVLink peer memory (the
+ *                          reference runs the DiT on one process, net.py:240-276)
  */
 #ifndef FTB2_H
 #define FTB2_H
@@ -37,6 +40,9 @@ extern "C" {
 #define FTB_ECUDA 2
 #define FTB_ENCCL 3
 #define FTB_ENONFINITE 4
+
+#define FTB_MAX_PEERS 8          /* ranks of one NVLink domain addressed by a peer epilogue */
+#define FTB_IPC_HANDLE_BYTES 64
 
 int ftb_version(void);
 const char* ftb_last_error(void);
@@ -73,6 +79,12 @@ typedef struct ftb_epilogue {
    * stored at ((dest*M + row)*3 + which)*hpr*hd + (head%hpr)*hd + d, dest = head/hpr. */
   int32_t heads, head_dim, heads_per_rank;
   const ftb_rope3d* rope;  /* NULL: no rotation */
+  /* Peer stores (Ulysses over NVLink; 0 = local `out`):
+   *  QKV_ROPE: n_peers = heads/heads_per_rank; head group `dest`'s block [M][3][hpr][hd]
+   *            goes to peer_out[dest] (rank dest's receive buffer at this rank's slot);
+   *  F32:      every peer_out[i] receives the full [M][ldc] result (fused all-gather). */
+  int32_t n_peers;
+  void* peer_out[FTB_MAX_PEERS];
 } ftb_epilogue;
 
 /* C[M,N] = A[M,K] . B[N,K]^T (bf16 in, fp32 accumulate, tcgen05 + TMEM, TMA-fed).
@@ -107,6 +119,28 @@ int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const 
 int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk,
                        const void* v, int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk,
                        int32_t heads, int32_t head_dim, float scale, void* stream);
+
+/* Ulysses all-to-all #2 fused into the epilogue: output row r is stored at row r % peer_rows
+ * of o_peers[r / peer_rows] (device pointers, peer-mapped; host array of n_peers entries). */
+int ftb_attention_scatter(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+                          void* const* o_peers, int32_t n_peers, int64_t peer_rows, int64_t ldo, int32_t Lq,
+                          int32_t Lk, int32_t heads, int32_t head_dim, float scale, void* stream);
+
+/* ---------------------------------------------------------------- peer memory (multi-GPU) */
+/* IPC-exportable zeroed device allocation / free. */
+int ftb_sym_alloc(size_t bytes, void** ptr);
+int ftb_sym_free(void* ptr);
+/* cudaIpc handle of an ftb_sym_alloc pointer (FTB_IPC_HANDLE_BYTES bytes) and its import
+ * into another process of the node (peer access enabled lazily); close undoes import. */
+int ftb_ipc_export(const void* ptr, uint8_t* handle);
+int ftb_ipc_import(const uint8_t* handle, void** ptr);
+int ftb_ipc_close(void* ptr);
+/* Stream-ordered barrier over `world` ranks: flags[i] = rank i's [world] u32 flag words
+ * (peer-mapped), epoch = this rank's device counter (incremented per call, so the barrier
+ * is CUDA-graph capturable). Fences prior stores system-wide, signals every rank, then
+ * waits for all; traps after timeout_s seconds instead of hanging. */
+int ftb_peer_barrier(uint32_t* const* flags, uint32_t* epoch, int32_t rank, int32_t world, double timeout_s,
+                     void* stream);
 
 /* ---------------------------------------------------------------- elementwise */
 int ftb_gelu_bf16(const void* x, void* y, int64_t n, void* stream);

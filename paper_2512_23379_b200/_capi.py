@@ -16,6 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libftb2.so")
 
 FTB_OK, FTB_EINVAL, FTB_ECUDA, FTB_ENCCL, FTB_ENONFINITE = 0, 1, 2, 3, 4
+MAX_PEERS, IPC_HANDLE_BYTES = 8, 64
 EPI_BF16, EPI_GELU_BF16, EPI_F32, EPI_RESID_F32, EPI_ROWADD_F32, EPI_QKV_ROPE = range(6)
 
 vp, i32, i64, f32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint64
@@ -28,7 +29,8 @@ class Rope3D(C.Structure):
 class Epilogue(C.Structure):
     _fields_ = [("kind", i32), ("rows_per_group", i32), ("row_offset", i64), ("bias", vp),
                 ("group_vec", vp), ("group_ld", i64), ("out", vp), ("ldc", i64),
-                ("heads", i32), ("head_dim", i32), ("heads_per_rank", i32), ("rope", C.POINTER(Rope3D))]
+                ("heads", i32), ("head_dim", i32), ("heads_per_rank", i32), ("rope", C.POINTER(Rope3D)),
+                ("n_peers", i32), ("peer_out", vp * MAX_PEERS)]
 
 
 _SIGS = {
@@ -41,6 +43,14 @@ _SIGS = {
     "ftb_norm_modulate": ([vp, i64, i32, i32, vp, vp, vp, vp, i64, i32, i64, f32, vp, i64, vp, vp, vp], i32),
     "ftb_attention": ([vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),
     "ftb_attention_impl": ([i32, vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),
+    "ftb_attention_scatter": ([vp, i64, vp, i64, vp, i64, C.POINTER(vp), i32, i64, i64, i32, i32, i32, i32, f32,
+                               vp], i32),
+    "ftb_sym_alloc": ([C.c_size_t, C.POINTER(vp)], i32),
+    "ftb_sym_free": ([vp], i32),
+    "ftb_ipc_export": ([vp, C.c_char_p], i32),
+    "ftb_ipc_import": ([C.c_char_p, C.POINTER(vp)], i32),
+    "ftb_ipc_close": ([vp], i32),
+    "ftb_peer_barrier": ([C.POINTER(vp), vp, i32, i32, C.c_double, vp], i32),
     "ftb_gelu_bf16": ([vp, vp, i64, vp], i32),
     "ftb_silu_f32_to_bf16": ([vp, vp, i64, vp], i32),
     "ftb_cast_f32_bf16": ([vp, vp, i64, vp], i32),

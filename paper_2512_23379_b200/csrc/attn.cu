@@ -28,7 +28,20 @@ struct AttnParams {
   long long ldq, ldk, ldv, ldo;
   int Lq, Lk, heads, hd;
   float scale_log2;  // scale * log2(e)
+  // Ulysses scatter epilogue (n_peers > 0): output row r goes to rank r / peer_rows,
+  // row r % peer_rows of that rank's buffer (a peer-mapped pointer over NVLink)
+  int n_peers;
+  long long peer_rows;
+  __nv_bfloat16* o_peers[FTB_MAX_PEERS];
 };
+
+__device__ __forceinline__ __nv_bfloat16* attn_out_row(const AttnParams& p, long long row) {
+  if (p.n_peers) {
+    const long long d = row / p.peer_rows;
+    return p.o_peers[d] + (row - d * p.peer_rows) * p.ldo;
+  }
+  return p.o + row * p.ldo;
+}
 
 // ============================================================ tcgen05 flash kernel
 template <int HD>
@@ -238,7 +251,7 @@ __global__ void __launch_bounds__(256, 1)
       tmem_ld32(tmem + lane_off + C::TM_O + c0, o);
       tmem_ld_wait();
       if (grow < p.Lq) {
-        uint4* dst = reinterpret_cast<uint4*>(p.o + (long long)grow * p.ldo + head * HD + c0);
+        uint4* dst = reinterpret_cast<uint4*>(attn_out_row(p, grow) + head * HD + c0);
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
           uint4 w;
@@ -503,7 +516,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_ld32(tO + c0, o);
       tmem_ld_wait();
       if (grow < p.Lq) {
-        uint4* dst = reinterpret_cast<uint4*>(p.o + (long long)grow * p.ldo + head * HD + c0);
+        uint4* dst = reinterpret_cast<uint4*>(attn_out_row(p, grow) + head * HD + c0);
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
           uint4 w;
@@ -602,7 +615,7 @@ __global__ void __launch_bounds__(128) attn_small_kernel(const AttnParams p) {
 #pragma unroll
     for (int i = 0; i < DPL; ++i) {
       const int d = lane + 32 * i;
-      if (d < HD) p.o[(long long)gr * p.ldo + head * HD + d] = __float2bfloat16_rn(acc[r][i] * inv);
+      if (d < HD) attn_out_row(p, gr)[head * HD + d] = __float2bfloat16_rn(acc[r][i] * inv);
     }
   }
 }
@@ -668,14 +681,9 @@ static int launch_small(const AttnParams& p, cudaStream_t s) {
 
 using namespace ftb;
 
-extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
-                                  int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads,
-                                  int32_t head_dim, float scale, void* stream) {
-  if (!q || !k || !v || !o || Lq < 0 || Lk <= 0 || heads <= 0 || head_dim <= 0)
-    return set_error(FTB_EINVAL, "attention: bad arguments");
-  if (Lq == 0) return FTB_OK;
-  AttnParams p{(const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (__nv_bfloat16*)o,
-               ldq, ldk, ldv, ldo, Lq, Lk, heads, head_dim, scale * 1.4426950408889634f};
+static int attention_run(int32_t impl, AttnParams& p, void* stream) {
+  const long long ldq = p.ldq, ldk = p.ldk, ldv = p.ldv, ldo = p.ldo;
+  const int head_dim = p.hd;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (impl == 0 || impl == 2) {
     if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
@@ -695,9 +703,64 @@ extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, cons
   return set_error(FTB_EINVAL, "attention: head_dim must be <= 128");
 }
 
+static int default_impl(int Lq, int head_dim) { return ((head_dim == 64 || head_dim == 128) && Lq >= 64) ? 0 : 1; }
+
+extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                                  int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads,
+                                  int32_t head_dim, float scale, void* stream) {
+  if (!q || !k || !v || !o || Lq < 0 || Lk <= 0 || heads <= 0 || head_dim <= 0)
+    return set_error(FTB_EINVAL, "attention: bad arguments");
+  if (Lq == 0) return FTB_OK;
+  AttnParams p{};
+  p.q = (const __nv_bfloat16*)q;
+  p.k = (const __nv_bfloat16*)k;
+  p.v = (const __nv_bfloat16*)v;
+  p.o = (__nv_bfloat16*)o;
+  p.ldq = ldq;
+  p.ldk = ldk;
+  p.ldv = ldv;
+  p.ldo = ldo;
+  p.Lq = Lq;
+  p.Lk = Lk;
+  p.heads = heads;
+  p.hd = head_dim;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  return attention_run(impl, p, stream);
+}
+
+extern "C" int ftb_attention_scatter(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                                     int64_t ldv, void* const* o_peers, int32_t n_peers, int64_t peer_rows,
+                                     int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
+                                     float scale, void* stream) {
+  if (!q || !k || !v || !o_peers || n_peers < 1 || n_peers > FTB_MAX_PEERS || peer_rows <= 0 || Lq < 0 || Lk <= 0 ||
+      heads <= 0 || head_dim <= 0)
+    return set_error(FTB_EINVAL, "attention_scatter: bad arguments");
+  if ((long long)n_peers * peer_rows < Lq) return set_error(FTB_EINVAL, "attention_scatter: rows exceed peers");
+  for (int i = 0; i < n_peers; ++i)
+    if (!o_peers[i]) return set_error(FTB_EINVAL, "attention_scatter: null peer pointer");
+  if (Lq == 0) return FTB_OK;
+  AttnParams p{};
+  p.q = (const __nv_bfloat16*)q;
+  p.k = (const __nv_bfloat16*)k;
+  p.v = (const __nv_bfloat16*)v;
+  p.o = (__nv_bfloat16*)o_peers[0];
+  p.ldq = ldq;
+  p.ldk = ldk;
+  p.ldv = ldv;
+  p.ldo = ldo;
+  p.Lq = Lq;
+  p.Lk = Lk;
+  p.heads = heads;
+  p.hd = head_dim;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.n_peers = n_peers;
+  p.peer_rows = peer_rows;
+  for (int i = 0; i < n_peers; ++i) p.o_peers[i] = (__nv_bfloat16*)o_peers[i];
+  return attention_run(default_impl(Lq, head_dim), p, stream);
+}
+
 extern "C" int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                              void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
                              float scale, void* stream) {
-  const int impl = ((head_dim == 64 || head_dim == 128) && Lq >= 64) ? 0 : 1;
-  return ftb_attention_impl(impl, q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim, scale, stream);
+  return ftb_attention_impl(default_impl(Lq, head_dim), q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim, scale, stream);
 }

@@ -36,6 +36,8 @@ struct GemmParams {
   int heads, head_dim, hpr;
   ftb_rope3d rope;
   int has_rope;
+  int n_peers;                  // > 0: QKV_ROPE / F32 stores go to peer-mapped buffers
+  void* peers[FTB_MAX_PEERS];
 };
 
 template <int BN>
@@ -47,6 +49,13 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
+
+// QKV_ROPE destination block [M][3][hpr][hd] for head group `dest`: a slice of `out`, or
+// (Ulysses over peer memory) the peer-mapped receive block of rank `dest`.
+__device__ __forceinline__ __nv_bfloat16* qkv_dest_block(const GemmParams& p, __nv_bfloat16* base, int dest) {
+  if (p.n_peers) return reinterpret_cast<__nv_bfloat16*>(p.peers[dest]);
+  return base + (long long)dest * p.M * 3 * ((long long)p.hpr * p.head_dim);
+}
 
 // Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int gc0, float (&v)[32]) {
@@ -82,6 +91,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
       break;
     }
     case FTB_EPI_F32: {
+      if (p.n_peers) {  // replicated store: the all-gather of the result rides the epilogue
+        for (int r = 0; r < p.n_peers; ++r) {
+          float* o = reinterpret_cast<float*>(p.peers[r]) + (long long)gr * p.ldc + gc0;
+          for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] = v[j];
+        }
+        break;
+      }
       float* o = reinterpret_cast<float*>(p.out) + (long long)gr * p.ldc + gc0;
       if (full && ((p.ldc & 3) == 0)) {
 #pragma unroll
@@ -150,8 +166,8 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
         }
         const int dest = h / p.hpr;
         const int hl = h - dest * p.hpr;
-        uint4* o4 = reinterpret_cast<uint4*>(base + (((long long)dest * p.M + gr) * 3 + which) *
-                                                        ((long long)p.hpr * p.head_dim) +
+        uint4* o4 = reinterpret_cast<uint4*>(qkv_dest_block(p, base, dest) +
+                                             ((long long)gr * 3 + which) * ((long long)p.hpr * p.head_dim) +
                                              (long long)hl * p.head_dim + d0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -182,9 +198,8 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
         }
         int dest = h / p.hpr;
         int hl = h - dest * p.hpr;
-        long long idx = (((long long)dest * p.M + gr) * 3 + which) * ((long long)p.hpr * p.head_dim) +
-                        (long long)hl * p.head_dim + d;
-        *reinterpret_cast<uint32_t*>(base + idx) = pack_bf16(x0, x1);
+        long long idx = ((long long)gr * 3 + which) * ((long long)p.hpr * p.head_dim) + (long long)hl * p.head_dim + d;
+        *reinterpret_cast<uint32_t*>(qkv_dest_block(p, base, dest) + idx) = pack_bf16(x0, x1);
       }
       break;
     }
@@ -522,7 +537,18 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
         epi->heads % epi->heads_per_rank || N != 3 * epi->heads * epi->head_dim)
       return set_error(FTB_EINVAL, "gemm: bad QKV layout");
   }
+  if (epi->n_peers < 0 || epi->n_peers > FTB_MAX_PEERS) return set_error(FTB_EINVAL, "gemm: bad peer count");
+  if (epi->n_peers) {
+    if (epi->kind != FTB_EPI_QKV_ROPE && epi->kind != FTB_EPI_F32)
+      return set_error(FTB_EINVAL, "gemm: peer stores need the QKV_ROPE or F32 epilogue");
+    if (epi->kind == FTB_EPI_QKV_ROPE && epi->n_peers != epi->heads / epi->heads_per_rank)
+      return set_error(FTB_EINVAL, "gemm: QKV peers must equal heads / heads_per_rank");
+    for (int i = 0; i < epi->n_peers; ++i)
+      if (!epi->peer_out[i]) return set_error(FTB_EINVAL, "gemm: null peer pointer");
+  }
   GemmParams p{};
+  p.n_peers = epi->n_peers;
+  for (int i = 0; i < epi->n_peers; ++i) p.peers[i] = epi->peer_out[i];
   p.M = M;
   p.N = N;
   p.K = K;

@@ -14,8 +14,21 @@ tokens [r*Ls, (r+1)*Ls). Weights are replicated. Per layer:
 Cross-attention K/V (conditioning tokens) and the AdaLN tables are replicated,
 so they need no exchange; after the out-projection the x0 tokens are
 all-gathered so every rank applies the same DDIM update (replicated sampler
-state). Communication is NCCL over NVLink through torch.distributed; a
-thread-based emulation (`ThreadComm`) runs g ranks on one device for tests.
+state).
+
+Two transports:
+  * collective comms (`TorchComm`: NCCL all_to_all / all_gather through
+    torch.distributed; `ThreadComm` emulates g ranks on one device for tests);
+  * peer comms (`PeerComm`): the exchanges are FUSED into the producing kernels.
+    Every rank exposes symmetric receive buffers; the QKV GEMM epilogue stores each
+    head group's block straight into its owner's `qkv_recv`, the FMHA epilogue
+    stores each output row into its owner's `ao`, and the out-projection epilogue
+    replicates x0 into every rank's `x0tok`, all over NVLink peer mappings. One
+    stream-ordered barrier after each producer replaces the collective. `IpcPeerComm`
+    is the multi-process transport (cudaIpc handles exchanged through
+    torch.distributed, device flag barrier); `ThreadPeerComm` runs g emulated ranks
+    on one device (peer addresses are the other ranks' buffers, barrier on the host)
+    so the fused layouts are tested without kernels that wait on one another.
 """
 
 import threading
@@ -61,8 +74,16 @@ class LocalComm:
         out.copy_(inp)
 
 
+def _on(stream):
+    import contextlib
+    if stream is None or not torch.cuda.is_available():
+        return contextlib.nullcontext()
+    return torch.cuda.stream(stream)
+
+
 class TorchComm:
-    """torch.distributed (NCCL on GPUs, gloo on CPU) equal-split collectives."""
+    """torch.distributed (NCCL on GPUs, gloo on CPU) equal-split collectives,
+    enqueued on the caller's stream."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -72,10 +93,12 @@ class TorchComm:
         self.rank = dist.get_rank(group)
 
     def all_to_all(self, out, inp, stream=None):
-        self.dist.all_to_all_single(out.reshape(-1), inp.reshape(-1), group=self.group)
+        with _on(stream):
+            self.dist.all_to_all_single(out.reshape(-1), inp.reshape(-1), group=self.group)
 
     def all_gather(self, out, inp, stream=None):
-        self.dist.all_gather_into_tensor(out.reshape(-1), inp.reshape(-1), group=self.group)
+        with _on(stream):
+            self.dist.all_gather_into_tensor(out.reshape(-1), inp.reshape(-1), group=self.group)
 
     def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
         """Spatial-split halo swap: my first row -> rank-1 (its bottom halo), my last
@@ -162,3 +185,160 @@ class ThreadComm:
                 recv_bot.zero_()
         s.synchronize()
         self.hub.barrier.wait()
+
+
+# ---------------------------------------------------------------- peer-memory transport
+_TYPESTR = {torch.float32: "<f4", torch.int32: "<i4", torch.bfloat16: "<i2", torch.uint8: "|u1"}
+
+
+class _SymAlloc:
+    """Owner of one ftb_sym_alloc block, exposed to torch via __cuda_array_interface__
+    (the tensor keeps this object alive; freeing it releases the block)."""
+
+    def __init__(self, shape, dtype):
+        import ctypes as C
+
+        from . import _capi as A
+        self.A = A
+        n = 1
+        for x in shape:
+            n *= int(x)
+        self.nbytes = max(1, n) * torch.tensor([], dtype=dtype).element_size()
+        p = C.c_void_p()
+        A.check(A.lib.ftb_sym_alloc(self.nbytes, C.byref(p)), "ftb_sym_alloc")
+        self.ptr = p.value
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": _TYPESTR[dtype],
+                                         "data": (self.ptr, False), "version": 2, "strides": None}
+
+    def __del__(self):
+        try:
+            self.A.lib.ftb_sym_free(self.ptr)
+        except Exception:
+            pass
+
+
+def _sym_tensor(shape, dtype, device):
+    own = _SymAlloc(shape, dtype)
+    t = torch.as_tensor(own, device=device)
+    return t.view(dtype) if dtype == torch.bfloat16 else t
+
+
+class PeerComm:
+    """Base of the fused-exchange transports. `sym(name, shape, dtype)` is collective
+    (every rank calls it in the same order) and returns this rank's tensor;
+    `addrs(name)` lists every rank's device address of that buffer (peer-mapped);
+    `barrier(stream)` is stream-ordered: stores issued before it on any rank are
+    visible to every rank's work enqueued after it."""
+
+    peer = True
+    capturable = False
+
+    def __init__(self, world, rank):
+        self.world, self.rank = int(world), int(rank)
+        if self.world > 8:
+            raise ConfigError("peer transport spans at most 8 ranks (one NVLink domain)")
+        self._addrs = {}
+
+    def addrs(self, name):
+        return self._addrs[name]
+
+    # collective fallbacks used outside the fused path (VAE halo, tests)
+    def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
+        raise NotImplementedError
+
+
+class ThreadPeerComm(PeerComm):
+    """g emulated ranks in one process (threads sharing one device): a rank's peer
+    addresses are the other ranks' tensors; the barrier synchronises this rank's
+    stream and meets the others on a host barrier (kernels never spin on peers)."""
+
+    def __init__(self, hub, rank):
+        super().__init__(hub.world, rank)
+        self.hub = hub
+        self._inner = ThreadComm(hub, rank)
+
+    @staticmethod
+    def make(world):
+        hub = _ThreadHub(world)
+        hub.sym = {}
+        return [ThreadPeerComm(hub, r) for r in range(world)]
+
+    def sym(self, name, shape, dtype, device):
+        t = torch.zeros(shape, dtype=dtype, device=device)
+        torch.cuda.synchronize(device)
+        self.hub.sym.setdefault(name, [None] * self.world)[self.rank] = t
+        self.hub.barrier.wait()
+        self._addrs[name] = [x.data_ptr() for x in self.hub.sym[name]]
+        self.hub.barrier.wait()
+        return t
+
+    def barrier(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        s.synchronize()
+        self.hub.barrier.wait()
+
+    def neighbor_exchange(self, *a, **k):
+        self._inner.neighbor_exchange(*a, **k)
+
+
+class IpcPeerComm(PeerComm):
+    """One process per GPU of a node: buffers from ftb_sym_alloc, cudaIpc handles
+    all-gathered through torch.distributed, imported once; barrier = ftb_peer_barrier
+    (device flag words in a symmetric buffer, per-rank epoch counter on the device,
+    so the whole chunk can be captured in a CUDA graph)."""
+
+    def __init__(self, device, group=None, timeout_s=60.0, barrier_mode="device"):
+        import torch.distributed as dist
+        super().__init__(dist.get_world_size(group), dist.get_rank(group))
+        if barrier_mode not in ("device", "host"):
+            raise ConfigError("barrier_mode must be 'device' or 'host'")
+        self.dist, self.group, self.device, self.timeout_s = dist, group, device, float(timeout_s)
+        # "host": stream sync + process-group barrier (tests that put several ranks on one
+        # GPU, where a spinning kernel must never wait on another process's kernel)
+        self.barrier_mode = barrier_mode
+        self.capturable = barrier_mode == "device"
+        self._coll = TorchComm(group)
+        self._imported = []
+        self._keep = []
+        self.flags = self.sym("__flags", (self.world,), torch.int32, device)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def sym(self, name, shape, dtype, device=None):
+        import ctypes as C
+
+        from . import _capi as A
+        t = _sym_tensor(shape, dtype, device or self.device)
+        self._keep.append(t)
+        h = C.create_string_buffer(A.IPC_HANDLE_BYTES)
+        A.check(A.lib.ftb_ipc_export(t.data_ptr(), h), "ftb_ipc_export")
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, bytes(h.raw), group=self.group)
+        addrs = []
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                addrs.append(t.data_ptr())
+                continue
+            p = C.c_void_p()
+            A.check(A.lib.ftb_ipc_import(C.create_string_buffer(hb, A.IPC_HANDLE_BYTES), C.byref(p)),
+                    "ftb_ipc_import")
+            self._imported.append(p.value)
+            addrs.append(p.value)
+        self._addrs[name] = addrs
+        return t
+
+    def barrier(self, stream=None):
+        from . import ops
+        if self.barrier_mode == "host":
+            (stream if stream is not None else torch.cuda.current_stream()).synchronize()
+            self.dist.barrier(group=self.group)
+            return
+        ops.peer_barrier(self._addrs["__flags"], self.epoch, self.rank, self.world, self.timeout_s, stream=stream)
+
+    def neighbor_exchange(self, *a, **k):
+        self._coll.neighbor_exchange(*a, **k)
+
+    def close(self):
+        from . import _capi as A
+        for p in self._imported:
+            A.lib.ftb_ipc_close(p)
+        self._imported = []

@@ -175,7 +175,18 @@ class DeviceDenoiser:
             "temb_act": torch.empty(F, m, dtype=bf, device=d),
             "e0": torch.empty(F, 6 * m, dtype=f32, device=d),
         }
-        if g > 1:
+        self.peer = g > 1 and getattr(self.comm, "peer", False)
+        if self.peer:
+            # symmetric receive buffers: the producers' epilogues store into them over NVLink
+            c = self.comm
+            self.buf["qkv_recv"] = c.sym("qkv_recv", (Lp, 3 * hw), bf, d)     # [src][Ls][3][hpr][hd]
+            self.buf["ao_recv"] = c.sym("ao_recv", (g * Ls, hw), bf, d)       # [src head group][Ls][hw]
+            self.buf["x0tok"] = c.sym("x0tok", (Lp, self.ko), f32, d)
+            r = self.plan.rank
+            self._qkv_peers = [a + r * Ls * 3 * hw * 2 for a in c.addrs("qkv_recv")]
+            self._ao_peers = [a + r * Ls * hw * 2 for a in c.addrs("ao_recv")]
+            self._x0_peers = [a + r * Ls * self.ko * 4 for a in c.addrs("x0tok")]
+        elif g > 1:
             self.buf["qkv_recv"] = torch.empty(Lp, 3 * hw, dtype=bf, device=d)
             self.buf["attn_full"] = torch.empty(Lp, hw, dtype=bf, device=d)
             self.buf["x0tok"] = torch.empty(Lp, self.ko, dtype=f32, device=d)
@@ -311,8 +322,16 @@ class DeviceDenoiser:
             else:
                 ops.norm_modulate(h, u, gamma=W.vecs[p + "ln1.g"], beta=W.vecs[p + "ln1.b"], stream=s)
             ops.gemm(u, W.mats[p + "self.wqkv"][0], qkv, "qkv_rope", heads=H_, head_dim=hd, heads_per_rank=hpr,
-                     row_offset=s0, rope=self.rope, stream=s)
-            if g == 1:
+                     row_offset=s0, rope=self.rope, peers=self._qkv_peers if self.peer else None, stream=s)
+            if self.peer:
+                # all-to-all #1 rode the QKV epilogue; #2 rides the FMHA epilogue
+                rq = B["qkv_recv"]
+                self.comm.barrier(s)
+                ops.attention_scatter(rq[:, 0:hw], rq[:, hw:2 * hw], rq[:, 2 * hw:], hpr, hd, pl.L_pad, L,
+                                      self.scale, self._ao_peers, Ls, hw, stream=s)
+                self.comm.barrier(s)
+                o_in = dict(a=B["ao_recv"], M=Ls, K=m, lda=hw, a_chunks=g, a_chunk_stride=Ls * hw)
+            elif g == 1:
                 ops.attention(qkv[:, 0:m], qkv[:, m:2 * m], qkv[:, 2 * m:], ao, H_, hd, L, L, self.scale, stream=s)
                 o_in = dict(a=ao)
             else:
@@ -348,9 +367,12 @@ class DeviceDenoiser:
             ops.norm_modulate(h, u, shift=fm[:, 0:m], scale=fm[:, m:2 * m], rows_per_group=T, row_offset=s0, stream=s)
         else:
             ops.norm_modulate(h, u, gamma=W.vecs["final.g"], beta=W.vecs["final.b"], stream=s)
-        ops.gemm(u, W.mats["out.w"][0], B["x0loc"], "f32", bias=W.vecs["out.b"], stream=s)
+        ops.gemm(u, W.mats["out.w"][0], B["x0loc"], "f32", bias=W.vecs["out.b"],
+                 peers=self._x0_peers if self.peer else None, stream=s)
         x0t = B["x0tok"]
-        if g > 1:
+        if self.peer:
+            self.comm.barrier(s)                       # all-gather rode the out-projection epilogue
+        elif g > 1:
             self.comm.all_gather(x0t, B["x0loc"], stream=s)
         if x0_out is not None:
             ops.unpatch_ddim(x0t[:L, :cfg.out_features], self.Lm, self.Lc, D, self.H, self.W, self.ph, self.pw, z,

@@ -69,9 +69,12 @@ class RopeTables:
 
 def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=0, row_offset=0,
          M=None, K=None, lda=None, a_chunks=1, a_chunk_stride=0, heads=0, head_dim=0,
-         heads_per_rank=0, rope=None, stream=None):
+         heads_per_rank=0, rope=None, peers=None, stream=None):
     """out <- epilogue(a[M,K] @ w_t[N,K]^T). `a` may be a raw buffer when
-    a_chunks > 1 (Ulysses gather: M, K, lda, a_chunk_stride explicit)."""
+    a_chunks > 1 (Ulysses gather: M, K, lda, a_chunk_stride explicit).
+    peers: device addresses (ints) for the peer-store epilogues (qkv_rope: one
+    receive block per head group; f32: replicated all-gather); `out` then only
+    fixes dtype/ldc."""
     _need(a, torch.bfloat16, "A")
     _need(w_t, torch.bfloat16, "W^T")
     N, Kw = w_t.shape
@@ -94,6 +97,12 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
         _need(bias, torch.float32, "bias")
     epi = A.Epilogue(k, rows_per_group, row_offset, A.ptr(bias), A.ptr(group_vec), group_ld, A.ptr(out), ldc,
                      heads, head_dim, heads_per_rank, C.pointer(rope.struct) if rope is not None else None)
+    if peers:
+        if len(peers) > A.MAX_PEERS:
+            raise ConfigError("at most %d peers" % A.MAX_PEERS)
+        epi.n_peers = len(peers)
+        for i, pp in enumerate(peers):
+            epi.peer_out[i] = int(pp)
     with _Prof("gemm" if PROFILE_DETAIL is None else "gemm:%s:%dx%dx%d" % (kind, M, N, K), 2.0 * M * N * K, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
         A.call("ftb_gemm_bf16", A.ptr(a), lda, a_chunks, a_chunk_stride, A.ptr(w_t), _ld(w_t), M, N, K,
                C.byref(epi), A.stream_ptr(stream))
@@ -131,6 +140,26 @@ def attention(q, k, v, out, heads, head_dim, Lq, Lk, scale, *, impl=None, stream
     with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
         A.call("ftb_attention_impl", int(impl), *args)
     return out
+
+
+def attention_scatter(q, k, v, heads, head_dim, Lq, Lk, scale, o_peers, peer_rows, ldo, *, stream=None):
+    """attention() whose output row r lands in row r % peer_rows of the buffer at
+    device address o_peers[r // peer_rows] (Ulysses all-to-all #2 in the epilogue)."""
+    for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+        _need(t, torch.bfloat16, nm)
+    if not (1 <= len(o_peers) <= A.MAX_PEERS):
+        raise ConfigError("attention_scatter: 1..%d peers" % A.MAX_PEERS)
+    arr = (C.c_void_p * len(o_peers))(*[int(x) for x in o_peers])
+    kind = "fmha" if Lk > 256 else "fmha_short_kv"
+    with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
+        A.call("ftb_attention_scatter", A.ptr(q), _ld(q), A.ptr(k), _ld(k), A.ptr(v), _ld(v), arr, len(o_peers),
+               int(peer_rows), int(ldo), Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))
+
+
+def peer_barrier(flag_ptrs, epoch, rank, world, timeout_s=30.0, *, stream=None):
+    """Stream-ordered cross-rank barrier over peer-mapped flag words (dist.PeerComm)."""
+    arr = (C.c_void_p * len(flag_ptrs))(*[int(x) for x in flag_ptrs])
+    A.call("ftb_peer_barrier", arr, A.ptr(epoch), rank, world, float(timeout_s), A.stream_ptr(stream))
 
 
 def patchify(motion, z, reference, Lm, Lc, D, H, W, ph, pw, out, stream=None):

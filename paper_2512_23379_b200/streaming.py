@@ -90,7 +90,7 @@ class DeviceStreamer:
         self.slot = 0
         self._k = 0
         self._h2d_ev = [None, None]
-        self.use_graph = use_graph and self.d.comm.world == 1
+        self.use_graph = use_graph and (self.d.comm.world == 1 or getattr(self.d.comm, "capturable", False))
         self.graph = None
         self.graph_launches = 0
         self._eager_runs = 0

@@ -1,0 +1,50 @@
+"""FMHA variant check + timing: each impl vs torch SDPA on the 14B/1.3B shapes and
+ragged cases. Usage: python scripts/attn_bench.py [impl ...]"""
+import math
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2512_23379_b200 import ops  # noqa: E402
+
+
+def timeit(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def main():
+    impls = [int(a) for a in sys.argv[1:]] or [0]
+    dev = torch.device("cuda")
+    torch.manual_seed(0)
+    for (Lq, Lk, H, hd) in [(300, 300, 2, 128), (257, 70, 3, 64), (1000, 129, 2, 128), (4096, 4096, 4, 64)]:
+        q, k, v = (torch.randn(L, H * hd, device=dev).to(torch.bfloat16) for L in (Lq, Lk, Lk))
+        qt, kt, vt = (x.view(-1, H, hd).transpose(0, 1).float() for x in (q, k, v))
+        ref = torch.nn.functional.scaled_dot_product_attention(qt, kt, vt).transpose(0, 1).reshape(Lq, H * hd)
+        for impl in impls:
+            o = torch.zeros(Lq, H * hd, device=dev, dtype=torch.bfloat16)
+            ops.attention(q, k, v, o, H, hd, Lq, Lk, 1 / math.sqrt(hd), impl=impl)
+            torch.cuda.synchronize()
+            err = ((o.float() - ref).norm() / ref.norm()).item()
+            print("check impl=%d Lq=%d Lk=%d H=%d hd=%d rel=%.2e" % (impl, Lq, Lk, H, hd, err), flush=True)
+    L = 10530
+    for (H, hd, tag) in [(40, 128, "attn14b"), (12, 128, "attn1.3b")]:
+        q, k, v = (torch.randn(L, H * hd, device=dev).to(torch.bfloat16) for _ in range(3))
+        o = torch.empty_like(q)
+        fl = 4.0 * L * L * H * hd
+        for impl in impls:
+            t = timeit(lambda: ops.attention(q, k, v, o, H, hd, L, L, 1 / math.sqrt(hd), impl=impl))
+            print("%s impl=%d %.3f ms %.0f TFLOP/s" % (tag, impl, t, fl / t / 1e9), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -30,12 +30,13 @@ def _setup(heads=4, hd=64, Lc=3, Lm=1, H=12, W=18, layers=2, seed=5):
     return cfg, store, x, (Lc, Lm, H, W)
 
 
-def _run(cfg, store, x, geo, world, dev):
-    from paper_2512_23379_b200.dist import ThreadComm
+def _run(cfg, store, x, geo, world, dev, transport="coll"):
+    from paper_2512_23379_b200.dist import ThreadComm, ThreadPeerComm
     from paper_2512_23379_b200.model import DeviceDenoiser, DeviceWeights
     Lc, Lm, H, W = geo
     w = DeviceWeights.from_host(cfg, store.params, dev)
-    comms = ThreadComm.make(world) if world > 1 else [None]
+    make = ThreadPeerComm.make if transport == "peer" else ThreadComm.make
+    comms = make(world) if world > 1 else [None]
     out, errs = [None] * world, []
     frame_t = np.where(np.arange(Lc) < Lm, 0.0, 0.75)
 
@@ -76,6 +77,49 @@ def test_ulysses_matches_single_rank(cuda, world):
                                                        latent_dim=16, patch=(1, 2, 2), audio_tokens=2, audio_dim=16),
                      x["motion"], x["z"], x["ref"], x["audio"], frame_t)
     assert rel(many[0], ref) < 1e-2
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ulysses_peer_epilogues_match_collectives(cuda, world):
+    """Fused transport (QKV / FMHA / out-projection epilogues storing into the peers'
+    receive buffers, barrier after each producer) == the NCCL-style collective
+    transport, bit for bit: same kernels, same operands, only the store targets move."""
+    cfg, store, x, geo = _setup()
+    coll, _ = _run(cfg, store, x, geo, world, cuda, "coll")
+    peer, _ = _run(cfg, store, x, geo, world, cuda, "peer")
+    for r in range(world):
+        assert np.array_equal(peer[r], coll[r]), r
+    assert all(np.array_equal(peer[r], peer[0]) for r in range(world))   # replicated x0
+
+
+def test_ulysses_peer_padding_path(cuda):
+    cfg, store, x, geo = _setup(Lc=3, Lm=1, H=12, W=18)
+    one, _ = _run(cfg, store, x, geo, 1, cuda)
+    many, _ = _run(cfg, store, x, geo, 4, cuda, "peer")
+    assert rel(many[3], one[0]) < 5e-3
+
+
+def test_peer_barrier_kernel_single_rank(cuda):
+    """Device barrier mechanics at world 1 (signals and waits on itself): the epoch
+    counter advances once per call, also when replayed from a CUDA graph."""
+    from paper_2512_23379_b200 import ops
+    flags = torch.zeros(1, dtype=torch.int32, device=cuda)
+    epoch = torch.zeros(1, dtype=torch.int32, device=cuda)
+    for _ in range(3):
+        ops.peer_barrier([flags.data_ptr()], epoch, 0, 1, 5.0)
+    torch.cuda.synchronize()
+    assert int(epoch.item()) == 3 and int(flags.item()) == 3
+    s = torch.cuda.Stream(device=cuda)
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ops.peer_barrier([flags.data_ptr()], epoch, 0, 1, 5.0)
+        ops.peer_barrier([flags.data_ptr()], epoch, 0, 1, 5.0)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    assert int(epoch.item()) == 7 and int(flags.item()) == 7
 
 
 def test_ulysses_padding_path(cuda):
