@@ -259,10 +259,20 @@ def main():
         d.stage_cond(windows[c], ref_host, 0)
         cond_all.append(d._cond_stage[0].to(dev))
 
-    def chunk(c):
+    marks = []   # per-chunk (start, denoised, decoded) events: component split for latency.py
+
+    def chunk(c, mark=False):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if mark else None
+        if mark:
+            ev[0].record(stream)
         x0 = ds.run_resident(z_all[c], cond_all[c])
+        if mark:
+            ev[1].record(stream)
         if vae is not None:
             vae.decode_device_tensor(x0, stream)
+        if mark:
+            ev[2].record(stream)
+            marks.append(ev)
 
     # ---------------- warm-up (also fills the per-ladder AdaLN cache)
     for c in range(args.warmup):
@@ -277,7 +287,7 @@ def main():
     torch.cuda.synchronize()
     e0.record(stream)
     for c in range(args.warmup, nsteps):
-        chunk(c)
+        chunk(c, mark=True)
     e1.record(stream)
     torch.cuda.synchronize()
     launches = _capi.LAUNCHES[0] - launches0 + (ds.graph_launches * args.steps if ds.graph is not None else 0)
@@ -288,6 +298,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     fps = frames_per_chunk * 1000.0 / ms   # one stream sharded over all ranks (strong scaling)
+    comp = {"denoise": float(np.mean([a.elapsed_time(b) for a, b, _ in marks])),
+            "decode": float(np.mean([b.elapsed_time(c) for _, b, c in marks])),
+            "steps_per_chunk": scfg.sampler.steps, "frames_per_chunk": frames_per_chunk}
 
     # ---------------- e2e through the public engine API (host inputs, D2H result)
     e2e = None
@@ -392,6 +405,7 @@ def main():
                            "decode": "causal VAE decoder, 7 latents -> 28 RGB8 frames %dx%d" % (Hpx, Wpx)
                            if vae is not None else "none",
                            "l2": "working set > L2 (weights %.1f GB)" % (w.nbytes() / 1e9)},
+                "components_ms": comp,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk}
         print(json.dumps(line), flush=True)

@@ -687,7 +687,7 @@ static int attention_run(int32_t impl, AttnParams& p, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (impl == 0 || impl == 2) {
     if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
-    if (impl == 0) {  // 2 Q tiles per CTA, ping-pong softmax warpgroups
+    if (impl == 0) {  // 2 Q tiles per CTA, two softmax warpgroups
       if (head_dim == 128) return launch_fmha2<128>(p, s);
       if (head_dim == 64) return launch_fmha2<64>(p, s);
     } else {          // v1: 1 Q tile per CTA

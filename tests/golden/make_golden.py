@@ -14,6 +14,7 @@ What is frozen (reference call sites in parentheses):
   r_*     rollout_stream over 5 chunks + Codec.decode (metrics.py:128-149, world.py:206-210)
   e_*     threaded StreamSession (streaming.py:123-356): emitted indices/states
   w_*     chunk windows incl. pre-roll and motion_len=0 geometry (streaming.py:259-270)
+  r_P/r_w world identity injection and mouth readout (world.py:76-120) for the server tests
 """
 
 import os
@@ -111,6 +112,9 @@ def main():
     ctx = make_stream_context(world, codec, 3, 0, 35)
     gen = NetGenerator(stores["default"], cfg, SamplerPlan())
     targets, motions = rollout_stream(gen, ctx, 35)
+    # world readouts for the WebSocket front door (world.py:76-120): identity injection P, mouth w
+    from ftlk.world import sample_identity
+    g.update(r_P=world.P, r_w=world.w, r_identity=sample_identity(1, world.spec.identity_dim))
     g.update(r_Q=world.Q, r_seed=np.array(ctx.seed, dtype=np.uint64), r_signal=ctx.signal,
              r_reference_latent=ctx.reference_latent, r_reference_frame=ctx.reference_frame,
              r_targets=targets, r_motions=np.stack(motions), r_frames=codec.decode(targets))
