@@ -108,6 +108,10 @@ int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t N,
                       int32_t rows_per_group, int64_t row_offset, float eps,
                       void* y, int64_t ldy, float* mean_out, float* rstd_out, void* stream);
 
+/* Norm kernel variant (benchmarks): 0 auto (register-resident vector kernel when the row
+ * fits), 1 generic three-pass kernel. */
+int ftb_set_norm_variant(int32_t variant);
+
 /* ---------------------------------------------------------------- attention */
 /* o[r, h*hd + d] = softmax_j(q_r . k_j * scale) v_j  per head h (bidirectional, no mask
  * beyond Lk). Row r of q at q + r*ldq + h*head_dim (bf16); same for k, v, o. */

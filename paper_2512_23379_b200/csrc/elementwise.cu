@@ -66,6 +66,74 @@ __global__ void __launch_bounds__(THREADS) norm_modulate_kernel(
   }
 }
 
+// Register-resident variant (N % 4 == 0, N <= 4*T*VMAX, 16-byte aligned rows): the
+// row is read from HBM once as float4, both passes run on registers, and the output
+// leaves as bf16x4. Same arithmetic as norm_modulate_kernel (two-pass fp32).
+template <int VMAX, int T, bool STREAM>
+__global__ void __launch_bounds__(T) norm_modulate_vec_kernel(
+    const float* __restrict__ x, long long ldx, int N, const float* __restrict__ gamma,
+    const float* __restrict__ beta, const float* __restrict__ scale, const float* __restrict__ shift,
+    long long mod_ld, int rows_per_group, long long row_offset, float eps, __nv_bfloat16* __restrict__ y,
+    long long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  __shared__ float red[T / 32];
+  const long long row = blockIdx.x;
+  const int n4 = N >> 2;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
+  float4 v[VMAX];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VMAX; ++i) {
+    const int c = threadIdx.x + i * T;
+    v[i] = c < n4 ? (STREAM ? __ldcs(xr + c) : __ldg(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mean = block_sum<T>(s, red) / N;
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VMAX; ++i) {
+    if (threadIdx.x + i * T < n4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+      ss += (a * a + b * b) + (c * c + d * d);
+    }
+  }
+  const float rstd = rsqrtf(block_sum<T>(ss, red) / N + eps);
+  const long long g = rows_per_group > 0 ? (row + row_offset) / rows_per_group : 0;
+  const float4* sc = scale ? reinterpret_cast<const float4*>(scale + g * mod_ld) : nullptr;
+  const float4* sh = shift ? reinterpret_cast<const float4*>(shift + g * mod_ld) : nullptr;
+  const float4* ga = reinterpret_cast<const float4*>(gamma);
+  const float4* be = reinterpret_cast<const float4*>(beta);
+  uint2* yr = reinterpret_cast<uint2*>(y + row * ldy);
+#pragma unroll
+  for (int i = 0; i < VMAX; ++i) {
+    const int c = threadIdx.x + i * T;
+    if (c < n4) {
+      float4 o = make_float4((v[i].x - mean) * rstd, (v[i].y - mean) * rstd, (v[i].z - mean) * rstd,
+                             (v[i].w - mean) * rstd);
+      if (gamma) {
+        const float4 t = __ldg(ga + c);
+        o = make_float4(o.x * t.x, o.y * t.y, o.z * t.z, o.w * t.w);
+      }
+      if (sc) {
+        const float4 t = __ldg(sc + c);
+        o = make_float4(o.x * (1.f + t.x), o.y * (1.f + t.y), o.z * (1.f + t.z), o.w * (1.f + t.w));
+      }
+      if (beta) {
+        const float4 t = __ldg(be + c);
+        o = make_float4(o.x + t.x, o.y + t.y, o.z + t.z, o.w + t.w);
+      }
+      if (sh) {
+        const float4 t = __ldg(sh + c);
+        o = make_float4(o.x + t.x, o.y + t.y, o.z + t.z, o.w + t.w);
+      }
+      yr[c] = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (mean_out) mean_out[row] = mean;
+    if (rstd_out) rstd_out[row] = rstd;
+  }
+}
+
 // Composite assembly (diffusion.py:150-179 + stacked :133-135) fused with the
 // 2x2 spatial patchify of the wan-mode token grid. One thread per output element.
 __global__ void patchify_kernel(const float* __restrict__ motion, const float* __restrict__ z,
@@ -212,6 +280,12 @@ static inline int grid_for(long long n, int threads) {
 using namespace ftb;
 #define S(stream) reinterpret_cast<cudaStream_t>(stream)
 
+static int g_norm_variant = 0;
+extern "C" int ftb_set_norm_variant(int32_t v) {
+  g_norm_variant = v;
+  return FTB_OK;
+}
+
 extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t N, const float* gamma,
                                  const float* beta, const float* scale, const float* shift, int64_t mod_ld,
                                  int32_t rows_per_group, int64_t row_offset, float eps, void* y, int64_t ldy,
@@ -219,7 +293,26 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
   if (!x || !y || M < 0 || N <= 0) return set_error(FTB_EINVAL, "norm: bad arguments");
   if (M == 0) return FTB_OK;
   if ((scale || shift) && rows_per_group <= 0) return set_error(FTB_EINVAL, "norm: modulation needs rows_per_group");
-  if (N >= 1024)
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool vec = (N % 4 == 0) && N <= 4 * 256 * 8 && (ldx % 4 == 0) && (ldy % 4 == 0) && (!scale || mod_ld % 4 == 0) &&
+                   al16(x) && (reinterpret_cast<uintptr_t>(y) & 7) == 0 && (!gamma || al16(gamma)) &&
+                   (!beta || al16(beta)) && (!scale || al16(scale)) && (!shift || al16(shift)) && N >= 512;
+  if (vec && g_norm_variant != 1) {
+    const int nv = (N / 4 + 255) / 256;   // float4 per thread at 256 threads
+#define FTB_NORM_VEC(V)                                                                                             \
+  norm_modulate_vec_kernel<V, 256, true><<<M, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, \
+                                                                   rows_per_group, row_offset, eps,              \
+                                                                   (__nv_bfloat16*)y, ldy, mean_out, rstd_out)
+    if (nv <= 2)
+      FTB_NORM_VEC(2);
+    else if (nv <= 4)
+      FTB_NORM_VEC(4);
+    else if (nv <= 5)
+      FTB_NORM_VEC(5);
+    else
+      FTB_NORM_VEC(8);
+#undef FTB_NORM_VEC
+  } else if (N >= 1024)
     norm_modulate_kernel<256><<<M, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, rows_per_group,
                                                           row_offset, eps, (__nv_bfloat16*)y, ldy, mean_out, rstd_out);
   else

@@ -1,5 +1,5 @@
 """Run each hot kernel at its 14B-shape size a few times (for ncu capture).
-usage: python scripts/profile_kernels.py [gemm|fmha|cross|conv|all]"""
+usage: python scripts/profile_kernels.py [gemm|oproj|ffn2|norm|fmha|cross|conv|all]"""
 import math
 import sys
 
@@ -19,6 +19,22 @@ def main(which):
         out = torch.empty(L, 3 * m, device=dev, dtype=torch.bfloat16)
         for _ in range(3):
             ops.gemm(a, w, out, "bf16")
+    if which in ("oproj", "ffn2", "all"):
+        K = m if which != "ffn2" else 13824
+        a = torch.randn(L, K, device=dev).to(torch.bfloat16)
+        w = (torch.randn(m, K, device=dev) / 70).to(torch.bfloat16)
+        h = torch.randn(L, m, device=dev)
+        gate = torch.randn(10, m, device=dev)
+        for _ in range(3):
+            ops.gemm(a, w, h, "resid_f32", group_vec=gate, rows_per_group=1170)
+    if which in ("norm", "all"):
+        h = torch.randn(L, m, device=dev)
+        u = torch.empty(L, m, device=dev, dtype=torch.bfloat16)
+        mod = torch.randn(10, 2 * m, device=dev)
+        for var in (1, 0):
+            A.call("ftb_set_norm_variant", var)
+            for _ in range(2):
+                ops.norm_modulate(h, u, shift=mod[:, :m], scale=mod[:, m:], rows_per_group=1170)
     if which in ("fmha", "all"):
         q = torch.randn(L, H * hd, device=dev).to(torch.bfloat16)
         o = torch.empty_like(q)

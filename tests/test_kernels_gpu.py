@@ -184,7 +184,7 @@ def test_attention_small(ops, cuda, Lq, Lk, heads, hd):
     assert rel(o.float(), torch_attn(q, k, v, heads, hd, scale)) < 5e-3
 
 
-@pytest.mark.parametrize("M,N", [(9, 32), (300, 1536), (17, 5120)])
+@pytest.mark.parametrize("M,N", [(9, 32), (300, 1536), (17, 5120), (5, 6144), (7, 1000), (3, 1030), (4, 8200)])
 def test_norm_modulate(ops, cuda, M, N):
     g = torch.Generator().manual_seed(N)
     x = (torch.randn(M, N, generator=g) * 3 + 1.5).to(cuda)
