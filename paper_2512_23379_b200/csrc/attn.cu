@@ -535,6 +535,316 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ============================================================ short-KV tcgen05 kernel
+// Cross-attention of the wan DiT: 10 530 queries against Lk <= 128 conditioning keys
+// (37 at the 14B shape). One key block, so the softmax is exact (no running max).
+// Persistent CTAs (two per SM: 256 TMEM columns, < 100 KB smem each) walk a contiguous
+// run of (head, query tile) items, so K/V (NKP = roundup(Lk, 16) rows) reload only when
+// the head changes; Q of item k+1 loads while item k computes, and the MMA warp issues
+// S(k+1) while the epilogue of item k drains O, so the kernel streams at the HBM rate of
+// reading Q and writing O. TMEM: S/P [0,128) (P bf16 pairs aliased on S), O [128, 128+HD).
+// The epilogue stages the bf16 O tile in the item's (consumed) Q slot and warp 3 writes it
+// with TMA stores, so HBM sees full-line writes (TSTORE; the Ulysses scatter epilogue
+// keeps per-row stores).
+template <int HD>
+struct XattnCfg {
+  static constexpr int QBOX = 128 * 64 * 2;
+  static constexpr int NBOX = HD / 64;
+  static constexpr int QTILE = NBOX * QBOX;
+  static constexpr int KVBOX = 128 * 64 * 2;          // sized for NKP <= 128
+  static constexpr int KVTILE = NBOX * KVBOX;
+  static constexpr int OFF_Q = 0;                     // [2] Q tiles
+  static constexpr int OFF_K = OFF_Q + 2 * QTILE;
+  static constexpr int OFF_V = OFF_K + KVTILE;
+  static constexpr int OFF_BAR = OFF_V + KVTILE;
+  static constexpr int SMEM_MAX = OFF_BAR + 256 + 1024;
+};
+
+template <int HD, int KMAX, bool TSTORE>
+__global__ void __launch_bounds__(256, KMAX == 64 ? 2 : 1)
+    xattn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                    const AttnParams p, int nkp, int n_qt) {
+  using C = XattnCfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int kvbox = nkp * 128;                        // bytes of one 64-column K/V box
+  const int kvtile = C::NBOX * kvbox;
+  uint8_t* sQ = smem + C::OFF_Q;
+  uint8_t* sK = sQ + 2 * C::QTILE;
+  uint8_t* sV = sK + kvtile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kvtile);
+  uint64_t* in_full = bars + 0;   // [2] Q tile
+  uint64_t* in_empty = bars + 2;  // [2]
+  uint64_t* s_full = bars + 4;
+  uint64_t* p_full = bars + 5;
+  uint64_t* o_full = bars + 6;
+  uint64_t* o_free = bars + 7;
+  uint64_t* kv_full = bars + 8;   // K/V of the current head
+  uint64_t* kv_empty = bars + 9;
+  uint64_t* staged = bars + 10;   // [2] O tile of slot b written to smem (TSTORE)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = warp_id(), lane = lane_id();
+  const long long n_items = (long long)n_qt * p.heads;
+  const int first = (int)(n_items * blockIdx.x / gridDim.x);
+  const int last = (int)(n_items * (blockIdx.x + 1) / gridDim.x);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&in_full[b], 1);
+      mbar_init(&in_empty[b], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(o_full, 1);
+    mbar_init(o_free, 4);
+    mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
+    mbar_init(&staged[0], 4);
+    mbar_init(&staged[1], 4);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int k = 0, hk = 0, cur = -1;
+      for (int it = first; it < last; ++it, ++k) {
+        const int b = k & 1;
+        const int head = it / n_qt, qt = it - head * n_qt;
+        if (head != cur) {  // new head: K/V reload once the previous head's PVs are done
+          mbar_wait(kv_empty, (hk & 1) ^ 1);
+          mbar_arrive_expect_tx(kv_full, 2 * kvtile);
+          for (int x = 0; x < C::NBOX; ++x) {
+            tma_load_2d(sK + x * kvbox, &tmK, kv_full, head * HD + 64 * x, 0);
+            tma_load_2d(sV + x * kvbox, &tmV, kv_full, head * HD + 64 * x, 0);
+          }
+          cur = head;
+          ++hk;
+        }
+        mbar_wait(&in_empty[b], ((k >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&in_full[b], C::QTILE);
+        for (int x = 0; x < C::NBOX; ++x)
+          tma_load_2d(sQ + b * C::QTILE + x * C::QBOX, &tmQ, &in_full[b], head * HD + 64 * x, qt * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc_s = idesc_bf16(128, nkp, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
+      int k = 0, hk = 0, cur = -1;
+      for (int it = first; it < last; ++it, ++k) {
+        const int b = k & 1;
+        const int head = it / n_qt;
+        if (head != cur) {
+          mbar_wait(kv_full, hk & 1);
+          cur = head;
+          ++hk;
+        }
+        mbar_wait(&in_full[b], (k >> 1) & 1);
+        // S(k) overwrites P(k-1): ordered after PV(k-1) on the tensor pipe; the softmax
+        // of item k-1 finished with S before it wrote P (p_full), which PV(k-1) waited on.
+        tc_fence_after();
+        const uint32_t sq = smem_u32(sQ + b * C::QTILE), sk = smem_u32(sK);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t offq = (kk >> 2) * C::QBOX + (kk & 3) * 32;
+          const uint32_t offk = (kk >> 2) * kvbox + (kk & 3) * 32;
+          mma_bf16_ss(tmem, sdesc_sw128(sq + offq, 16, 1024), sdesc_sw128(sk + offk, 16, 1024), idesc_s, kk > 0);
+        }
+        mma_commit(s_full);
+        mbar_wait(p_full, k & 1);
+        if (k > 0) mbar_wait(o_free, (k - 1) & 1);   // epilogue of item k-1 has read O
+        tc_fence_after();
+        const uint32_t sv = smem_u32(sV);
+        for (int kk = 0; kk < nkp / 16; ++kk) {
+          const uint64_t bd = sdesc_sw128(sv + kk * 16 * 128, kvbox, 1024);
+          mma_bf16_ts(tmem + 128, tmem + kk * 8, bd, idesc_o, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(o_full);
+        if (!TSTORE) mma_commit(&in_empty[b]);   // TSTORE: freed by the store warp
+        if (it + 1 == last || (it + 1) / n_qt != head) mma_commit(kv_empty);  // head done with K/V
+      }
+    }
+  } else if (warp == 3) {
+    if (TSTORE && lane == 0) {
+      int k = 0;
+      for (int it = first; it < last; ++it, ++k) {
+        const int b = k & 1;
+        const int head = it / n_qt, qt = it - head * n_qt;
+        mbar_wait(&staged[b], (k >> 1) & 1);
+        for (int x = 0; x < C::NBOX; ++x) tma_store_2d(&tmO, sQ + b * C::QTILE + x * C::QBOX, head * HD + 64 * x, qt * 128);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&in_empty[b]);   // slot b may take the Q tile of item k+2
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+  } else if (warp >= 4) {
+    const int qw = warp & 3;
+    const int row = qw * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(qw * 32) << 16;
+    const uint32_t tS = tmem + lane_off, tO = tmem + lane_off + 128;
+    int k = 0;
+    for (int it = first; it < last; ++it, ++k) {
+      const int head = it / n_qt, qt = it - head * n_qt;
+      mbar_wait(s_full, k & 1);
+      tc_fence_after();
+      uint32_t sr[KMAX];
+#pragma unroll
+      for (int c = 0; c < KMAX / 32; ++c)
+        if (c * 32 < nkp) tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
+      tmem_ld_wait();
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < KMAX; ++c)
+        if (c < p.Lk) mx = fmaxf(mx, __uint_as_float(sr[c]));
+      mx *= p.scale_log2;
+      float l = 0.f;
+#pragma unroll
+      for (int c = 0; c < KMAX; c += 2) {
+        if (c < nkp) {
+          const float e0 = c < p.Lk ? ex2(fmaf(__uint_as_float(sr[c]), p.scale_log2, -mx)) : 0.f;
+          const float e1 = c + 1 < p.Lk ? ex2(fmaf(__uint_as_float(sr[c + 1]), p.scale_log2, -mx)) : 0.f;
+          l += e0 + e1;
+          sr[c >> 1] = pack_bf16(e0, e1);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < KMAX / 64; ++c)
+        if (c * 64 < nkp) tmem_st32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sr + c * 32));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      mbar_wait(o_full, k & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const long long grow = (long long)qt * 128 + row;
+      if (TSTORE) {
+        uint8_t* stg = sQ + (k & 1) * C::QTILE + row * 128;
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld32(tO + c0, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q8 = 0; q8 < 4; ++q8) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(o[8 * q8 + 0]) * inv, __uint_as_float(o[8 * q8 + 1]) * inv);
+            w.y = pack_bf16(__uint_as_float(o[8 * q8 + 2]) * inv, __uint_as_float(o[8 * q8 + 3]) * inv);
+            w.z = pack_bf16(__uint_as_float(o[8 * q8 + 4]) * inv, __uint_as_float(o[8 * q8 + 5]) * inv);
+            w.w = pack_bf16(__uint_as_float(o[8 * q8 + 6]) * inv, __uint_as_float(o[8 * q8 + 7]) * inv);
+            const int c16 = ((c0 & 63) >> 3) + q8;   // 16-byte chunk within the 128-byte row
+            *reinterpret_cast<uint4*>(stg + (c0 >> 6) * C::QBOX + ((c16 ^ (row & 7)) << 4)) = w;
+          }
+        }
+      } else {
+        __nv_bfloat16* orow = attn_out_row(p, grow < p.Lq ? grow : 0) + head * HD;
+#pragma unroll 1
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+          uint32_t o[32];
+          tmem_ld32(tO + c0, o);
+          tmem_ld_wait();
+          if (grow < p.Lq) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+            for (int q8 = 0; q8 < 4; ++q8) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(o[8 * q8 + 0]) * inv, __uint_as_float(o[8 * q8 + 1]) * inv);
+              w.y = pack_bf16(__uint_as_float(o[8 * q8 + 2]) * inv, __uint_as_float(o[8 * q8 + 3]) * inv);
+              w.z = pack_bf16(__uint_as_float(o[8 * q8 + 4]) * inv, __uint_as_float(o[8 * q8 + 5]) * inv);
+              w.w = pack_bf16(__uint_as_float(o[8 * q8 + 6]) * inv, __uint_as_float(o[8 * q8 + 7]) * inv);
+              dst[q8] = w;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      if (TSTORE) fence_proxy_async_smem();  // staged tile visible to the TMA (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(o_free);   // O drained: PV(k+1) may overwrite it
+        if (TSTORE) mbar_arrive(&staged[k & 1]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<256>(tmem);
+}
+
+// Output columns the TMA store may touch: all heads of this call.
+static long long head_cols(const AttnParams& p) { return (long long)p.heads * p.hd; }
+
+template <int HD>
+static int launch_xattn(const AttnParams& p, cudaStream_t s) {
+  using C = XattnCfg<HD>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaSuccess;
+    for (auto fn : {xattn_tc_kernel<HD, 64, true>, xattn_tc_kernel<HD, 128, true>, xattn_tc_kernel<HD, 64, false>,
+                    xattn_tc_kernel<HD, 128, false>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_MAX);
+    if (e != cudaSuccess) return set_cuda_error(e, "xattn smem attribute");
+    configured = true;
+  }
+  const int nkp = (p.Lk + 15) & ~15;
+  CUtensorMap tq, tk, tv;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)p.ldq, (uint64_t)p.Lq};
+    uint64_t strides[1] = {(uint64_t)p.ldq * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = make_tmap_bf16(&tq, p.q, 2, dims, strides, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)p.ldk, (uint64_t)p.Lk};
+    uint64_t strides[1] = {(uint64_t)p.ldk * 2};
+    uint32_t box[2] = {64, (uint32_t)nkp};
+    if ((rc = make_tmap_bf16(&tk, p.k, 2, dims, strides, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)p.ldv, (uint64_t)p.Lk};
+    uint64_t strides[1] = {(uint64_t)p.ldv * 2};
+    uint32_t box[2] = {64, (uint32_t)nkp};
+    if ((rc = make_tmap_bf16(&tv, p.v, 2, dims, strides, box))) return rc;
+  }
+  CUtensorMap to{};
+  const bool tstore = p.n_peers == 0;
+  if (tstore) {
+    uint64_t dims[2] = {(uint64_t)(head_cols(p)), (uint64_t)p.Lq};
+    uint64_t strides[1] = {(uint64_t)p.ldo * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = make_tmap_bf16(&to, p.o, 2, dims, strides, box))) return rc;
+  }
+  const int n_qt = (p.Lq + 127) / 128;
+  const int items = n_qt * p.heads;
+  const int smem = C::OFF_K + 2 * (C::NBOX * nkp * 128) + 256 + 1024;
+  const int grid = items < 2 * sm_count() ? items : 2 * sm_count();
+  if (tstore) {
+    if (nkp <= 64)
+      xattn_tc_kernel<HD, 64, true><<<grid, 256, smem, s>>>(tq, tk, tv, to, p, nkp, n_qt);
+    else
+      xattn_tc_kernel<HD, 128, true><<<grid, 256, smem, s>>>(tq, tk, tv, to, p, nkp, n_qt);
+  } else {
+    if (nkp <= 64)
+      xattn_tc_kernel<HD, 64, false><<<grid, 256, smem, s>>>(tq, tk, tv, to, p, nkp, n_qt);
+    else
+      xattn_tc_kernel<HD, 128, false><<<grid, 256, smem, s>>>(tq, tk, tv, to, p, nkp, n_qt);
+  }
+  return check_launch("xattn_tc_kernel");
+}
+
 // ============================================================ short-KV CUDA-core kernel
 // grid (ceil(Lq/16), heads), 128 threads: warp w owns query rows 4w..4w+3 of the block.
 // HDMAX bounds the shared-memory tile; the head width itself is runtime (any hd <= HDMAX).
@@ -685,6 +995,13 @@ static int attention_run(int32_t impl, AttnParams& p, void* stream) {
   const long long ldq = p.ldq, ldk = p.ldk, ldv = p.ldv, ldo = p.ldo;
   const int head_dim = p.hd;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (impl == 3) {  // short-KV tcgen05 kernel (Lk <= 128)
+    if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "xattn: ld alignment");
+    if (p.Lk > 128) return set_error(FTB_EINVAL, "xattn: Lk must be <= 128");
+    if (head_dim == 128) return launch_xattn<128>(p, s);
+    if (head_dim == 64) return launch_xattn<64>(p, s);
+    return set_error(FTB_EINVAL, "xattn: head_dim must be 64 or 128");
+  }
   if (impl == 0 || impl == 2) {
     if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
     if (impl == 0) {  // 2 Q tiles per CTA, two softmax warpgroups
@@ -703,7 +1020,10 @@ static int attention_run(int32_t impl, AttnParams& p, void* stream) {
   return set_error(FTB_EINVAL, "attention: head_dim must be <= 128");
 }
 
-static int default_impl(int Lq, int head_dim) { return ((head_dim == 64 || head_dim == 128) && Lq >= 64) ? 0 : 1; }
+static int default_impl(int Lq, int Lk, int head_dim) {
+  if ((head_dim == 64 || head_dim == 128) && Lq >= 64) return Lk <= 128 ? 3 : 0;
+  return 1;
+}
 
 extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                                   int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads,
@@ -756,11 +1076,11 @@ extern "C" int ftb_attention_scatter(const void* q, int64_t ldq, const void* k, 
   p.n_peers = n_peers;
   p.peer_rows = peer_rows;
   for (int i = 0; i < n_peers; ++i) p.o_peers[i] = (__nv_bfloat16*)o_peers[i];
-  return attention_run(default_impl(Lq, head_dim), p, stream);
+  return attention_run(default_impl(Lq, Lk, head_dim), p, stream);
 }
 
 extern "C" int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                              void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
                              float scale, void* stream) {
-  return ftb_attention_impl(default_impl(Lq, head_dim), q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim, scale, stream);
+  return ftb_attention_impl(default_impl(Lq, Lk, head_dim), q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim, scale, stream);
 }

@@ -134,9 +134,9 @@ def attention(q, k, v, out, heads, head_dim, Lq, Lk, scale, *, impl=None, stream
         _need(t, torch.bfloat16, nm)
     args = (A.ptr(q), _ld(q), A.ptr(k), _ld(k), A.ptr(v), _ld(v), A.ptr(out), _ld(out),
             Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))
-    if impl is None:
-        impl = 0 if (head_dim in (64, 128) and Lq >= 64) else 1
-    kind = ("fmha" if Lk > 256 else "fmha_short_kv") if impl in (0, 2) else "attn_small"
+    if impl is None:   # the library's dispatch (ftb_attention): short-KV tcgen05 kernel when Lk <= 128
+        impl = (3 if Lk <= 128 else 0) if (head_dim in (64, 128) and Lq >= 64) else 1
+    kind = {0: "fmha", 2: "fmha", 3: "xattn"}.get(impl, "attn_small")
     with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
         A.call("ftb_attention_impl", int(impl), *args)
     return out
@@ -150,7 +150,7 @@ def attention_scatter(q, k, v, heads, head_dim, Lq, Lk, scale, o_peers, peer_row
     if not (1 <= len(o_peers) <= A.MAX_PEERS):
         raise ConfigError("attention_scatter: 1..%d peers" % A.MAX_PEERS)
     arr = (C.c_void_p * len(o_peers))(*[int(x) for x in o_peers])
-    kind = "fmha" if Lk > 256 else "fmha_short_kv"
+    kind = "fmha" if Lk > 128 else "xattn"
     with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
         A.call("ftb_attention_scatter", A.ptr(q), _ld(q), A.ptr(k), _ld(k), A.ptr(v), _ld(v), arr, len(o_peers),
                int(peer_rows), int(ldo), Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))

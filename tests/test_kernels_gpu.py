@@ -171,6 +171,41 @@ def test_fmha_strided_qkv_layout(ops, cuda):
     assert rel(o.float(), torch_attn(q, k, v, heads, hd, 1 / math.sqrt(hd))) < 1e-2
 
 
+@pytest.mark.parametrize("Lq,Lk,heads,hd", [(1170, 37, 4, 128), (10530 // 8, 37, 5, 128), (300, 128, 2, 64),
+                                            (129, 1, 1, 128), (2000, 65, 3, 128), (64, 16, 2, 64)])
+def test_xattn_short_kv(ops, cuda, Lq, Lk, heads, hd):
+    """Short-KV tcgen05 kernel (cross-attention, Lk <= 128): TMA-stored output into a
+    strided view (only its own head columns written) and the default dispatch."""
+    g = torch.Generator().manual_seed(Lq + 7 * Lk)
+    q = bf(torch.randn(Lq, heads * hd, generator=g) * 2).to(cuda)
+    kv = bf(torch.randn(Lk, 2 * heads * hd, generator=g)).to(cuda)
+    k, v = kv[:, :heads * hd], kv[:, heads * hd:]
+    big = torch.full((Lq, heads * hd + 64), 7.0, device=cuda).to(torch.bfloat16)
+    o = big[:, :heads * hd]
+    scale = 1 / math.sqrt(hd)
+    ops.attention(q, k, v, o, heads, hd, Lq, Lk, scale, impl=3)
+    want = torch_attn(q, k, v, heads, hd, scale)
+    assert rel(o.float(), want) < 5e-3
+    assert torch.all(big[:, heads * hd:] == 7.0)          # TMA store clipped to the view
+    o2 = torch.empty_like(o)
+    ops.attention(q, k, v, o2, heads, hd, Lq, Lk, scale)  # default dispatch picks the same kernel
+    assert torch.equal(o2, o)
+
+
+def test_xattn_scatter_rows(ops, cuda):
+    """Ulysses scatter epilogue on the short-KV kernel: row r -> peer r // rows."""
+    Lq, Lk, heads, hd, g_ = 300, 37, 2, 128, 3
+    gen = torch.Generator().manual_seed(3)
+    q = bf(torch.randn(Lq, heads * hd, generator=gen)).to(cuda)
+    k = bf(torch.randn(Lk, heads * hd, generator=gen)).to(cuda)
+    v = bf(torch.randn(Lk, heads * hd, generator=gen)).to(cuda)
+    rows = Lq // g_
+    outs = [torch.zeros(rows, heads * hd, device=cuda, dtype=torch.bfloat16) for _ in range(g_)]
+    ops.attention_scatter(q, k, v, heads, hd, Lq, Lk, 0.1, [t.data_ptr() for t in outs], rows, heads * hd)
+    want = torch_attn(q, k, v, heads, hd, 0.1)
+    assert rel(torch.cat(outs).float(), want) < 5e-3
+
+
 @pytest.mark.parametrize("Lq,Lk,heads,hd", [(9, 9, 2, 16), (9, 10, 2, 16), (1170, 37, 4, 128), (100, 70, 3, 64),
                                             (5, 3, 4, 8), (33, 100, 2, 32)])
 def test_attention_small(ops, cuda, Lq, Lk, heads, hd):
