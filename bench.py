@@ -336,7 +336,7 @@ def main():
 
     # ---------------- instrumented chunk: per-kernel durations for the roofline
     ops.PROFILER = []
-    ops.PROFILE_DETAIL = True if args.detail else None
+    ops.PROFILE_DETAIL = True               # per-shape kinds ("gemm:qkv_rope:MxNxK", "conv:...")
     ds.z.copy_(z_all[nsteps - 1])
     ds.d.buf["cond_in"].copy_(cond_all[nsteps - 1])
     ds._device_chunk()                      # eager: every launch bracketed by events
@@ -345,39 +345,50 @@ def main():
     torch.cuda.synchronize()
     prof = ops.PROFILER
     ops.PROFILER = None
-    agg = {}
-    if args.detail:
-        det = {}
-        for kind, a, b, fl, nb in prof:
-            g = det.setdefault(kind, [0.0, 0.0, 0])
-            g[0] += a.elapsed_time(b)
+    ops.PROFILE_DETAIL = None
+    det, agg = {}, {}
+    for kind, a, b, fl, nb in prof:
+        t = a.elapsed_time(b)
+        for key, table in ((kind, det), (kind.split(":")[0], agg)):
+            g = table.setdefault(key, [0.0, 0.0, 0.0, 0])
+            g[0] += t
             g[1] += fl
-            g[2] += 1
+            g[2] += nb
+            g[3] += 1
+    if args.detail:
         for k, v in sorted(det.items(), key=lambda kv: -kv[1][0]):
             sys.stderr.write("%-50s %9.3f ms %5d launches %8.1f TFLOP/s\n" % (
-                k, v[0], v[2], v[1] / (v[0] * 1e-3) / 1e12 if v[1] else 0.0))
-    for kind, a, b, fl, nb in prof:
-        kind = "gemm" if kind.startswith("gemm") else kind
-        t = a.elapsed_time(b)
-        g = agg.setdefault(kind, [0.0, 0.0, 0.0, 0])
-        g[0] += t
-        g[1] += fl
-        g[2] += nb
-        g[3] += 1
+                k, v[0], v[3], v[1] / (v[0] * 1e-3) / 1e12 if v[1] else 0.0))
     pk, pk_src = peaks()
+    peak = pk["bf16_tflops_sustained"]
+    # dominant kernel: the tcgen05 GEMM at its largest launch (QKV projection + RoPE epilogue)
+    qkv = [(k, v) for k, v in det.items() if k.startswith("gemm:qkv_rope")]
+    qk, qv = max(qkv, key=lambda kv: kv[1][1]) if qkv else max(
+        ((k, v) for k, v in det.items() if k.startswith("gemm")), key=lambda kv: kv[1][1])
+    q_ms = qv[0] / qv[3]
+    q_flops = qv[1] / qv[3]
+    ach = q_flops / (q_ms * 1e-3) / 1e12
+    traffic, traffic_src = None, None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))["kernels"]["gemm"]
+        if qk.split(":")[-1] in tr["shape"].replace(" ", ""):
+            traffic, traffic_src = tr["dram_bytes"], "profiles/ncu_traffic.json (%s, ncu --set full)" % tr["shape"]
+    except Exception:  # noqa: BLE001
+        pass
     gem = agg.get("gemm", [1e-9, 0, 0, 1])
     conv = agg.get("conv", [1e-9, 0, 0, 1])
-    ach = gem[1] / (gem[0] * 1e-3) / 1e12
-    peak = pk["bf16_tflops_sustained"]
     breakdown = {k: {"ms": v[0], "launches": v[3], "tflops": (v[1] / (v[0] * 1e-3) / 1e12) if v[1] else None,
                      "gbs": (v[2] / (v[0] * 1e-3) / 1e9)} for k, v in agg.items()}
-    dit_flops = sum(v[1] for v in agg.values())
-    roofline = {"bound": "tensor", "kernel": "ftb gemm_tc_kernel (all DiT GEMMs of one chunk)",
+    dit_flops = sum(v[1] for k, v in agg.items() if k != "conv")
+    roofline = {"bound": "tensor", "kernel": "ftb gemm_tc_pair_kernel, %s" % qk,
                 "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "peak_source": pk_src + " bf16_tflops_sustained", "traffic": None,
-                "flops_per_launch": gem[1] / gem[3], "avg_launch_ms": gem[0] / gem[3],
-                "chunk_flops": dit_flops, "chunk_tflops_achieved": dit_flops / (ms * 1e-3) / 1e12,
-                "chunk_frac": dit_flops / (ms * 1e-3) / 1e12 / peak, "per_kind": breakdown,
+                "peak_source": pk_src + " bf16_tflops_sustained (kernel timed inside the chunk)",
+                "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": qv[2] / qv[3],
+                "flops_per_launch": q_flops, "avg_launch_ms": q_ms, "launches_per_chunk": qv[3],
+                "all_gemms_tflops": gem[1] / (gem[0] * 1e-3) / 1e12,
+                "dit_chunk_flops": dit_flops, "dit_tflops_achieved": dit_flops / (comp["denoise"] * 1e-3) / 1e12,
+                "dit_frac": dit_flops / (comp["denoise"] * 1e-3) / 1e12 / peak, "per_kind": breakdown,
                 "vae_conv_tflops": conv[1] / (conv[0] * 1e-3) / 1e12 if conv[1] else None}
 
     cpu = None

@@ -5,7 +5,8 @@
 // Activations are channel-last bf16 [T][H][W][C]; the causal time padding is
 // the 2 cached frames the caller keeps in front of the current chunk's frames
 // (t0 = 0 with a KT=3 kernel reads frames t, t+1, t+2 of the padded buffer).
-// An M tile is 128 consecutive output pixels of one (t, y) row; for every tap
+// An M tile is 128 consecutive output pixels of one (t, y) row (tiles ordered x, t, y so
+// consecutive tiles re-read the same input rows from L2); for every tap
 // the producer issues one 4D TMA box {BK channels, 128 px, 1 row, 1 frame} at
 // the shifted coordinates — spatial zero padding is the TMA out-of-bounds
 // fill. The B operand is W^T [Cout][taps*Cin] (K-major). Same warp-specialised
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(256, 1)
         const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
         const int xt = m_blk % p.num_xt;
         const int ty = m_blk / p.num_xt;
-        const int y = ty % p.H, t = ty / p.H;
+        const int t = ty % p.T, y = ty / p.T;  // frames fastest: the 3 input frames a tap row reads stay in L2
         for (int kb = 0; kb < num_kb; ++kb) {
           const int tap = kb / p.kb_per_tap, cb = kb - tap * p.kb_per_tap;
           const int dx = tap % p.KW, dy = (tap / p.KW) % p.KH, dt = tap / (p.KW * p.KH);
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(256, 1)
       const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
       const int xt = m_blk % p.num_xt;
       const int ty = m_blk / p.num_xt;
-      const int y = ty % p.H, t = ty / p.H;
+      const int t = ty % p.T, y = ty / p.T;  // frames fastest: the 3 input frames a tap row reads stay in L2
       const int x = xt * 128 + q * 32 + lane;
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(256, 1)
         const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
         const int xt = m_blk % p.num_xt;
         const int ty = m_blk / p.num_xt;
-        const int y = ty % p.H, t = ty / p.H;
+        const int t = ty % p.T, y = ty / p.T;  // frames fastest: the 3 input frames a tap row reads stay in L2
         for (int kb = 0; kb < num_kb; ++kb) {
           const int r = kb / p.kb_per_tap, cb = kb - r * p.kb_per_tap;
           const int dy = r % 3, dt = r / 3;
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(256, 1)
       const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
       const int xt = m_blk % p.num_xt;
       const int ty = m_blk / p.num_xt;
-      const int y = ty % p.H, t = ty / p.H;
+      const int t = ty % p.T, y = ty / p.T;  // frames fastest: the 3 input frames a tap row reads stay in L2
       const int x = xt * 128 + q * 32 + lane;
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);

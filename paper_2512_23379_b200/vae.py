@@ -308,7 +308,8 @@ class DeviceVAEDecoder:
 
     def _rms(self, x, npix, C, g, y, stream):
         fn = "ftb_rmsnorm_silu_f32" if x.dtype == torch.float32 else "ftb_rmsnorm_silu_bf16"
-        A.call(fn, A.ptr(x), npix, C, A.ptr(g), 1e-12, 1, A.ptr(y), A.stream_ptr(stream))
+        with ops._Prof("vae_norm", 0.0, float(npix) * C * (x.element_size() + 2), stream):
+            A.call(fn, A.ptr(x), npix, C, A.ptr(g), 1e-12, 1, A.ptr(y), A.stream_ptr(stream))
 
     # ------------------------------------------------------------ decode
     def decode_device_tensor(self, z, stream=None):
@@ -366,7 +367,8 @@ class DeviceVAEDecoder:
                 l += 1
             elif op == "resample":
                 up = self.upbuf[:npx * 4 * cin]
-                A.call("ftb_upsample2x_f32_bf16", A.ptr(x), T_, H_, W_, cin, A.ptr(up), A.stream_ptr(s))
+                with ops._Prof("vae_upsample", 0.0, float(npx) * cin * (4 + 4 * 2), s):
+                    A.call("ftb_upsample2x_f32_bf16", A.ptr(x), T_, H_, W_, cin, A.ptr(up), A.stream_ptr(s))
                 nxt = lv[l + 1]
                 self._conv(up, T_, 2 * H_, 2 * W_, cin, self.W[name], nxt["x"], cout, 0, F32, None, 0, T_, s)
                 l += 1
