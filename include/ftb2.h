@@ -97,6 +97,9 @@ int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_
 
 /* Kernel variant for ftb_gemm_bf16: 0 auto (CTA pair when M,N >= 256), 1 single CTA, 2 CTA pair. */
 int ftb_set_gemm_variant(int32_t variant);
+/* CTA-pair raster group (256-row m-blocks sharing one B sweep in L2): 0 auto (A panels of
+ * the group ~40 MB, at least 8), else the given count (benchmarks). */
+int ftb_set_gemm_group(int32_t group_m);
 
 /* ---------------------------------------------------------------- norms */
 /* y = ((x - mean) * rstd) * (gamma?gamma:1) * (scale?1+scale[g]:1) + (beta?beta:0) + (shift?shift[g]:0)

@@ -40,6 +40,7 @@ _SIGS = {
     "ftb_set_gemm_variant": ([i32], i32),
     "ftb_set_conv_variant": ([i32], i32),
     "ftb_set_norm_variant": ([i32], i32),
+    "ftb_set_gemm_group": ([i32], i32),
     "ftb_gemm_bf16": ([vp, i64, i32, i64, vp, i64, i32, i32, i32, C.POINTER(Epilogue), vp], i32),
     "ftb_norm_modulate": ([vp, i64, i32, i32, vp, vp, vp, vp, i64, i32, i64, f32, vp, i64, vp, vp, vp], i32),
     "ftb_attention": ([vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),

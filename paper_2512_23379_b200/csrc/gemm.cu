@@ -36,6 +36,7 @@ struct GemmParams {
   int heads, head_dim, hpr;
   ftb_rope3d rope;
   int has_rope;
+  int group_m;                  // pair kernel: m-blocks per raster group (B reuse in L2)
   int n_peers;                  // > 0: QKV_ROPE / F32 stores go to peer-mapped buffers
   void* peers[FTB_MAX_PEERS];
 };
@@ -345,13 +346,12 @@ constexpr int PAIR_A_BYTES = 128 * GEMM_BK * 2;
 constexpr int PAIR_B_BYTES = 128 * GEMM_BK * 2;
 constexpr int PAIR_STAGE_BYTES = PAIR_A_BYTES + PAIR_B_BYTES;
 constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 1024 + 256;
-constexpr int PAIR_GROUP_M = 8;
 
-__device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int& m_blk, int& n_blk) {
-  const int group = PAIR_GROUP_M * num_n;
+__device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int group_m, int& m_blk, int& n_blk) {
+  const int group = group_m * num_n;
   const int g = tile / group;
-  const int first_m = g * PAIR_GROUP_M;
-  const int gm = min(num_m - first_m, PAIR_GROUP_M);
+  const int first_m = g * group_m;
+  const int gm = min(num_m - first_m, group_m);
   const int local = tile - g * group;
   m_blk = first_m + local % gm;
   n_blk = local / gm;
@@ -401,7 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
         int m_blk, n_blk;
-        pair_raster(tile, num_m, num_n, m_blk, n_blk);
+        pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * PAIR_STAGE_BYTES;
@@ -452,7 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     int it = 0;
     for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
       int m_blk, n_blk;
-      pair_raster(tile, num_m, num_n, m_blk, n_blk);
+      pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
@@ -521,6 +521,12 @@ extern "C" int ftb_set_gemm_variant(int32_t v) {
   return FTB_OK;
 }
 
+static int g_gemm_group = 0;
+extern "C" int ftb_set_gemm_group(int32_t g) {
+  g_gemm_group = g;
+  return FTB_OK;
+}
+
 extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_stride, const void* B,
                              int64_t ldb, int32_t M, int32_t N, int32_t K, const ftb_epilogue* epi, void* stream) {
   if (!A || !B || !epi || !epi->out) return set_error(FTB_EINVAL, "gemm: null pointer");
@@ -569,6 +575,14 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
 
   const int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   const bool pair = g_gemm_variant == 2 || (g_gemm_variant == 0 && M >= 256 && N >= 256);
+  {
+    // raster group: enough 256-row m-blocks that their A panels (~40 MB) stay in L2 while
+    // the B panel streams past once per group
+    const long long panel = 256LL * K * 2;
+    int gmax = (int)(40LL * 1024 * 1024 / (panel > 0 ? panel : 1));
+    if (g_gemm_group > 0) gmax = g_gemm_group;
+    p.group_m = gmax < 8 ? 8 : gmax;
+  }
   CUtensorMap ta, tb;
   // A: 3D {kc, M, chunks}
   {

@@ -17,8 +17,11 @@ def main(which):
         a = torch.randn(L, m, device=dev).to(torch.bfloat16)
         w = (torch.randn(3 * m, m, device=dev) / 70).to(torch.bfloat16)
         out = torch.empty(L, 3 * m, device=dev, dtype=torch.bfloat16)
-        for _ in range(3):
-            ops.gemm(a, w, out, "bf16")
+        groups = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0]
+        for g in groups:
+            A.call("ftb_set_gemm_group", g)
+            for _ in range(3):
+                ops.gemm(a, w, out, "bf16")
     if which in ("oproj", "ffn2", "all"):
         K = m if which != "ffn2" else 13824
         a = torch.randn(L, K, device=dev).to(torch.bfloat16)
