@@ -195,6 +195,22 @@ int ftb_conv3d_halo_bf16(const void* in, const void* halo_top, const void* halo_
                          int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW,
                          int32_t t0, const float* bias, const void* resid, int64_t resid_ld, void* out,
                          int64_t out_ld, int32_t T_out, int32_t mode, void* stream);
+/* Fused RMS norm (+SiLU) of the conv output over all Cout channels (Wan RMS_norm:
+ * y = x / max(||x||_2, 1e-12) * sqrt(C) * gamma), written as bf16 channel-last
+ * [T_out][H][W][ld] — the next conv's input — in the same epilogue. */
+typedef struct ftb_conv_norm {
+  const float* gamma;  /* [Cout] */
+  void* out;           /* bf16 */
+  int64_t ld;
+  int32_t silu;
+  int32_t write_main;  /* 0: skip the main output (`out` of the conv may be NULL, no residual) */
+} ftb_conv_norm;
+/* As ftb_conv3d_halo_bf16 (halos may both be NULL) with the fused norm; store mode 0 and
+ * Cout <= 192 (one N tile holds every channel of a pixel). */
+int ftb_conv3d_norm_bf16(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in, int32_t H,
+                         int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW,
+                         int32_t t0, const float* bias, const void* resid, int64_t resid_ld, void* out,
+                         int64_t out_ld, int32_t T_out, int32_t mode, const ftb_conv_norm* norm, void* stream);
 /* Conv kernel variant: 0 auto (one haloed TMA box per (dt,dy) feeds the 3 dx taps when KH=KW=3 and
  * Cin % 64 == 0), 1 per-tap boxes. */
 int ftb_set_conv_variant(int32_t variant);

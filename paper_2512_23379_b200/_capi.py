@@ -33,6 +33,10 @@ class Epilogue(C.Structure):
                 ("n_peers", i32), ("peer_out", vp * MAX_PEERS)]
 
 
+class ConvNorm(C.Structure):
+    _fields_ = [("gamma", vp), ("out", vp), ("ld", i64), ("silu", i32), ("write_main", i32)]
+
+
 _SIGS = {
     "ftb_version": ([], i32),
     "ftb_last_error": ([], C.c_char_p),
@@ -68,6 +72,8 @@ _SIGS = {
                         i32),
     "ftb_conv3d_halo_bf16": ([vp, vp, vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, vp, vp, i64, vp, i64, i32,
                               i32, vp], i32),
+    "ftb_conv3d_norm_bf16": ([vp, vp, vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, vp, vp, i64, vp, i64, i32,
+                              i32, C.POINTER(ConvNorm), vp], i32),
     "ftb_rmsnorm_silu_bf16": ([vp, i64, i32, vp, f32, i32, vp, vp], i32),
     "ftb_upsample2x_bf16": ([vp, i32, i32, i32, i32, vp, vp], i32),
     "ftb_nchw_to_nhwc_bf16": ([vp, i32, i32, i32, i32, vp, i32, vp], i32),

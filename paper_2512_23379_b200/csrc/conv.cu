@@ -31,6 +31,13 @@ struct ConvParams {
   int out_f32;    // mode bit 4: fp32 output
   int resid_f32;  // mode bit 5: fp32 residual
   int halo;       // dx-reuse kernel: rows -1 / H come from the halo maps (spatial split)
+  // fused RMS norm (+SiLU) of the output pixel over all Cout channels (one N tile):
+  // norm_out[pix*norm_ld + c] = bf16(silu(v_c * sqrt(Cout) / max(||v||, eps) * gamma_c))
+  const float* norm_gamma;
+  __nv_bfloat16* norm_out;
+  long long norm_ld;
+  int norm_silu;
+  int write_main;  // 0: only the normalised output (the raw conv output has no other consumer)
 };
 
 template <int BN, int BK>
@@ -44,6 +51,63 @@ struct ConvCfg {
   static constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 4u;  // SW128 / SW64
   static constexpr uint32_t SBO = 8 * BK * 2;               // 8 rows of one swizzle atom
 };
+
+// acc -> + bias (+ residual) for the norm path (mode 0, full 32-column chunks)
+__device__ __forceinline__ void conv_epilogue_values(const ConvParams& p, int t, int y, int x, int gc0,
+                                                     float (&v)[32]) {
+  if (p.bias) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] += __ldg(p.bias + gc0 + j);
+  }
+  if (p.resid) {
+    const long long pix = ((long long)t * p.H + y) * p.W + x;
+    if (p.resid_f32) {
+      const float4* r = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.resid) + pix * p.resid_ld + gc0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 f = r[q];
+        v[4 * q] += f.x;
+        v[4 * q + 1] += f.y;
+        v[4 * q + 2] += f.z;
+        v[4 * q + 3] += f.w;
+      }
+    } else {
+      const __nv_bfloat16* r = p.resid + pix * p.resid_ld + gc0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w = *reinterpret_cast<const uint4*>(r + 8 * q);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 f = __bfloat1622float2(h2[e]);
+          v[8 * q + 2 * e] += f.x;
+          v[8 * q + 2 * e + 1] += f.y;
+        }
+      }
+    }
+  }
+}
+
+// main store of a finished chunk (mode 0)
+__device__ __forceinline__ void conv_store(const ConvParams& p, int t, int y, int x, int gc0, const float (&v)[32]) {
+  const long long pix = ((long long)t * p.H + y) * p.W + x;
+  if (p.out_f32) {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + pix * p.out_ld + gc0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return;
+  }
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + pix * p.out_ld + gc0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 w;
+    w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+    w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+    w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+    w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+    reinterpret_cast<uint4*>(o)[q] = w;
+  }
+}
 
 __device__ __forceinline__ void conv_epilogue(const ConvParams& p, int t, int y, int x, int gc0, float (&v)[32]) {
   const bool full = gc0 + 32 <= p.Cout;
@@ -109,6 +173,81 @@ __device__ __forceinline__ void conv_epilogue(const ConvParams& p, int t, int y,
     w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
     w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
     reinterpret_cast<uint4*>(o)[q] = w;
+  }
+}
+
+// Epilogue of one pixel (thread) over the tile's BN columns: bias / residual / main store
+// per 32-column chunk, then (norm_out) a second pass that normalises the pixel's channels.
+template <int BN>
+__device__ __forceinline__ void conv_epilogue_tile(const ConvParams& p, uint32_t tmem_row, int n_blk, int t, int y,
+                                                   int x) {
+  const bool live = x < p.W;
+  float ss = 0.f;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    const int gc0 = n_blk * BN + c0;
+    if (gc0 >= p.Cout) break;
+    uint32_t r[32];
+    tmem_ld32(tmem_row + c0, r);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    if (!live) continue;
+    if (p.norm_out) {
+      conv_epilogue_values(p, t, y, x, gc0, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) ss += v[j] * v[j];
+      if (p.write_main) conv_store(p, t, y, x, gc0, v);
+    } else {
+      conv_epilogue(p, t, y, x, gc0, v);
+    }
+  }
+  if (!p.norm_out) return;
+  // every lane stays in the loop: tcgen05.ld is warp-collective (dead pixels only skip memory)
+  const float inv = sqrtf((float)p.Cout) / fmaxf(sqrtf(ss), 1e-12f);
+  const long long pix = ((long long)t * p.H + y) * p.W + x;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    if (c0 >= p.Cout) break;
+    float v[32];
+    if (p.write_main && p.out_f32) {  // the values this thread just stored (same-thread read-back)
+      if (!live) continue;
+      const float4* o = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.out) + pix * p.out_ld + c0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = o[q];
+        v[4 * q] = f.x;
+        v[4 * q + 1] = f.y;
+        v[4 * q + 2] = f.z;
+        v[4 * q + 3] = f.w;
+      }
+    } else {  // recompute from the accumulator (no residual on this path)
+      uint32_t r[32];
+      tmem_ld32(tmem_row + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      if (!live) continue;
+      conv_epilogue_values(p, t, y, x, c0, v);
+    }
+    __nv_bfloat16* o = p.norm_out + pix * p.norm_ld + c0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float a[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float f = v[8 * q + e] * inv * __ldg(p.norm_gamma + c0 + 8 * q + e);
+        if (p.norm_silu) f = f * fmaf(0.5f, tanh_fast(0.5f * f), 0.5f);   // silu = f * sigmoid(f), one MUFU
+        a[e] = f;
+      }
+      uint4 w;
+      w.x = pack_bf16(a[0], a[1]);
+      w.y = pack_bf16(a[2], a[3]);
+      w.z = pack_bf16(a[4], a[5]);
+      w.w = pack_bf16(a[6], a[7]);
+      reinterpret_cast<uint4*>(o)[q] = w;
+    }
   }
 }
 
@@ -216,18 +355,7 @@ __global__ void __launch_bounds__(256, 1)
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const int gc0 = n_blk * BN + c0;
-        if (gc0 >= p.Cout) break;
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (x < p.W) conv_epilogue(p, t, y, x, gc0, v);
-      }
+      conv_epilogue_tile<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, n_blk, t, y, x);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -409,18 +537,7 @@ __global__ void __launch_bounds__(256, 1)
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const int gc0 = n_blk * BN + c0;
-        if (gc0 >= p.Cout) break;
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (x < p.W) conv_epilogue(p, t, y, x, gc0, v);
-      }
+      conv_epilogue_tile<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, n_blk, t, y, x);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -488,9 +605,16 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
                        int32_t W, int32_t Cin, const void* w_t,
                                int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0, const float* bias,
                                const void* resid, int64_t resid_ld, void* out, int64_t out_ld, int32_t T_out,
-                               int32_t mode, void* stream) {
-  if (!in || !w_t || !out || T_out <= 0 || H <= 0 || W <= 0 || Cin <= 0 || Cout <= 0)
+                               int32_t mode, void* stream, const ftb_conv_norm* nrm = nullptr) {
+  const bool norm = nrm && nrm->out;
+  if (!in || !w_t || (!out && !(norm && !nrm->write_main)) || T_out <= 0 || H <= 0 || W <= 0 || Cin <= 0 || Cout <= 0)
     return set_error(FTB_EINVAL, "conv3d: bad arguments");
+  if (norm) {
+    if ((mode & 15) != 0) return set_error(FTB_EINVAL, "conv3d: fused norm needs store mode 0");
+    if (Cout > 192 || Cout % 32 || !nrm->gamma || (nrm->ld % 8))
+      return set_error(FTB_EINVAL, "conv3d: fused norm needs Cout <= 192 (one N tile), Cout % 32 == 0, gamma");
+    if (!nrm->write_main && resid) return set_error(FTB_EINVAL, "conv3d: fused norm without main output takes no residual");
+  }
   const int out_f32 = (mode >> 4) & 1, resid_f32 = (mode >> 5) & 1;
   mode &= 15;
   if (Cin % 8) return set_error(FTB_EINVAL, "conv3d: Cin must be a multiple of 8");
@@ -500,7 +624,7 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
   if (mode != 2 && (Cout % 32)) return set_error(FTB_EINVAL, "conv3d: Cout must be a multiple of 32");
   if (mode == 1 && (Cout % 64)) return set_error(FTB_EINVAL, "conv3d: time-split needs Cout multiple of 64");
   if (resid && (resid_ld % 8)) return set_error(FTB_EINVAL, "conv3d: resid_ld alignment");
-  if (mode != 2 && (out_ld % 8)) return set_error(FTB_EINVAL, "conv3d: out_ld alignment");
+  if (mode != 2 && out && (out_ld % 8)) return set_error(FTB_EINVAL, "conv3d: out_ld alignment");
   ConvParams p{};
   p.T = T_out;
   p.H = H;
@@ -524,6 +648,13 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
   p.out_f32 = out_f32;
   p.resid_f32 = resid_f32;
   p.halo = halo_top != nullptr;
+  if (norm) {
+    p.norm_gamma = nrm->gamma;
+    p.norm_out = reinterpret_cast<__nv_bfloat16*>(nrm->out);
+    p.norm_ld = nrm->ld;
+    p.norm_silu = nrm->silu;
+    p.write_main = nrm->write_main;
+  }
   if (p.halo && (!halo_bot || KH != 3 || KW != 3 || Cin % 32))
     return set_error(FTB_EINVAL, "conv3d: halo rows need a 3x3 kernel, both halo buffers and Cin % 32 == 0");
   if ((g_conv_variant != 1 || p.halo) && KH == 3 && KW == 3 && Cin % 32 == 0) {
@@ -563,6 +694,17 @@ extern "C" int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t 
                                int32_t mode, void* stream) {
   return conv3d_impl(in, nullptr, nullptr, T_in, H, W, Cin, w_t, Cout, KT, KH, KW, t0, bias, resid, resid_ld, out,
                      out_ld, T_out, mode, stream);
+}
+
+extern "C" int ftb_conv3d_norm_bf16(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in,
+                                    int32_t H, int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT,
+                                    int32_t KH, int32_t KW, int32_t t0, const float* bias, const void* resid,
+                                    int64_t resid_ld, void* out, int64_t out_ld, int32_t T_out, int32_t mode,
+                                    const ftb_conv_norm* norm, void* stream) {
+  if (!norm || !norm->out) return set_error(FTB_EINVAL, "conv3d_norm: norm output required");
+  if ((halo_top == nullptr) != (halo_bot == nullptr)) return set_error(FTB_EINVAL, "conv3d_norm: both halos or none");
+  return conv3d_impl(in, halo_top, halo_bot, T_in, H, W, Cin, w_t, Cout, KT, KH, KW, t0, bias, resid, resid_ld, out,
+                     out_ld, T_out, mode, stream, norm);
 }
 
 extern "C" int ftb_conv3d_halo_bf16(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in,

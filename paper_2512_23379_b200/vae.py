@@ -22,6 +22,7 @@ Device layout: channel-last bf16 activations, convs are tcgen05 implicit GEMMs
 the host is PyTorch's Conv3d (Cout, Cin, kt, kh, kw) float64.
 """
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -155,12 +156,20 @@ class DeviceVAEDecoder:
     (zeros at the global edges), so the split decode equals the unsplit one.
     The causal caches of the halo rows travel with the caches of the slabs."""
 
-    def __init__(self, cfg: VAEConfig, device, params=None, seed=0, rgb8=True, comm=None):
+    def __init__(self, cfg: VAEConfig, device, params=None, seed=0, rgb8=True, comm=None, fuse_norm=True):
         from .dist import LocalComm
         self.cfg = cfg
         self.dev = torch.device(device)
         self.prog, shapes = vae_program(cfg)
         self.rgb8 = rgb8
+        # RMS norm + SiLU of a conv output folded into that conv's epilogue whenever one N tile
+        # holds every channel of a pixel (Cout <= 192): the normalised bf16 tensor is written
+        # straight into the next conv's input buffer (no fp32 re-read, no separate pass)
+        # True / "all": conv1 -> norm2 and conv2 / resample -> next norm1 / head norm;
+        # "conv1": only conv1 -> norm2 (no fp32 main output); False / "none": separate passes
+        self.fuse_norm = {True: "all", False: "none"}.get(fuse_norm, fuse_norm)
+        if self.fuse_norm not in ("all", "conv1", "none"):
+            raise ConfigError("fuse_norm must be True/False/'all'/'conv1'/'none'")
         self.frames_per_latent = cfg.time_factor
         self.comm = comm if comm is not None else LocalComm()
         self.W, self.G = {}, {}
@@ -217,7 +226,8 @@ class DeviceVAEDecoder:
                              sc=torch.empty(px * C, dtype=f32, device=self.dev),     # 1x1 shortcut
                              h=torch.empty(px * C, dtype=bf, device=self.dev),       # conv1 output
                              xb=torch.empty(px * C, dtype=bf, device=self.dev),      # bf16 view of x
-                             work=torch.empty(Tp * gg["H"] * gg["W"] * C, dtype=bf, device=self.dev))
+                             work=torch.empty(Tp * gg["H"] * gg["W"] * C, dtype=bf, device=self.dev),
+                             work2=torch.empty(Tp * gg["H"] * gg["W"] * C, dtype=bf, device=self.dev))
             if self.split:  # halo rows (+2 cache frames) and contiguous edge-row send buffers
                 row = gg["W"] * max(C, gg.get("HC", 0))
                 levels[l].update(top=torch.zeros(Tp * row, dtype=bf, device=self.dev),
@@ -261,17 +271,19 @@ class DeviceVAEDecoder:
         self.comm.neighbor_exchange(first, last, top, bot)
         return L["top"][:(off + T_in) * row], L["bot"][:(off + T_in) * row]
 
-    def _causal(self, cw, L, Cin, producer, out, out_ld, mode, resid=None, resid_ld=0, stream=None, halo=True):
+    def _causal(self, cw, L, Cin, producer, out, out_ld, mode, resid=None, resid_ld=0, stream=None, halo=True,
+                work_key="work", norm=None):
         """KT=3 causal conv on level L: cache -> work[0:2], producer fills
-        work[2:], (split: halo exchange of the new frames), conv, last 2 input
-        frames -> cache (for the next chunk)."""
+        work[2:] (None: a previous conv's fused-norm epilogue already did), (split: halo
+        exchange of the new frames), conv, last 2 input frames -> cache (next chunk)."""
         T, H, W = L["T"], L["H"], L["W"]
         fr = H * W * Cin
-        work = L["work"][:(T + 2) * fr]
+        work = L[work_key][:(T + 2) * fr]
         if cw.cache is None:
             cw.cache = torch.zeros(2 * fr, dtype=torch.bfloat16, device=self.dev)
         work[:2 * fr].copy_(cw.cache)
-        producer(work[2 * fr:])
+        if producer is not None:
+            producer(work[2 * fr:])
         halos = None
         if self.split and halo and cw.k[1] == 3:
             row = W * Cin
@@ -285,11 +297,11 @@ class DeviceVAEDecoder:
             cw.hcache[1].copy_(bv[T * row:(T + 2) * row])
             halos = (tv, bv)
         self._conv(work, T + 2, H, W, Cin, cw, out, out_ld, 0, mode, resid, resid_ld, T, stream, halos,
-                   allow_halo=halo)
+                   allow_halo=halo, norm=norm)
         cw.cache.copy_(work[T * fr:(T + 2) * fr])
 
     def _conv(self, inp, T_in, H, W, Cin, cw, out, out_ld, t0, mode, resid, resid_ld, T_out, stream, halos=None,
-              allow_halo=True):
+              allow_halo=True, norm=None):
         kt, kh, kw = cw.k
         cout = cw.cout if (mode & 15) != 0 or cw.cout % 32 == 0 else cw.wt.shape[0]
         if self.split and allow_halo and kh == 3 and halos is None:   # non-causal 3x3 (resample)
@@ -298,7 +310,14 @@ class DeviceVAEDecoder:
         tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%d %d->%d k%d%d%d" % (
             T_out, H, W, Cin, cw.cout, kt, kh, kw)
         with ops._Prof(tag, 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
-            if halos is not None:
+            if norm is not None:
+                gamma, nout, write_main = norm
+                nrm = A.ConvNorm(A.ptr(gamma), A.ptr(nout), cout, 1, int(write_main))
+                A.call("ftb_conv3d_norm_bf16", A.ptr(inp), A.ptr(halos[0]) if halos else None,
+                       A.ptr(halos[1]) if halos else None, T_in, H, W, Cin, A.ptr(cw.wt), cout, kt, kh, kw, t0,
+                       A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld, T_out, mode, C.byref(nrm),
+                       A.stream_ptr(stream))
+            elif halos is not None:
                 A.call("ftb_conv3d_halo_bf16", A.ptr(inp), A.ptr(halos[0]), A.ptr(halos[1]), T_in, H, W, Cin,
                        A.ptr(cw.wt), cout, kt, kh, kw, t0, A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld,
                        T_out, mode, A.stream_ptr(stream))
@@ -340,7 +359,10 @@ class DeviceVAEDecoder:
             C0 = cw.cout
             lv[0]["x"][:T * self.rows * w * C0].view(T, self.rows, w, C0).copy_(
                 self.full0.view(T, h, w, C0)[:, self.row0:self.row0 + self.rows])
-        for op, name, cin, cout in self.prog[1:]:
+        pre = None   # (level, work key) whose frames [2:] already hold the next conv's normalised input
+        prog = self.prog
+        for i in range(1, len(prog)):
+            op, name, cin, cout = prog[i]
             L = lv[l]
             T_, H_, W_ = L["T"], L["H"], L["W"]
             npx = T_ * H_ * W_
@@ -354,33 +376,62 @@ class DeviceVAEDecoder:
                     resid = L["sc"]
                 else:
                     resid = x
-                self._causal(c1, L, cin, lambda dst: self._rms(x[:npx * cin], npx, cin, self.G[name + ".norm1"],
-                                                               dst, s), L["h"], cout, 0, stream=s)
-                # conv2 updates the fp32 residual stream in place (one thread reads and writes each pixel)
-                self._causal(c2, L, cout, lambda dst: self._rms(L["h"][:npx * cout], npx, cout,
-                                                                self.G[name + ".norm2"], dst, s),
-                             x, cout, F32 | R32, resid=resid, resid_ld=cout, stream=s)
+                prod1 = None if pre == (l, "work") else (
+                    lambda dst: self._rms(x[:npx * cin], npx, cin, self.G[name + ".norm1"], dst, s))
+                fr2 = H_ * W_ * cout
+                if self.fuse_norm != "none" and cout <= 192:   # conv1 -> norm2 + SiLU -> conv2's input
+                    self._causal(c1, L, cin, prod1, None, cout, 0, stream=s,
+                                 norm=(self.G[name + ".norm2"], L["work2"][2 * fr2:], False))
+                    prod2 = None
+                else:
+                    self._causal(c1, L, cin, prod1, L["h"], cout, 0, stream=s)
+                    prod2 = (lambda dst: self._rms(L["h"][:npx * cout], npx, cout, self.G[name + ".norm2"], dst, s))
+                # conv2 updates the fp32 residual stream in place (one thread reads and writes each pixel) and,
+                # fused, writes the next block's (or the head's) normalised input
+                nxt = self._next_norm(i, cout)
+                self._causal(c2, L, cout, prod2, x, cout, F32 | R32, resid=resid, resid_ld=cout, stream=s,
+                             work_key="work2",
+                             norm=(nxt, L["work"][2 * fr2:], True) if nxt is not None else None)
+                pre = (l, "work") if nxt is not None else None
             elif op == "time":
                 nxt = lv[l + 1]
                 self._causal(self.W[name], L, cin, lambda dst: ops.cast_f32_bf16(x[:npx * cin], dst, stream=s),
                              nxt["x"], cin, 1 | F32, stream=s)
                 l += 1
+                pre = None
             elif op == "resample":
                 up = self.upbuf[:npx * 4 * cin]
                 with ops._Prof("vae_upsample", 0.0, float(npx) * cin * (4 + 4 * 2), s):
                     A.call("ftb_upsample2x_f32_bf16", A.ptr(x), T_, H_, W_, cin, A.ptr(up), A.stream_ptr(s))
                 nxt = lv[l + 1]
-                self._conv(up, T_, 2 * H_, 2 * W_, cin, self.W[name], nxt["x"], cout, 0, F32, None, 0, T_, s)
+                g = self._next_norm(i, cout)
+                fr_n = nxt["H"] * nxt["W"] * cout
+                self._conv(up, T_, 2 * H_, 2 * W_, cin, self.W[name], nxt["x"], cout, 0, F32, None, 0, T_, s,
+                           norm=(g, nxt["work"][2 * fr_n:], True) if g is not None else None)
                 l += 1
+                pre = (l, "work") if g is not None else None
             elif op == "head":
                 hw_ = self.W["head.conv"]
-                prod = lambda dst: self._rms(x[:npx * cin], npx, cin, self.G["head.norm"], dst, s)  # noqa: E731
+                prod = None if pre == (l, "work") else (
+                    lambda dst: self._rms(x[:npx * cin], npx, cin, self.G["head.norm"], dst, s))
                 if self.rgb8:
                     self._causal(hw_, L, cin, prod, self.out_rgb, 3, 2, stream=s)
                     return self.out_rgb[:npx * 3].view(T_, H_, W_, 3)
                 self._causal(hw_, L, cin, prod, self.out_f, 32, F32, stream=s)
                 return self.out_f[:npx * 32].view(T_, H_, W_, 32)
         raise ConfigError("VAE program has no head")
+
+    def _next_norm(self, i, c):
+        """Gain of the RMS norm that consumes op i's c-channel output (next resblock's norm1
+        or the head norm) when it can ride op i's conv epilogue, else None."""
+        if self.fuse_norm != "all" or c > 192 or i + 1 >= len(self.prog):
+            return None
+        op, name, cin, _ = self.prog[i + 1]
+        if op == "res" and cin == c:
+            return self.G[name + ".norm1"]
+        if op == "head" and cin == c:
+            return self.G["head.norm"]
+        return None
 
     def _full_work(self, T, h, w, zc):
         buf = getattr(self, "_fw", None)
