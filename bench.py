@@ -211,10 +211,25 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FTB_EMULATE_RANKS=1 (tests only): every rank on GPU 0, gloo process group, peer transport
+    # with host barriers — exercises the N>1 plumbing on a one-GPU box; the timing is meaningless
+    emulate = world > 1 and os.environ.get("FTB_EMULATE_RANKS") == "1"
+    if emulate:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if emulate:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cpu" if emulate else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     cfg = getattr(C, MODELS[args.model])
     Hpx, Wpx = C.BUCKETS[args.bucket]
@@ -227,7 +242,10 @@ def main():
     torch.cuda.set_stream(stream)
     w = DeviceWeights.synthetic(cfg, dev, seed=200)
     comm, comm_note = None, "none"
-    if world > 1:
+    if emulate:
+        from paper_2512_23379_b200.dist import IpcPeerComm
+        comm, comm_note = IpcPeerComm(dev, barrier_mode="host"), "peer (emulated ranks on one GPU, host barrier)"
+    elif world > 1:
         # Ulysses sequence parallel: one chunk sharded over all ranks (strong scaling)
         comm, comm_note = pick_comm(args, w, Lc, Lm, lat_hw, stream, dev)
     d = DeviceDenoiser(w, Lc, Lm, lat_hw, stream=stream, comm=comm)
@@ -291,12 +309,8 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     launches = _capi.LAUNCHES[0] - launches0 + (ds.graph_launches * args.steps if ds.graph is not None else 0)
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     fps = frames_per_chunk * 1000.0 / ms   # one stream sharded over all ranks (strong scaling)
     comp = {"denoise": float(np.mean([a.elapsed_time(b) for a, b, _ in marks])),
             "decode": float(np.mean([b.elapsed_time(c) for _, b, c in marks])),
@@ -325,11 +339,7 @@ def main():
             e2e_chunk(c)
         ee1.record(stream)
         torch.cuda.synchronize()
-        ems = ee0.elapsed_time(ee1) / args.steps
-        if world > 1:
-            te = torch.tensor([ems], device=dev)
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            ems = float(te.item())
+        ems = max_over_ranks(ee0.elapsed_time(ee1) / args.steps)
         h2d = ds.noise_host[0].numel() * 4 + d.buf["cond_in"].numel() * 2
         e2e = {"value": frames_per_chunk * 1000.0 / ems, "unit": "FPS", "ms_per_step": ems,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0]}

@@ -1,0 +1,47 @@
+"""bench.py contract on the B200: the JSON line of a 1-GPU run (tiny model, fast) and the
+N>1 plumbing (torchrun, Ulysses shards, peer transport, max-over-ranks timing) with two
+ranks emulated on the one GPU of the box (FTB_EMULATE_RANKS=1: gloo + host barriers)."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+        "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"}
+
+
+def _line(out):
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert lines, out[-2000:]
+    return json.loads(lines[-1])
+
+
+def test_bench_single_gpu_line(cuda):
+    r = subprocess.run([sys.executable, "bench.py", "--model", "tiny", "--steps", "3", "--warmup", "3"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _line(r.stdout)
+    assert KEYS <= set(d), KEYS - set(d)
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["frac"] > 0 and d["roofline"]["unit"] == "TFLOP/s"
+
+
+def test_bench_two_emulated_ranks(cuda):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, FTB_EMULATE_RANKS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--model", "1.3b", "--steps", "2",
+           "--warmup", "1", "--no-decode", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, (r.stdout[-1500:], r.stderr[-3000:])
+    d = _line(r.stdout)
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "ulysses_sp2"
+    assert d["config"]["comm"].startswith("peer") and d["value"] > 0 and d["e2e"]["value"] > 0
