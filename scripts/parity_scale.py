@@ -1,0 +1,64 @@
+"""Parity at the 14B width and the full streaming token count ("re-measure at
+L = 10 530", where bf16 error may grow toward the budget): the device DiT vs the fp64
+oracle (oracle/wan_oracle.py) with shared bf16-rounded weights, m=5120 / 40 heads /
+ff=13824, 416x720 latent grid (L = 9 x 1170 tokens), `layers` transformer layers.
+usage: python scripts/parity_scale.py [layers] [--sampler]   (writes gpurun_out/parity_scale.json)"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import wan_oracle as WO  # noqa: E402
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def main():
+    from paper_2512_23379_b200.config import NetConfig, SamplerPlan
+    from paper_2512_23379_b200.diffusion import composite_from_state, few_step_sample
+    from paper_2512_23379_b200.net import Denoiser, ParamStore
+    from paper_2512_23379_b200.seeding import STREAM_NOISE, rng_for
+    layers = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 2
+    sampler = "--sampler" in sys.argv
+    m, heads, ff, D, A, adim, Lc, Lm, H, W = 5120, 40, 13824, 16, 4, 768, 9, 2, 52, 90
+    cfg = NetConfig(m, layers, heads, ff, D, mode="wan", patch=(1, 2, 2), audio_dim=adim, audio_tokens=A)
+    t0 = time.time()
+    store = ParamStore.init(cfg, 200)
+    r = np.random.default_rng(1)
+    x = dict(motion=r.standard_normal((Lm, D, H, W)), z=r.standard_normal((Lc - Lm, D, H, W)),
+             ref=r.standard_normal((D, H, W)), audio=r.standard_normal((Lc, A, adim)))
+    ocfg = dict(model_dim=m, layers=layers, heads=heads, latent_dim=D, patch=(1, 2, 2), audio_tokens=A,
+                audio_dim=adim)
+    P = store.bf16_rounded().params
+    res = {"model_dim": m, "heads": heads, "ff": ff, "layers": layers, "tokens": Lc * (H // 2) * (W // 2),
+           "init_s": time.time() - t0}
+    comp = composite_from_state(x["motion"], x["z"], x["ref"], x["audio"], 0.75)
+    net = Denoiser(cfg)
+    out = net.forward(store, comp)
+    t1 = time.time()
+    want = WO.denoise(P, ocfg, x["motion"], x["z"], x["ref"], x["audio"], comp.frame_t)
+    res["oracle_forward_s"] = time.time() - t1
+    res["forward_rel_l2"] = rel(out, want)
+    res["forward_rel_l2_targets"] = rel(out[Lm:], want[Lm:])
+    print(json.dumps(res), flush=True)
+    if sampler:
+        chunk = few_step_sample(net.as_denoise_fn(store), SamplerPlan(), x["motion"], x["ref"], x["audio"],
+                                rng_for(11, STREAM_NOISE, 0))
+        z0 = rng_for(11, STREAM_NOISE, 0).standard_normal(x["z"].shape)
+        t2 = time.time()
+        ref = WO.sample_chunk(P, ocfg, (1.0, 0.75, 0.5, 0.25), x["motion"], x["ref"], x["audio"], z0)
+        res["oracle_sampler_s"] = time.time() - t2
+        res["chunk_rel_l2"] = rel(chunk.targets, ref[Lm:])
+    os.makedirs("gpurun_out", exist_ok=True)
+    json.dump(res, open("gpurun_out/parity_scale_%d.json" % layers, "w"), indent=1)
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
