@@ -301,7 +301,9 @@ struct Fmha2Cfg {
 
 // TMEM map (512 columns): S_t fp32 at [128t, 128t+128) with P_t (bf16 pairs) aliased onto
 // its first 64 columns; O_t fp32 at [256 + 128t, 256 + 128t + HD).
-template <int HD>
+// SPLITP: the softmax hands P over in two 64-key halves so PV of the first half overlaps
+// the exponentials of the second (shortens the S -> softmax -> PV -> S chain).
+template <int HD, bool SPLITP>
 __global__ void __launch_bounds__(384, 1)
     fmha2_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
@@ -316,7 +318,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* s_full = bars + 1 + 2 * NS; // [2] per tile
   uint64_t* p_full = s_full + 2;        // [2]
   uint64_t* o_done = s_full + 4;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 6);
+  uint64_t* p_lo = s_full + 6;          // [2] first P half written (SPLITP)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int warp = warp_id(), lane = lane_id();
   const int qblk = blockIdx.x, head = blockIdx.y;
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4);
+      mbar_init(&p_lo[t], 4);
       mbar_init(&o_done[t], 1);
     }
     fence_barrier_init();
@@ -380,13 +384,23 @@ __global__ void __launch_bounds__(384, 1)
         }
         mma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int j) {  // O_t += P_t (TMEM) . V_j (smem, MN-major)
+      auto issue_pv_part = [&](int t, int j, int k0, int k1) {  // O_t += P_t (TMEM) . V_j (smem, MN-major)
         const uint32_t sv = smem_u32(smem + C::OFF_KV + ((2 * j + 1) % NS) * C::TILE);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int kk = k0; kk < k1; ++kk) {
           const uint64_t bd = sdesc_sw128(sv + kk * 16 * 128, C::BOX, 1024);
           mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
+      };
+      auto issue_pv = [&](int t, int j) {
+        if (SPLITP) {
+          mbar_wait(&p_lo[t], j & 1);
+          tc_fence_after();
+          issue_pv_part(t, j, 0, 4);
+        }
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        issue_pv_part(t, j, SPLITP ? 4 : 0, 8);
         mma_commit(&o_done[t]);
       };
       mbar_wait(q_full, 0);
@@ -399,15 +413,11 @@ __global__ void __launch_bounds__(384, 1)
       // holds P_t(j), so it is issued after PV_t(j) (tcgen05 ops of a CTA execute in order).
       for (int j = 0; j < n_kv; ++j) {
         wait_item(2 * j + 1);  // V_j
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
         issue_pv(0, j);
         if (j + 1 < n_kv) {
           wait_item(2 * j + 2);  // K_{j+1}
           issue_s(0, j + 1);
         }
-        mbar_wait(&p_full[1], j & 1);
-        tc_fence_after();
         issue_pv(1, j);
         mma_commit(&kv_empty[(2 * j + 1) % NS]);  // V_j consumed
         if (j + 1 < n_kv) {
@@ -462,46 +472,69 @@ __global__ void __launch_bounds__(384, 1)
       const float2 nm2 = make_float2(-m_use, -m_use);
       float2 rs2 = make_float2(0.f, 0.f);
       // P_t (bf16 pairs) overwrites the first 64 columns of S_t: pack in place in sr[0..63]
+      auto exp_chunks = [&](int ch0, int ch1) {
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
-        float2 e[4];
+        for (int ch = ch0; ch < ch1; ++ch) {
+          float2 e[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          float2 x = ffma2(make_float2(__uint_as_float(sr[ch * 8 + 2 * u]), __uint_as_float(sr[ch * 8 + 2 * u + 1])),
-                           sc2, nm2);
-          if (u == 3) {  // one pair in four on the FMA pipe (offloads MUFU)
-            x.x = fmaxf(x.x, -126.f);
-            x.y = fmaxf(x.y, -126.f);
-            e[u] = ex2_poly2(x);
-          } else {
-            e[u] = make_float2(ex2(x.x), ex2(x.y));
+          for (int u = 0; u < 4; ++u) {
+            float2 x = ffma2(make_float2(__uint_as_float(sr[ch * 8 + 2 * u]), __uint_as_float(sr[ch * 8 + 2 * u + 1])),
+                             sc2, nm2);
+            if (u == 3) {  // one pair in four on the FMA pipe (offloads MUFU)
+              x.x = fmaxf(x.x, -126.f);
+              x.y = fmaxf(x.y, -126.f);
+              e[u] = ex2_poly2(x);
+            } else {
+              e[u] = make_float2(ex2(x.x), ex2(x.y));
+            }
+            rs2 = fadd2(rs2, e[u]);
           }
-          rs2 = fadd2(rs2, e[u]);
-        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) sr[ch * 4 + u] = pack_bf16(e[u].x, e[u].y);
-      }
-      const float rs = rs2.x + rs2.y;
-      if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) done: O_t stable
-      tc_fence_after();
-      tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
-      tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-      if (__any_sync(0xffffffffu, rescale)) {
-        const float f = rescale ? ex2(m_ref - m_use) : 1.f;
-        l *= f;
+          for (int u = 0; u < 4; ++u) sr[ch * 4 + u] = pack_bf16(e[u].x, e[u].y);
+        }
+      };
+      auto rescale_o = [&]() {
+        if (__any_sync(0xffffffffu, rescale)) {
+          const float f = rescale ? ex2(m_ref - m_use) : 1.f;
+          l *= f;
 #pragma unroll 1
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-          uint32_t o[32];
-          tmem_ld32(tO + c0, o);
-          tmem_ld_wait();
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t o[32];
+            tmem_ld32(tO + c0, o);
+            tmem_ld_wait();
 #pragma unroll
-          for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * f);
-          tmem_st32(tO + c0, o);
+            for (int u = 0; u < 32; ++u) o[u] = __float_as_uint(__uint_as_float(o[u]) * f);
+            tmem_st32(tO + c0, o);
+          }
         }
+      };
+      if (SPLITP) {
+        exp_chunks(0, 8);
+        if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) done: O_t stable, P region free
+        tc_fence_after();
+        rescale_o();
+        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_lo[t]);
+        exp_chunks(8, 16);
+        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        tmem_st_wait();
+        l += rs2.x + rs2.y;
+        m_ref = m_use;
+      } else {
+        exp_chunks(0, 16);
+        const float rs = rs2.x + rs2.y;
+        if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) done: O_t stable
+        tc_fence_after();
+        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
+        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+        rescale_o();
+        tmem_st_wait();
+        l += rs;
+        m_ref = m_use;
       }
-      tmem_st_wait();
-      l += rs;
-      m_ref = m_use;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
@@ -956,11 +989,14 @@ static int launch_fmha(const AttnParams& p, cudaStream_t s) {
 }
 
 template <int HD>
-static int launch_fmha2(const AttnParams& p, cudaStream_t s) {
+static int launch_fmha2(const AttnParams& p, cudaStream_t s, bool splitp = false) {
   using C = Fmha2Cfg<HD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fmha2_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(fmha2_tc_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fmha2_tc_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "fmha2 smem attribute");
     configured = true;
   }
@@ -976,7 +1012,10 @@ static int launch_fmha2(const AttnParams& p, cudaStream_t s) {
   if ((rc = mk(&tk, p.k, p.ldk, p.Lk))) return rc;
   if ((rc = mk(&tv, p.v, p.ldv, p.Lk))) return rc;
   dim3 grid((p.Lq + 255) / 256, p.heads);
-  fmha2_tc_kernel<HD><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
+  if (splitp)
+    fmha2_tc_kernel<HD, true><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
+  else
+    fmha2_tc_kernel<HD, false><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
   return check_launch("fmha2_tc_kernel");
 }
 
@@ -1002,11 +1041,15 @@ static int attention_run(int32_t impl, AttnParams& p, void* stream) {
     if (head_dim == 64) return launch_xattn<64>(p, s);
     return set_error(FTB_EINVAL, "xattn: head_dim must be 64 or 128");
   }
+  if (impl == 5) {  // A/B reference: P handed over in one piece
+    if (head_dim == 128) return launch_fmha2<128>(p, s, false);
+    if (head_dim == 64) return launch_fmha2<64>(p, s, false);
+  }
   if (impl == 0 || impl == 2) {
     if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
-    if (impl == 0) {  // 2 Q tiles per CTA, two softmax warpgroups
-      if (head_dim == 128) return launch_fmha2<128>(p, s);
-      if (head_dim == 64) return launch_fmha2<64>(p, s);
+    if (impl == 0) {  // 2 Q tiles per CTA, two softmax warpgroups, P handed over in two halves
+      if (head_dim == 128) return launch_fmha2<128>(p, s, true);
+      if (head_dim == 64) return launch_fmha2<64>(p, s, true);
     } else {          // v1: 1 Q tile per CTA
       if (head_dim == 128) return launch_fmha<128>(p, s);
       if (head_dim == 64) return launch_fmha<64>(p, s);
