@@ -2,7 +2,7 @@
 L = 10 530", where bf16 error may grow toward the budget): the device DiT vs the fp64
 oracle (oracle/wan_oracle.py) with shared bf16-rounded weights, m=5120 / 40 heads /
 ff=13824, 416x720 latent grid (L = 9 x 1170 tokens), `layers` transformer layers.
-usage: python scripts/parity_scale.py [layers] [--sampler]   (writes gpurun_out/parity_scale.json)"""
+usage: python scripts/parity_scale.py [layers] [--sampler]   (writes gpurun_out/parity_scale_<layers>.json)"""
 import json
 import os
 import sys
@@ -35,7 +35,12 @@ def main():
              ref=r.standard_normal((D, H, W)), audio=r.standard_normal((Lc, A, adim)))
     ocfg = dict(model_dim=m, layers=layers, heads=heads, latent_dim=D, patch=(1, 2, 2), audio_tokens=A,
                 audio_dim=adim)
-    P = store.bf16_rounded().params
+    # round the weights to bf16 in place (one host copy: 40 layers of fp64 are 112 GB); the device
+    # uses exactly these values, so the comparison isolates kernel arithmetic
+    import torch
+    for k_, v_ in store.params.items():
+        v_[...] = torch.from_numpy(v_).to(torch.bfloat16).to(torch.float64).numpy()
+    P = store.params
     res = {"model_dim": m, "heads": heads, "ff": ff, "layers": layers, "tokens": Lc * (H // 2) * (W // 2),
            "init_s": time.time() - t0}
     comp = composite_from_state(x["motion"], x["z"], x["ref"], x["audio"], 0.75)
