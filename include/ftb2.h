@@ -142,6 +142,8 @@ int ftb_sym_free(void* ptr);
 int ftb_ipc_export(const void* ptr, uint8_t* handle);
 int ftb_ipc_import(const uint8_t* handle, void** ptr);
 int ftb_ipc_close(void* ptr);
+/* Stream-ordered device-to-device copy (peer-mapped destinations: VAE halo rows). */
+int ftb_copy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 /* Stream-ordered barrier over `world` ranks: flags[i] = rank i's [world] u32 flag words
  * (peer-mapped), epoch = this rank's device counter (incremented per call, so the barrier
  * is CUDA-graph capturable). Fences prior stores system-wide, signals every rank, then

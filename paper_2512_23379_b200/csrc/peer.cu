@@ -54,6 +54,13 @@ extern "C" int ftb_ipc_close(void* ptr) {
   return e == cudaSuccess ? FTB_OK : set_cuda_error(e, "ipc_close");
 }
 
+extern "C" int ftb_copy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
+  if (!dst || !src) return set_error(FTB_EINVAL, "copy_d2d: null pointer");
+  if (!bytes) return FTB_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FTB_OK : set_cuda_error(e, "copy_d2d");
+}
+
 struct BarrierParams {
   uint32_t* flags[FTB_MAX_PEERS];  // rank i's flag words [world]; flags[i][r] = last epoch rank r signalled i
   uint32_t* epoch;                 // this rank's local epoch counter (device word)

@@ -242,9 +242,37 @@ class PeerComm:
     def addrs(self, name):
         return self._addrs[name]
 
+    def halo_store(self, top_name, bot_name, offset_bytes, send_first, send_last, recv_top, recv_bot, stream=None):
+        """Spatial-split halo swap over peer memory: my first rows go to rank-1's `bot_name`
+        buffer and my last rows to rank+1's `top_name` buffer (byte offset `offset_bytes`),
+        as device-to-device copies through the peer mappings; the global edges receive zeros.
+        A barrier before the stores (the neighbours have finished the conv that read the
+        previous halos) and one after (the rows are visible)."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        nb = send_first.numel() * send_first.element_size()
+        self.barrier(s)
+        with torch.cuda.stream(s):
+            if self.rank > 0:
+                _copy_to_peer(self._addrs[bot_name][self.rank - 1] + offset_bytes, send_first, nb, s)
+            else:
+                recv_top.zero_()
+            if self.rank + 1 < self.world:
+                _copy_to_peer(self._addrs[top_name][self.rank + 1] + offset_bytes, send_last, nb, s)
+            else:
+                recv_bot.zero_()
+        self.barrier(s)
+
     # collective fallbacks used outside the fused path (VAE halo, tests)
     def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
         raise NotImplementedError
+
+
+def _copy_to_peer(dst_addr, src, nbytes, stream):
+    """cudaMemcpyAsync D2D to a peer-mapped (or, emulated, same-device) address."""
+    import ctypes as C
+    from . import _capi as A
+    A.call("ftb_copy_d2d", C.c_void_p(int(dst_addr)), C.c_void_p(src.data_ptr()), C.c_size_t(int(nbytes)),
+           A.stream_ptr(stream))
 
 
 class ThreadPeerComm(PeerComm):

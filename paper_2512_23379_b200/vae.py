@@ -230,8 +230,14 @@ class DeviceVAEDecoder:
                              work2=torch.empty(Tp * gg["H"] * gg["W"] * C, dtype=bf, device=self.dev))
             if self.split:  # halo rows (+2 cache frames) and contiguous edge-row send buffers
                 row = gg["W"] * max(C, gg.get("HC", 0))
-                levels[l].update(top=torch.zeros(Tp * row, dtype=bf, device=self.dev),
-                                 bot=torch.zeros(Tp * row, dtype=bf, device=self.dev),
+                if getattr(self.comm, "peer", False):
+                    # symmetric receive buffers: the neighbours store their edge rows here over NVLink
+                    top = self.comm.sym("vae_top%d" % l, (Tp * row,), bf, self.dev)
+                    bot = self.comm.sym("vae_bot%d" % l, (Tp * row,), bf, self.dev)
+                else:
+                    top = torch.zeros(Tp * row, dtype=bf, device=self.dev)
+                    bot = torch.zeros(Tp * row, dtype=bf, device=self.dev)
+                levels[l].update(top=top, bot=bot, lvl=l,
                                  s_first=torch.empty(Tp * row, dtype=bf, device=self.dev),
                                  s_last=torch.empty(Tp * row, dtype=bf, device=self.dev))
         self.levels = levels
@@ -268,7 +274,11 @@ class DeviceVAEDecoder:
         last.copy_(v[:, H - 1])
         top = L["top"][off * row:(off + T_in) * row].view(T_in, row)
         bot = L["bot"][off * row:(off + T_in) * row].view(T_in, row)
-        self.comm.neighbor_exchange(first, last, top, bot)
+        if getattr(self.comm, "peer", False):   # stores into the neighbours' receive buffers + barrier
+            self.comm.halo_store("vae_top%d" % L["lvl"], "vae_bot%d" % L["lvl"], off * row * 2, first, last, top,
+                                 bot)
+        else:
+            self.comm.neighbor_exchange(first, last, top, bot)
         return L["top"][:(off + T_in) * row], L["bot"][:(off + T_in) * row]
 
     def _causal(self, cw, L, Cin, producer, out, out_ld, mode, resid=None, resid_ld=0, stream=None, halo=True,

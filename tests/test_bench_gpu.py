@@ -39,7 +39,7 @@ def test_bench_two_emulated_ranks(cuda):
     env = dict(os.environ, FTB_EMULATE_RANKS="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--model", "1.3b", "--steps", "2",
-           "--warmup", "1", "--no-decode", "--no-cpu-baseline"]
+           "--warmup", "1", "--no-cpu-baseline"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, (r.stdout[-1500:], r.stderr[-3000:])
     d = _line(r.stdout)

@@ -134,11 +134,13 @@ def test_ulysses_padding_path(cuda):
 SMALL_VAE = dict(z_dim=16, base_dim=32, dim_mult=(1, 2, 4, 4), num_res_blocks=2, temporal_upsample=(True, True, False))
 
 
+@pytest.mark.parametrize("transport", ["coll", "peer"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_split_vae_matches_unsplit(cuda, world):
+def test_split_vae_matches_unsplit(cuda, world, transport):
     """Spatially split causal VAE decode (row slabs + per-conv halo exchange, two
-    chunks so the causal caches of slabs and halos are exercised) == unsplit decode."""
-    from paper_2512_23379_b200.dist import ThreadComm
+    chunks so the causal caches of slabs and halos are exercised) == unsplit decode;
+    halos through collectives or stored into the neighbours' buffers (peer transport)."""
+    from paper_2512_23379_b200.dist import ThreadComm, ThreadPeerComm
     from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig, init_vae_params
     cfg = VAEConfig(**SMALL_VAE)
     P = init_vae_params(cfg, 4)
@@ -147,7 +149,7 @@ def test_split_vae_matches_unsplit(cuda, world):
     ref_dec = DeviceVAEDecoder(cfg, cuda, params=P, rgb8=False)
     want = [ref_dec.decode_device(torch.as_tensor(z, dtype=torch.float32, device=cuda), torch.cuda.current_stream())
             for z in zs]
-    comms = ThreadComm.make(world)
+    comms = (ThreadPeerComm if transport == "peer" else ThreadComm).make(world)
     got, errs = [[None] * world for _ in zs], []
 
     def worker(rk):
