@@ -301,11 +301,11 @@ def main():
             x0 = slots[k]
         if mark:
             ev[1].record(stream)
+        if overlap:
+            dstream.wait_stream(stream)
+        if mark:
+            ev[2].record(dstream)
         if vae is not None:
-            if overlap:
-                dstream.wait_stream(stream)
-            if mark:
-                ev[2].record(dstream)
             with torch.cuda.stream(dstream):
                 vae.decode_device_tensor(x0, dstream)
             if overlap:
