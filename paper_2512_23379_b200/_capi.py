@@ -13,7 +13,7 @@ import os
 from .errors import ConfigError, DeviceError, NumericError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libftb2.so")
+LIB_PATH = os.environ.get("FTB_LIB") or os.path.join(HERE, "_lib", "libftb2.so")   # FTB_LIB: A/B builds
 
 FTB_OK, FTB_EINVAL, FTB_ECUDA, FTB_ENCCL, FTB_ENONFINITE = 0, 1, 2, 3, 4
 MAX_PEERS, IPC_HANDLE_BYTES = 8, 64

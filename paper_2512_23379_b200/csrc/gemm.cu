@@ -20,7 +20,7 @@ namespace ftb {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 256;  // 4 control warps + 4 epilogue warps (EPG=2: + a second epilogue warpgroup)
 
 struct GemmParams {
   int M, N, K;
@@ -209,8 +209,8 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
   }
 }
 
-template <int BN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+template <int BN, int EPG>
+__global__ void __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmParams p) {
   using C = GemmCfg<BN>;
@@ -304,10 +304,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue
+    // ---------------- epilogue (EPG=2: warpgroup eg drains accumulator eg, every other tile, so
+    // a tile's epilogue has two mainloops of time — short-K GEMMs are epilogue-bound otherwise)
     const int q = warp & 3;  // TMEM lane quadrant
+    const int eg = (warp - 4) >> 2;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      if (EPG == 2 && (it & 1) != eg) continue;
       const int m_blk = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
@@ -357,7 +360,8 @@ __device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int 
   n_blk = local / gm;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+template <int EPG>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -449,8 +453,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
+    const int eg = (warp - 4) >> 2;  // EPG=2: epilogue warpgroup eg drains accumulator eg
     int it = 0;
     for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+      if (EPG == 2 && (it & 1) != eg) continue;
       int m_blk, n_blk;
       pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
       const int acc = it & 1;
@@ -480,32 +486,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) tmem_dealloc_pair<512>(tmem_base);
 }
 
+template <int EPG>
 static int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_pair_kernel<EPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
     configured = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.N + 255) / 256);
   const int max_pairs = sm_count() / 2;
   const int pairs = tiles < max_pairs ? tiles : max_pairs;
-  gemm_tc_pair_kernel<<<2 * pairs, GEMM_THREADS, PAIR_SMEM, stream>>>(ta, tb, p);
+  gemm_tc_pair_kernel<EPG><<<2 * pairs, GEMM_THREADS + (EPG - 1) * 128, PAIR_SMEM, stream>>>(ta, tb, p);
   return check_launch("gemm_tc_pair_kernel");
 }
 
-template <int BN>
+template <int BN, int EPG>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
   using C = GemmCfg<BN>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm smem attribute");
     configured = true;
   }
   const int tiles = ((p.M + GEMM_BM - 1) / GEMM_BM) * ((p.N + BN - 1) / BN);
   const int grid = tiles < sm_count() ? tiles : sm_count();
-  gemm_tc_kernel<BN><<<grid, GEMM_THREADS, C::SMEM, stream>>>(ta, tb, p);
+  gemm_tc_kernel<BN, EPG><<<grid, GEMM_THREADS + (EPG - 1) * 128, C::SMEM, stream>>>(ta, tb, p);
   return check_launch("gemm_tc_kernel");
 }
 
@@ -600,8 +607,10 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
     if (rc) return rc;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (pair) return launch_gemm_pair(ta, tb, p, s);
-  if (BN == 64) return launch_gemm<64>(ta, tb, p, s);
-  if (BN == 128) return launch_gemm<128>(ta, tb, p, s);
-  return launch_gemm<256>(ta, tb, p, s);
+  // short K: the per-tile mainloop is shorter than one epilogue warpgroup's drain -> two groups
+  const bool epg2 = K <= 2048;
+  if (pair) return epg2 ? launch_gemm_pair<2>(ta, tb, p, s) : launch_gemm_pair<1>(ta, tb, p, s);
+  if (BN == 64) return epg2 ? launch_gemm<64, 2>(ta, tb, p, s) : launch_gemm<64, 1>(ta, tb, p, s);
+  if (BN == 128) return epg2 ? launch_gemm<128, 2>(ta, tb, p, s) : launch_gemm<128, 1>(ta, tb, p, s);
+  return epg2 ? launch_gemm<256, 2>(ta, tb, p, s) : launch_gemm<256, 1>(ta, tb, p, s);
 }
