@@ -35,6 +35,20 @@ struct AttnParams {
   __nv_bfloat16* o_peers[FTB_MAX_PEERS];
 };
 
+#ifdef FTB_FMHA_TIMELINE
+// debug builds only: per-block clock64 stamps of the softmax warps of one CTA
+__device__ long long g_fmha_tl[2][128][8];
+#define FTB_TL(t, j, k)                                                                          \
+  do {                                                                                           \
+    if (blockIdx.x == 10 && blockIdx.y == 0 && (warp & 3) == 0 && lane == 0 && (j) < 128)          \
+      g_fmha_tl[t][j][k] = clock64();                                                            \
+  } while (0)
+#else
+#define FTB_TL(t, j, k) \
+  do {                  \
+  } while (0)
+#endif
+
 __device__ __forceinline__ __nv_bfloat16* attn_out_row(const AttnParams& p, long long row) {
   if (p.n_peers) {
     const long long d = row / p.peer_rows;
@@ -369,7 +383,8 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // warp-converged issue loop: one elected lane issues each tcgen05 op
+      __syncwarp();
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
       auto wait_item = [&](int i) { mbar_wait(&kv_full[i % NS], (i / NS) & 1); };
@@ -379,17 +394,17 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::BOX + (kk & 3) * 32;
-          mma_bf16_ss(tmem + t * 128, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024), idesc_s,
+          mma_bf16_ss_elect(tmem + t * 128, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024), idesc_s,
                       kk > 0);
         }
-        mma_commit(&s_full[t]);
+        mma_commit_elect(&s_full[t]);
       };
       auto issue_pv_part = [&](int t, int j, int k0, int k1) {  // O_t += P_t (TMEM) . V_j (smem, MN-major)
         const uint32_t sv = smem_u32(smem + C::OFF_KV + ((2 * j + 1) % NS) * C::TILE);
 #pragma unroll
         for (int kk = k0; kk < k1; ++kk) {
           const uint64_t bd = sdesc_sw128(sv + kk * 16 * 128, C::BOX, 1024);
-          mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts_elect(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
       };
       auto issue_pv = [&](int t, int j) {
@@ -401,14 +416,14 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
         issue_pv_part(t, j, SPLITP ? 4 : 0, 8);
-        mma_commit(&o_done[t]);
+        mma_commit_elect(&o_done[t]);
       };
       mbar_wait(q_full, 0);
       wait_item(0);
       tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
-      mma_commit(&kv_empty[0]);  // K_0 consumed by both tiles
+      mma_commit_elect(&kv_empty[0]);  // K_0 consumed by both tiles
       // Per block: PV_0(j), S_0(j+1), PV_1(j), S_1(j+1). S_t(j+1) overwrites the TMEM that
       // holds P_t(j), so it is issued after PV_t(j) (tcgen05 ops of a CTA execute in order).
       for (int j = 0; j < n_kv; ++j) {
@@ -419,10 +434,10 @@ __global__ void __launch_bounds__(384, 1)
           issue_s(0, j + 1);
         }
         issue_pv(1, j);
-        mma_commit(&kv_empty[(2 * j + 1) % NS]);  // V_j consumed
+        mma_commit_elect(&kv_empty[(2 * j + 1) % NS]);  // V_j consumed
         if (j + 1 < n_kv) {
           issue_s(1, j + 1);
-          mma_commit(&kv_empty[(2 * j + 2) % NS]);  // K_{j+1} consumed by both tiles
+          mma_commit_elect(&kv_empty[(2 * j + 2) % NS]);  // K_{j+1} consumed by both tiles
         }
       }
     }
@@ -437,7 +452,9 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tO = tmem + lane_off + 256 + t * 128;
     float m_ref = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kv; ++j) {
+      FTB_TL(t, j, 0);
       mbar_wait(&s_full[t], j & 1);
+      FTB_TL(t, j, 1);
       tc_fence_after();
       uint32_t sr[128];
       tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
@@ -445,21 +462,21 @@ __global__ void __launch_bounds__(384, 1)
       tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
       tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
       tmem_ld_wait();
+      FTB_TL(t, j, 2);
       const int valid = p.Lk - j * 128;
       if (valid < 128) {
 #pragma unroll
         for (int c = 0; c < 128; ++c)
           if (c >= valid) sr[c] = __float_as_uint(-INFINITY);
       }
-      float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+      float mm[8];
 #pragma unroll
-      for (int c = 0; c < 128; c += 8) {
-        m0 = fmax3(m0, __uint_as_float(sr[c + 0]), __uint_as_float(sr[c + 1]));
-        m1 = fmax3(m1, __uint_as_float(sr[c + 2]), __uint_as_float(sr[c + 3]));
-        m2 = fmax3(m2, __uint_as_float(sr[c + 4]), __uint_as_float(sr[c + 5]));
-        m3 = fmax3(m3, __uint_as_float(sr[c + 6]), __uint_as_float(sr[c + 7]));
-      }
-      const float mx = fmax3(m0, m1, fmaxf(m2, m3)) * p.scale_log2;
+      for (int u = 0; u < 8; ++u) mm[u] = fmaxf(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
+#pragma unroll
+      for (int c = 16; c < 128; c += 16)   // 8 independent FMNMX3 chains (latency), 7 deep
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mm[u] = fmax3(mm[u], __uint_as_float(sr[c + 2 * u]), __uint_as_float(sr[c + 2 * u + 1]));
+      const float mx = fmaxf(fmax3(mm[0], mm[1], mm[2]), fmax3(mm[3], mm[4], fmax3(mm[5], mm[6], mm[7]))) * p.scale_log2;
       float m_use = m_ref;
       bool rescale = false;
       if (j == 0) {
@@ -480,7 +497,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int u = 0; u < 4; ++u) {
             float2 x = ffma2(make_float2(__uint_as_float(sr[ch * 8 + 2 * u]), __uint_as_float(sr[ch * 8 + 2 * u + 1])),
                              sc2, nm2);
-            if (u == 3) {  // one pair in four on the FMA pipe (offloads MUFU)
+            if (u == 3) {  // one pair in four on the FMA pipe (offloads MUFU; 0 or 1/2 measured slower)
               x.x = fmaxf(x.x, -126.f);
               x.y = fmaxf(x.y, -126.f);
               e[u] = ex2_poly2(x);
@@ -509,8 +526,11 @@ __global__ void __launch_bounds__(384, 1)
         }
       };
       if (SPLITP) {
+        FTB_TL(t, j, 3);
         exp_chunks(0, 8);
+        FTB_TL(t, j, 4);
         if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) done: O_t stable, P region free
+        FTB_TL(t, j, 5);
         tc_fence_after();
         rescale_o();
         tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
@@ -521,6 +541,7 @@ __global__ void __launch_bounds__(384, 1)
         exp_chunks(8, 16);
         tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
         tmem_st_wait();
+        FTB_TL(t, j, 6);
         l += rs2.x + rs2.y;
         m_ref = m_use;
       } else {
@@ -993,10 +1014,9 @@ static int launch_fmha2(const AttnParams& p, cudaStream_t s, bool splitp = false
   using C = Fmha2Cfg<HD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fmha2_tc_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(fmha2_tc_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaSuccess;
+    for (auto fn : {fmha2_tc_kernel<HD, false>, fmha2_tc_kernel<HD, true>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "fmha2 smem attribute");
     configured = true;
   }
@@ -1067,6 +1087,12 @@ static int default_impl(int Lq, int Lk, int head_dim) {
   if ((head_dim == 64 || head_dim == 128) && Lq >= 64) return Lk <= 128 ? 3 : 0;
   return 1;
 }
+
+#ifdef FTB_FMHA_TIMELINE
+extern "C" int ftb_debug_fmha_timeline(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_fmha_tl, sizeof(g_fmha_tl)) == cudaSuccess ? FTB_OK : FTB_ECUDA;
+}
+#endif
 
 extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                                   int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads,
