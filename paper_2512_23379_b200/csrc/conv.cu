@@ -315,7 +315,8 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // warp-converged MMA issue, one elected lane
+      __syncwarp();
       constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -332,15 +333,15 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            mma_bf16_ss(tmem_d, sdesc(sa + k * 32, 16, C::SBO, C::LAYOUT), sdesc(sb + k * 32, 16, C::SBO, C::LAYOUT),
+            mma_bf16_ss_elect(tmem_d, sdesc(sa + k * 32, 16, C::SBO, C::LAYOUT), sdesc(sb + k * 32, 16, C::SBO, C::LAYOUT),
                         idesc, (kb | k) ? 1u : 0u);
-          mma_commit(&empty_bar[stage]);
+          mma_commit_elect(&empty_bar[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull_bar[acc]);
+        mma_commit_elect(&tfull_bar[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -495,7 +496,8 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // warp-converged MMA issue, one elected lane
+      __syncwarp();
       constexpr uint32_t idesc = idesc_bf16(128, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -514,15 +516,15 @@ __global__ void __launch_bounds__(256, 1)
           for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_ss(tmem_d, sdesc(sa + dx * C::ROW + k * 32, 16, C::SBO, C::LAYOUT),
+              mma_bf16_ss_elect(tmem_d, sdesc(sa + dx * C::ROW + k * 32, 16, C::SBO, C::LAYOUT),
                           sdesc(sb + dx * C::B_TAP + k * 32, 16, C::SBO, C::LAYOUT), idesc, (kb | dx | k) ? 1u : 0u);
-          mma_commit(&empty_bar[stage]);
+          mma_commit_elect(&empty_bar[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull_bar[acc]);
+        mma_commit_elect(&tfull_bar[acc]);
       }
     }
   } else if (warp >= 4) {

@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    {  // ---------------- MMA issuer: warp-converged, one elected lane issues (uniform descriptors)
+      __syncwarp();
       constexpr uint32_t idesc = idesc_bf16(GEMM_BM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -292,15 +292,15 @@ __global__ void __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             uint64_t ad = sdesc_sw128(sa + k * 32, 16, 1024);
             uint64_t bd = sdesc_sw128(sb + k * 32, 16, 1024);
-            mma_bf16_ss(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
+            mma_bf16_ss_elect(tmem_d, ad, bd, idesc, (kb | k) ? 1u : 0u);
           }
-          mma_commit(&empty_bar[stage]);
+          mma_commit_elect(&empty_bar[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull_bar[acc]);
+        mma_commit_elect(&tfull_bar[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -423,7 +423,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // warp-converged issue on the leader CTA, one elected lane
+      __syncwarp();
       constexpr uint32_t idesc = idesc_bf16(256, 256, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
@@ -440,15 +441,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
           const uint32_t sb = sa + PAIR_A_BYTES;
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k)
-            mma_bf16_ss_pair(tmem_d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
+            mma_bf16_ss_pair_elect(tmem_d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
                              (kb | k) ? 1u : 0u);
-          mma_commit_pair(&empty_bar[stage], 0x3);
+          mma_commit_pair_elect(&empty_bar[stage], 0x3);
           if (++stage == PAIR_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit_pair(&tfull_bar[acc], 0x3);
+        mma_commit_pair_elect(&tfull_bar[acc], 0x3);
       }
     }
   } else if (warp >= 4) {
