@@ -134,6 +134,81 @@ __global__ void __launch_bounds__(T) norm_modulate_vec_kernel(
   }
 }
 
+// Persistent variant: each CTA walks rows blockIdx.x, +gridDim.x, ... and prefetches the next
+// row into registers while it reduces and writes the current one.
+template <int VMAX, int T>
+__global__ void __launch_bounds__(T) norm_modulate_pipe_kernel(
+    const float* __restrict__ x, long long ldx, int N, const float* __restrict__ gamma,
+    const float* __restrict__ beta, const float* __restrict__ scale, const float* __restrict__ shift,
+    long long mod_ld, int rows_per_group, long long row_offset, float eps, __nv_bfloat16* __restrict__ y,
+    long long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out, long long M) {
+  __shared__ float red[T / 32];
+  const int n4 = N >> 2;
+  float4 v[VMAX], nv[VMAX];
+  auto load = [&](long long r, float4 (&dst)[VMAX]) {
+    const float4* xr = reinterpret_cast<const float4*>(x + r * ldx);
+#pragma unroll
+    for (int i = 0; i < VMAX; ++i) {
+      const int c = threadIdx.x + i * T;
+      dst[i] = (r < M && c < n4) ? __ldcs(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  load(blockIdx.x, v);
+  for (long long row = blockIdx.x; row < M; row += gridDim.x) {
+  load(row + gridDim.x, nv);   // next row in flight during this row's reductions and stores
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VMAX; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  const float mean = block_sum<T>(s, red) / N;
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VMAX; ++i) {
+    if (threadIdx.x + i * T < n4) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+      ss += (a * a + b * b) + (c * c + d * d);
+    }
+  }
+  const float rstd = rsqrtf(block_sum<T>(ss, red) / N + eps);
+  const long long g = rows_per_group > 0 ? (row + row_offset) / rows_per_group : 0;
+  const float4* sc = scale ? reinterpret_cast<const float4*>(scale + g * mod_ld) : nullptr;
+  const float4* sh = shift ? reinterpret_cast<const float4*>(shift + g * mod_ld) : nullptr;
+  const float4* ga = reinterpret_cast<const float4*>(gamma);
+  const float4* be = reinterpret_cast<const float4*>(beta);
+  uint2* yr = reinterpret_cast<uint2*>(y + row * ldy);
+#pragma unroll
+  for (int i = 0; i < VMAX; ++i) {
+    const int c = threadIdx.x + i * T;
+    if (c < n4) {
+      float4 o = make_float4((v[i].x - mean) * rstd, (v[i].y - mean) * rstd, (v[i].z - mean) * rstd,
+                             (v[i].w - mean) * rstd);
+      if (gamma) {
+        const float4 t = __ldg(ga + c);
+        o = make_float4(o.x * t.x, o.y * t.y, o.z * t.z, o.w * t.w);
+      }
+      if (sc) {
+        const float4 t = __ldg(sc + c);
+        o = make_float4(o.x * (1.f + t.x), o.y * (1.f + t.y), o.z * (1.f + t.z), o.w * (1.f + t.w));
+      }
+      if (beta) {
+        const float4 t = __ldg(be + c);
+        o = make_float4(o.x + t.x, o.y + t.y, o.z + t.z, o.w + t.w);
+      }
+      if (sh) {
+        const float4 t = __ldg(sh + c);
+        o = make_float4(o.x + t.x, o.y + t.y, o.z + t.z, o.w + t.w);
+      }
+      yr[c] = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (mean_out) mean_out[row] = mean;
+    if (rstd_out) rstd_out[row] = rstd;
+  }
+#pragma unroll
+  for (int i = 0; i < VMAX; ++i) v[i] = nv[i];
+  }
+}
+
 // Composite assembly (diffusion.py:150-179 + stacked :133-135) fused with the
 // 2x2 spatial patchify of the wan-mode token grid. One thread per output element.
 __global__ void patchify_kernel(const float* __restrict__ motion, const float* __restrict__ z,
@@ -303,7 +378,18 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
   norm_modulate_vec_kernel<V, 256, true><<<M, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, \
                                                                    rows_per_group, row_offset, eps,              \
                                                                    (__nv_bfloat16*)y, ldy, mean_out, rstd_out)
-    if (nv <= 2)
+    if (g_norm_variant == 2 && nv <= 5) {   // persistent, next row prefetched
+      const int grid = (int)(M < 4LL * sm_count() ? M : 4LL * sm_count());
+#define FTB_NORM_PIPE(V)                                                                                          \
+  norm_modulate_pipe_kernel<V, 256><<<grid, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld,   \
+                                                                rows_per_group, row_offset, eps, (__nv_bfloat16*)y, \
+                                                                ldy, mean_out, rstd_out, (long long)M)
+      if (nv <= 2)
+        FTB_NORM_PIPE(2);
+      else
+        FTB_NORM_PIPE(5);
+#undef FTB_NORM_PIPE
+    } else if (nv <= 2)
       FTB_NORM_VEC(2);
     else if (nv <= 4)
       FTB_NORM_VEC(4);
@@ -399,4 +485,136 @@ extern "C" int ftb_add_bcast_f32(const float* a, int64_t F, int64_t n, const flo
   long long total = (long long)Lb * F * n;
   add_bcast_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(a, b, out, F, n, total);
   return check_launch("add_bcast_kernel");
+}
+
+// ---------------------------------------------------------------- folded cross-attention
+// The cross-attention keys/values (C·Wk, C·Wv of the L_c·A+1 conditioning tokens) are fixed
+// for a chunk, so the projections fold through them (exact algebra, per layer and chunk):
+//   S_h = (U·Wq_h)·K_h^T·s = U·(s·Wq_h·K_h^T)        At[(h,j)][k] = s·Σ_d K[j][h,d]·Wq^T[(h,d)][k]
+//   out = Σ_h P_h·(V_h·Wo_h) = P·Bt^T                  Bt[n][(h,j)] = Σ_d Wo^T[n][(h,d)]·V[j][h,d]
+// turning the two m×m projections per token into two m×(H·J) GEMMs (J = roundup(n_cond, 8)).
+namespace ftb {
+
+template <int JMAX>
+__global__ void __launch_bounds__(256) xattn_fold_at_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv,
+                                                            int n_cond, int hd, int J, const __nv_bfloat16* __restrict__ wqT,
+                                                            long long ldw, int m, float scale,
+                                                            __nv_bfloat16* __restrict__ at) {
+  extern __shared__ float ksh[];  // [n_cond][hd]
+  const int h = blockIdx.y;
+  for (int i = threadIdx.x; i < n_cond * hd; i += blockDim.x) {
+    const int j = i / hd, d = i - j * hd;
+    ksh[i] = __bfloat162float(kv[(long long)j * ldkv + h * hd + d]);
+  }
+  __syncthreads();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  float acc[JMAX];
+#pragma unroll
+  for (int j = 0; j < JMAX; ++j) acc[j] = 0.f;
+  for (int d = 0; d < hd; ++d) {
+    const float w = __bfloat162float(wqT[(long long)(h * hd + d) * ldw + k]);   // coalesced over k
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j)
+      if (j < n_cond) acc[j] = fmaf(ksh[j * hd + d], w, acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < JMAX; ++j)
+    if (j < J) at[(long long)(h * J + j) * m + k] = __float2bfloat16_rn(j < n_cond ? acc[j] * scale : 0.f);
+}
+
+// Bt[n][(h,j)]: a block stages Wo^T rows n0..n0+63 of head h (64 x hd) and V_h in smem.
+template <int JMAX>
+__global__ void __launch_bounds__(256) xattn_fold_bt_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv,
+                                                            int n_cond, int hd, int J, const __nv_bfloat16* __restrict__ woT,
+                                                            long long ldw, int m, int heads,
+                                                            __nv_bfloat16* __restrict__ bt) {
+  extern __shared__ float sm[];
+  float* vsh = sm;                       // [n_cond][hd]
+  float* wsh = sm + n_cond * hd;         // [64][hd + 1]
+  const int h = blockIdx.y, n0 = blockIdx.x * 64;
+  const int voff = heads * hd;           // V follows K in the kv rows
+  for (int i = threadIdx.x; i < n_cond * hd; i += blockDim.x) {
+    const int j = i / hd, d = i - j * hd;
+    vsh[i] = __bfloat162float(kv[(long long)j * ldkv + voff + h * hd + d]);
+  }
+  for (int i = threadIdx.x; i < 64 * hd; i += blockDim.x) {
+    const int r = i / hd, d = i - r * hd;
+    wsh[r * (hd + 1) + d] = (n0 + r < m) ? __bfloat162float(woT[(long long)(n0 + r) * ldw + h * hd + d]) : 0.f;
+  }
+  __syncthreads();
+  // thread -> (row r, j-group): 64 rows x 4 groups of JMAX/4 outputs
+  const int r = threadIdx.x >> 2, g = threadIdx.x & 3;
+  constexpr int JG = JMAX / 4;
+  float acc[JG];
+#pragma unroll
+  for (int q = 0; q < JG; ++q) acc[q] = 0.f;
+  for (int d = 0; d < hd; ++d) {
+    const float w = wsh[r * (hd + 1) + d];
+#pragma unroll
+    for (int q = 0; q < JG; ++q) {
+      const int j = g * JG + q;
+      if (j < n_cond) acc[q] = fmaf(w, vsh[j * hd + d], acc[q]);
+    }
+  }
+  if (n0 + r >= m) return;
+#pragma unroll
+  for (int q = 0; q < JG; ++q) {
+    const int j = g * JG + q;
+    if (j < J) bt[(long long)(n0 + r) * (heads * J) + h * J + j] = __float2bfloat16_rn(j < n_cond ? acc[q] : 0.f);
+  }
+}
+
+// P = softmax over each head's J-column segment of S (first n_cond valid, rest -> 0), bf16.
+__global__ void xattn_softmax_kernel(const float* __restrict__ s, long long lds, int rows, int heads, int J,
+                                     int n_cond, __nv_bfloat16* __restrict__ p, long long ldp) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * heads) return;
+  const long long r = idx / heads;
+  const int h = (int)(idx - r * heads);
+  const float* sr = s + r * lds + h * J;
+  float mx = -INFINITY;
+  for (int j = 0; j < n_cond; ++j) mx = fmaxf(mx, sr[j]);
+  float sum = 0.f;
+  for (int j = 0; j < n_cond; ++j) sum += __expf(sr[j] - mx);
+  const float inv = 1.f / sum;
+  __nv_bfloat16* pr = p + r * ldp + h * J;
+  for (int j = 0; j < J; ++j) pr[j] = __float2bfloat16_rn(j < n_cond ? __expf(sr[j] - mx) * inv : 0.f);
+}
+
+}  // namespace ftb
+
+extern "C" int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim,
+                              int32_t J, const void* wqT, int64_t ldwq, const void* woT, int64_t ldwo, int32_t m,
+                              float scale, void* at, void* bt, void* stream) {
+  if (!kv || !wqT || !woT || !at || !bt || n_cond <= 0 || J < n_cond || J > 48 || heads * head_dim != m ||
+      head_dim > 256)
+    return set_error(FTB_EINVAL, "xattn_fold: bad arguments (n_cond <= J <= 48, heads*head_dim == m)");
+  const size_t sm_at = (size_t)n_cond * head_dim * 4;
+  const size_t sm_bt = sm_at + (size_t)64 * (head_dim + 1) * 4;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(xattn_fold_at_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(xattn_fold_bt_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    configured = true;
+  }
+  xattn_fold_at_kernel<48><<<dim3((m + 255) / 256, heads), 256, sm_at, S(stream)>>>(
+      (const __nv_bfloat16*)kv, ldkv, n_cond, head_dim, J, (const __nv_bfloat16*)wqT, ldwq, m, scale,
+      (__nv_bfloat16*)at);
+  int rc = check_launch("xattn_fold_at_kernel");
+  if (rc) return rc;
+  xattn_fold_bt_kernel<48><<<dim3((m + 63) / 64, heads), 256, sm_bt, S(stream)>>>(
+      (const __nv_bfloat16*)kv, ldkv, n_cond, head_dim, J, (const __nv_bfloat16*)woT, ldwo, m, heads,
+      (__nv_bfloat16*)bt);
+  return check_launch("xattn_fold_bt_kernel");
+}
+
+extern "C" int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond,
+                                 void* p, int64_t ldp, void* stream) {
+  if (!s || !p || rows < 0 || heads <= 0 || n_cond <= 0 || J < n_cond) return set_error(FTB_EINVAL, "xattn_softmax");
+  if (rows == 0) return FTB_OK;
+  const long long n = (long long)rows * heads;
+  xattn_softmax_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(s, lds, rows, heads, J, n_cond,
+                                                                          (__nv_bfloat16*)p, ldp);
+  return check_launch("xattn_softmax_kernel");
 }

@@ -131,7 +131,8 @@ class DeviceDenoiser:
     communicator of world g > 1 the step runs Ulysses sequence parallel
     (dist.py): this rank owns tokens [start, start + Ls) of the padded chunk."""
 
-    def __init__(self, weights: DeviceWeights, chunk_len, motion_len, latent_hw=(1, 1), stream=None, comm=None):
+    def __init__(self, weights: DeviceWeights, chunk_len, motion_len, latent_hw=(1, 1), stream=None, comm=None,
+                 fold_cross=True):
         from .dist import LocalComm, ShardPlan
         cfg = weights.cfg
         self.cfg, self.w = cfg, weights
@@ -175,6 +176,16 @@ class DeviceDenoiser:
             "temb_act": torch.empty(F, m, dtype=bf, device=d),
             "e0": torch.empty(F, 6 * m, dtype=f32, device=d),
         }
+        # folded cross-attention (wan): the projections fold through the chunk's fixed K/V
+        # (ops.xattn_fold) -> two m x (H*J) GEMMs per layer instead of two m x m ones
+        self.fold = cfg.mode == "wan" and self.n_cond <= 48 and fold_cross
+        if self.fold:
+            self.J = round8(self.n_cond)
+            HJ = cfg.heads * self.J
+            self.buf["xat"] = torch.empty(cfg.layers, HJ, m, dtype=bf, device=d)
+            self.buf["xbt"] = torch.empty(cfg.layers, m, HJ, dtype=bf, device=d)
+            self.buf["xs"] = torch.empty(Ls, HJ, dtype=f32, device=d)
+            self.buf["xp"] = torch.empty(Ls, HJ, dtype=bf, device=d)
         self.peer = g > 1 and getattr(self.comm, "peer", False)
         if self.peer:
             # symmetric receive buffers: the producers' epilogues store into them over NVLink
@@ -280,6 +291,11 @@ class DeviceDenoiser:
         ops.cast_f32_bf16(B["cond"], B["cond_bf"], stream=self.stream)
         for i in range(cfg.layers):
             ops.gemm(B["cond_bf"], W.mats["layers.%d.cross.wkv" % i][0], B["ckv"][i], "bf16", stream=self.stream)
+            if self.fold:
+                p = "layers.%d." % i
+                ops.xattn_fold(B["ckv"][i], W.mats[p + "cross.wq"][0], W.mats[p + "cross.wo"][0], B["xat"][i],
+                               B["xbt"][i], self.n_cond, cfg.heads, cfg.head_dim, self.J, self.scale,
+                               stream=self.stream)
 
     def prepare_cond(self, signal, reference):
         """cond = [sig tokens + frame pos ; ref token] and per-layer cross K|V
@@ -347,10 +363,15 @@ class DeviceDenoiser:
             else:
                 ops.gemm(o_in.pop("a"), W.mats[p + "self.wo"][0], h, "resid_f32", stream=s, **o_in)
             ops.norm_modulate(h, u, gamma=W.vecs[p + "ln2.g"], beta=W.vecs[p + "ln2.b"], stream=s)
-            ops.gemm(u, W.mats[p + "cross.wq"][0], qkv[:, 0:m], "bf16", stream=s)
-            ckv = B["ckv"][i]
-            ops.attention(qkv[:, 0:m], ckv[:, 0:m], ckv[:, m:], ao, H_, hd, Ls, self.n_cond, self.scale, stream=s)
-            ops.gemm(ao, W.mats[p + "cross.wo"][0], h, "resid_f32", stream=s)
+            if self.fold:   # S = U.At^T (f32) -> per-head softmax -> h += P.Bt^T
+                ops.gemm(u, B["xat"][i], B["xs"], "f32", stream=s)
+                ops.xattn_softmax(B["xs"], B["xp"], H_, self.J, self.n_cond, stream=s)
+                ops.gemm(B["xp"], B["xbt"][i], h, "resid_f32", stream=s)
+            else:
+                ops.gemm(u, W.mats[p + "cross.wq"][0], qkv[:, 0:m], "bf16", stream=s)
+                ckv = B["ckv"][i]
+                ops.attention(qkv[:, 0:m], ckv[:, 0:m], ckv[:, m:], ao, H_, hd, Ls, self.n_cond, self.scale, stream=s)
+                ops.gemm(ao, W.mats[p + "cross.wo"][0], h, "resid_f32", stream=s)
             if wan:
                 ops.norm_modulate(h, u, shift=md[:, 3 * m:4 * m], scale=md[:, 4 * m:5 * m], rows_per_group=T,
                                   row_offset=s0, stream=s)

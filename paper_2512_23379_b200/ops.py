@@ -223,3 +223,23 @@ def add_bcast(a, b, out, stream=None):
     Lb = b.shape[0]
     A.call("ftb_add_bcast_f32", A.ptr(a), F, n, A.ptr(b), Lb, A.ptr(out), A.stream_ptr(stream))
     return out
+
+
+def xattn_fold(kv, wq_t, wo_t, at, bt, n_cond, heads, head_dim, J, scale, *, stream=None):
+    """Fold the cross-attention projections through the chunk's fixed K/V (elementwise.cu):
+    at [heads*J][m] = scale * K_h . Wq_h^T,  bt [m][heads*J] = Wo_h^T . V_h^T (padded j -> 0)."""
+    for t, nm in ((kv, "kv"), (wq_t, "wq_t"), (wo_t, "wo_t"), (at, "at"), (bt, "bt")):
+        _need(t, torch.bfloat16, nm)
+    m = heads * head_dim
+    with _Prof("xattn_fold", 4.0 * n_cond * m * m, 0.0, stream):
+        A.call("ftb_xattn_fold", A.ptr(kv), _ld(kv), n_cond, heads, head_dim, J, A.ptr(wq_t), _ld(wq_t), A.ptr(wo_t),
+               _ld(wo_t), m, float(scale), A.ptr(at), A.ptr(bt), A.stream_ptr(stream))
+
+
+def xattn_softmax(s, p, heads, J, n_cond, *, stream=None):
+    """Per-head softmax over J-column segments of s (f32) -> p (bf16), padded columns 0."""
+    _need(s, torch.float32, "s")
+    _need(p, torch.bfloat16, "p")
+    rows = s.shape[0]
+    with _Prof("xattn", 0.0, float(rows) * heads * J * 6, stream):
+        A.call("ftb_xattn_softmax", A.ptr(s), _ld(s), rows, heads, J, n_cond, A.ptr(p), _ld(p), A.stream_ptr(stream))

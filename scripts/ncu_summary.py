@@ -51,7 +51,7 @@ def launches():
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
-           "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
            "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "sm__cycles_active.avg",
            "gpc__cycles_elapsed.max", "smsp__cycles_active.avg.per_second"]
@@ -109,7 +109,7 @@ def main():
                       "dram_write": wr, "us": us}
         out.append("| %s | %s | %.1f | %.1f | %.1f | %.1f | %.1f | %.1f | %.1f | %.1f | %d |" % (
             d["kernel"], SHAPES[w], us, rd / 1e6, wr / 1e6, g("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
-            g("sm__throughput.avg.pct_of_peak_sustained_elapsed"), g("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+            g("sm__throughput.avg.pct_of_peak_sustained_elapsed"), g("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             g("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
             g("smsp__issue_active.avg.pct_of_peak_sustained_active"), int(g("launch__registers_per_thread"))))
     open(os.path.join(PROF, "%s_ncu_full.md" % R), "w").write("\n".join(out) + "\n")

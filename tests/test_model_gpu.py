@@ -116,3 +116,27 @@ def test_wan_sampler_matches_oracle(cuda):
                           x["audio"], z0)
     assert np.array_equal(chunk.latents[:1], x["motion"])
     assert rel(chunk.targets, ref[1:]) < BUDGET
+
+
+def test_wan_folded_cross_attention_matches_projections(cuda):
+    """Cross-attention folded through the chunk's fixed K/V (ops.xattn_fold: S = U.(s Wq K^T),
+    out = P.(V Wo)) == the explicit Q projection -> attention -> O projection path."""
+    import torch
+
+    from paper_2512_23379_b200.model import DeviceDenoiser, DeviceWeights
+    cfg, store, x, ocfg = _wan("hd128")
+    Lc, Lm = x["audio"].shape[0], x["motion"].shape[0]
+    H, W = x["ref"].shape[1:]
+    w = DeviceWeights.from_host(cfg, store.params, cuda)
+    outs = []
+    for fold in (True, False):
+        d = DeviceDenoiser(w, Lc, Lm, (H, W), fold_cross=fold)
+        assert d.fold == fold
+        d.prepare_cond(x["audio"], x["ref"])
+        fv = d.frame_vectors(np.where(np.arange(Lc) < Lm, 0.0, 0.75))
+        args = [torch.as_tensor(x[k], dtype=torch.float32, device=cuda) for k in ("motion", "z", "ref")]
+        outs.append(d.tokens_to_frames(d.step(*args, fv)).double().cpu().numpy())
+    assert rel(outs[0], outs[1]) < 5e-3
+    ref = WO.denoise(store.bf16_rounded().params, ocfg, x["motion"], x["z"], x["ref"], x["audio"],
+                     np.where(np.arange(Lc) < Lm, 0.0, 0.75))
+    assert rel(outs[0], ref) < BUDGET
