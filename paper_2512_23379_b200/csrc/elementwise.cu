@@ -495,91 +495,193 @@ extern "C" int ftb_add_bcast_f32(const float* a, int64_t F, int64_t n, const flo
 // turning the two m×m projections per token into two m×(H·J) GEMMs (J = roundup(n_cond, 8)).
 namespace ftb {
 
-template <int JMAX>
+// Block-cooperative staging of a bf16 [rows][cols] global tile (row stride ld elements) into
+// fp32 smem dst[r * dld + c]; rows in [rows, pad_rows) and columns >= cols are zero-filled.
+// 16-byte loads (cols % 8 == 0, 16-byte aligned rows), 8 in flight per thread.
+__device__ __forceinline__ void stage_bf16_rows(float* dst, int dld, const __nv_bfloat16* src, long long ld, int rows,
+                                                int cols, int pad_rows = -1) {
+  const int c8 = (cols + 7) >> 3;
+  const int total = (pad_rows > rows ? pad_rows : rows) * c8;
+  for (int base = 0; base < total; base += 8 * blockDim.x) {
+    uint4 buf[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      const int r = i / c8, c = (i - r * c8) * 8;
+      buf[u] = (i < total && r < rows && c < cols) ? __ldg(reinterpret_cast<const uint4*>(src + (long long)r * ld + c))
+                                                  : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      if (i >= total) break;
+      const int r = i / c8, c = (i - r * c8) * 8;
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&buf[u]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h2[e]);
+        dst[r * dld + c + 2 * e] = f.x;
+        dst[r * dld + c + 2 * e + 1] = f.y;
+      }
+    }
+  }
+}
+
+// As stage_bf16_rows but stores transposed: dst[c * dld + r].
+__device__ __forceinline__ void stage_bf16_rows_t(float* dst, int dld, const __nv_bfloat16* src, long long ld, int rows,
+                                                  int cols) {
+  const int c8 = (cols + 7) >> 3;
+  const int total = 128 * c8;   // always stage 128 rows (zero beyond `rows`)
+  for (int base = 0; base < total; base += 8 * blockDim.x) {
+    uint4 buf[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      const int r = i / c8, c = (i - r * c8) * 8;
+      buf[u] = (i < total && r < rows) ? __ldg(reinterpret_cast<const uint4*>(src + (long long)r * ld + c))
+                                       : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + u * blockDim.x + threadIdx.x;
+      if (i >= total) break;
+      const int r = i / c8, c = (i - r * c8) * 8;
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&buf[u]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h2[e]);
+        dst[(c + 2 * e) * dld + r] = f.x;
+        dst[(c + 2 * e + 1) * dld + r] = f.y;
+      }
+    }
+  }
+}
+
+// At[(h,j)][k]: block = (head h, 128 columns k0..k0+127). Wq^T rows (h,d) x those columns and
+// K_h are staged as fp32 in smem; thread (k, jg) accumulates 24 j's over the hd reduction.
 __global__ void __launch_bounds__(256) xattn_fold_at_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv,
                                                             int n_cond, int hd, int J, const __nv_bfloat16* __restrict__ wqT,
                                                             long long ldw, int m, float scale,
                                                             __nv_bfloat16* __restrict__ at) {
-  extern __shared__ float ksh[];  // [n_cond][hd]
-  const int h = blockIdx.y;
-  for (int i = threadIdx.x; i < n_cond * hd; i += blockDim.x) {
-    const int j = i / hd, d = i - j * hd;
-    ksh[i] = __bfloat162float(kv[(long long)j * ldkv + h * hd + d]);
-  }
+  extern __shared__ float sm[];
+  float* wsh = sm;              // [hd][128]
+  float* ksh = sm + hd * 128;   // [48][hd]
+  const int h = blockIdx.y, k0 = blockIdx.x * 128;
+  // staging: 16-byte loads, all issued before any use (the loops are latency-bound otherwise)
+  stage_bf16_rows(wsh, 128, wqT + (long long)(h * hd) * ldw + k0, ldw, hd, min(128, m - k0));
+  stage_bf16_rows(ksh, hd, kv + h * hd, ldkv, n_cond, hd, 48);
   __syncthreads();
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= m) return;
-  float acc[JMAX];
+  // register tile: 4 columns (one float4 of wsh) x 6 j's per thread; j-group warp-uniform
+  const int kq = threadIdx.x & 31, jq = threadIdx.x >> 5;
+  float acc[6][4];
 #pragma unroll
-  for (int j = 0; j < JMAX; ++j) acc[j] = 0.f;
+  for (int q = 0; q < 6; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[q][e] = 0.f;
   for (int d = 0; d < hd; ++d) {
-    const float w = __bfloat162float(wqT[(long long)(h * hd + d) * ldw + k]);   // coalesced over k
+    const float4 w = *reinterpret_cast<const float4*>(wsh + d * 128 + 4 * kq);
 #pragma unroll
-    for (int j = 0; j < JMAX; ++j)
-      if (j < n_cond) acc[j] = fmaf(ksh[j * hd + d], w, acc[j]);
+    for (int q = 0; q < 6; ++q) {
+      const float kk = ksh[(jq * 6 + q) * hd + d];
+      acc[q][0] = fmaf(kk, w.x, acc[q][0]);
+      acc[q][1] = fmaf(kk, w.y, acc[q][1]);
+      acc[q][2] = fmaf(kk, w.z, acc[q][2]);
+      acc[q][3] = fmaf(kk, w.w, acc[q][3]);
+    }
   }
 #pragma unroll
-  for (int j = 0; j < JMAX; ++j)
-    if (j < J) at[(long long)(h * J + j) * m + k] = __float2bfloat16_rn(j < n_cond ? acc[j] * scale : 0.f);
+  for (int q = 0; q < 6; ++q) {
+    const int j = jq * 6 + q;
+    if (j >= J) continue;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = k0 + 4 * kq + e;
+      if (k < m) at[(long long)(h * J + j) * m + k] = __float2bfloat16_rn(j < n_cond ? acc[q][e] * scale : 0.f);
+    }
+  }
 }
 
-// Bt[n][(h,j)]: a block stages Wo^T rows n0..n0+63 of head h (64 x hd) and V_h in smem.
-template <int JMAX>
+// Bt[n][(h,j)]: block = (head h, 128 rows n0..n0+127). Wo^T[n][(h,d)] is staged transposed
+// ([d][n], padded) so both the coalesced global read and the compute reads are conflict-free;
+// the [128][J] output tile goes out through smem as contiguous row segments.
 __global__ void __launch_bounds__(256) xattn_fold_bt_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv,
                                                             int n_cond, int hd, int J, const __nv_bfloat16* __restrict__ woT,
                                                             long long ldw, int m, int heads,
                                                             __nv_bfloat16* __restrict__ bt) {
   extern __shared__ float sm[];
-  float* vsh = sm;                       // [n_cond][hd]
-  float* wsh = sm + n_cond * hd;         // [64][hd + 1]
-  const int h = blockIdx.y, n0 = blockIdx.x * 64;
-  const int voff = heads * hd;           // V follows K in the kv rows
-  for (int i = threadIdx.x; i < n_cond * hd; i += blockDim.x) {
-    const int j = i / hd, d = i - j * hd;
-    vsh[i] = __bfloat162float(kv[(long long)j * ldkv + voff + h * hd + d]);
-  }
-  for (int i = threadIdx.x; i < 64 * hd; i += blockDim.x) {
-    const int r = i / hd, d = i - r * hd;
-    wsh[r * (hd + 1) + d] = (n0 + r < m) ? __bfloat162float(woT[(long long)(n0 + r) * ldw + h * hd + d]) : 0.f;
-  }
+  float* wsh = sm;                        // [hd][132] (rows 16-byte aligned for float4 reads)
+  float* vsh = sm + hd * 132;             // [48][hd]
+  float* osh = vsh + 48 * hd;             // [128][48]
+  const int h = blockIdx.y, n0 = blockIdx.x * 128;
+  const int voff = heads * hd;            // V follows K in the kv rows
+  stage_bf16_rows_t(wsh, 132, woT + (long long)n0 * ldw + h * hd, ldw, min(128, m - n0), hd);
+  stage_bf16_rows(vsh, hd, kv + voff + h * hd, ldkv, n_cond, hd, 48);
   __syncthreads();
-  // thread -> (row r, j-group): 64 rows x 4 groups of JMAX/4 outputs
-  const int r = threadIdx.x >> 2, g = threadIdx.x & 3;
-  constexpr int JG = JMAX / 4;
-  float acc[JG];
+  // register tile: 4 rows (float4 of the transposed wsh) x 6 j's per thread; j-group warp-uniform
+  const int nq = threadIdx.x & 31, jq = threadIdx.x >> 5;
+  float acc[6][4];
 #pragma unroll
-  for (int q = 0; q < JG; ++q) acc[q] = 0.f;
+  for (int q = 0; q < 6; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[q][e] = 0.f;
   for (int d = 0; d < hd; ++d) {
-    const float w = wsh[r * (hd + 1) + d];
+    const float4 w = *reinterpret_cast<const float4*>(wsh + d * 132 + 4 * nq);
 #pragma unroll
-    for (int q = 0; q < JG; ++q) {
-      const int j = g * JG + q;
-      if (j < n_cond) acc[q] = fmaf(w, vsh[j * hd + d], acc[q]);
+    for (int q = 0; q < 6; ++q) {
+      const float vv = vsh[(jq * 6 + q) * hd + d];
+      acc[q][0] = fmaf(w.x, vv, acc[q][0]);
+      acc[q][1] = fmaf(w.y, vv, acc[q][1]);
+      acc[q][2] = fmaf(w.z, vv, acc[q][2]);
+      acc[q][3] = fmaf(w.w, vv, acc[q][3]);
     }
   }
-  if (n0 + r >= m) return;
 #pragma unroll
-  for (int q = 0; q < JG; ++q) {
-    const int j = g * JG + q;
-    if (j < J) bt[(long long)(n0 + r) * (heads * J) + h * J + j] = __float2bfloat16_rn(j < n_cond ? acc[q] : 0.f);
+  for (int q = 0; q < 6; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) osh[(4 * nq + e) * 48 + jq * 6 + q] = acc[q][e];
+  __syncthreads();
+  for (int i = threadIdx.x; i < 128 * J; i += blockDim.x) {
+    const int rr = i / J, j = i - rr * J;
+    if (n0 + rr < m)
+      bt[(long long)(n0 + rr) * (heads * J) + h * J + j] = __float2bfloat16_rn(j < n_cond ? osh[rr * 48 + j] : 0.f);
   }
 }
 
 // P = softmax over each head's J-column segment of S (first n_cond valid, rest -> 0), bf16.
-__global__ void xattn_softmax_kernel(const float* __restrict__ s, long long lds, int rows, int heads, int J,
-                                     int n_cond, __nv_bfloat16* __restrict__ p, long long ldp) {
+// Thread = (row, head); J % 8 == 0 so the segment moves as float4 / uint4.
+template <int JC>
+__global__ void xattn_softmax_kernel(const float* __restrict__ s, long long lds, int rows, int heads, int n_cond,
+                                     __nv_bfloat16* __restrict__ p, long long ldp) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= (long long)rows * heads) return;
   const long long r = idx / heads;
   const int h = (int)(idx - r * heads);
-  const float* sr = s + r * lds + h * J;
+  const float4* sr = reinterpret_cast<const float4*>(s + r * lds + h * JC);
+  float v[JC];
+#pragma unroll
+  for (int q = 0; q < JC / 4; ++q) {
+    const float4 f = __ldcs(sr + q);
+    v[4 * q] = f.x;
+    v[4 * q + 1] = f.y;
+    v[4 * q + 2] = f.z;
+    v[4 * q + 3] = f.w;
+  }
   float mx = -INFINITY;
-  for (int j = 0; j < n_cond; ++j) mx = fmaxf(mx, sr[j]);
+#pragma unroll
+  for (int j = 0; j < JC; ++j)
+    if (j < n_cond) mx = fmaxf(mx, v[j]);
   float sum = 0.f;
-  for (int j = 0; j < n_cond; ++j) sum += __expf(sr[j] - mx);
+#pragma unroll
+  for (int j = 0; j < JC; ++j) {
+    v[j] = j < n_cond ? __expf(v[j] - mx) : 0.f;
+    sum += v[j];
+  }
   const float inv = 1.f / sum;
-  __nv_bfloat16* pr = p + r * ldp + h * J;
-  for (int j = 0; j < J; ++j) pr[j] = __float2bfloat16_rn(j < n_cond ? __expf(sr[j] - mx) * inv : 0.f);
+  uint4* pr = reinterpret_cast<uint4*>(p + r * ldp + h * JC);
+#pragma unroll
+  for (int q = 0; q < JC / 8; ++q)
+    pr[q] = make_uint4(pack_bf16(v[8 * q] * inv, v[8 * q + 1] * inv), pack_bf16(v[8 * q + 2] * inv, v[8 * q + 3] * inv),
+                       pack_bf16(v[8 * q + 4] * inv, v[8 * q + 5] * inv), pack_bf16(v[8 * q + 6] * inv, v[8 * q + 7] * inv));
 }
 
 }  // namespace ftb
@@ -588,22 +690,22 @@ extern "C" int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int3
                               int32_t J, const void* wqT, int64_t ldwq, const void* woT, int64_t ldwo, int32_t m,
                               float scale, void* at, void* bt, void* stream) {
   if (!kv || !wqT || !woT || !at || !bt || n_cond <= 0 || J < n_cond || J > 48 || heads * head_dim != m ||
-      head_dim > 256)
-    return set_error(FTB_EINVAL, "xattn_fold: bad arguments (n_cond <= J <= 48, heads*head_dim == m)");
-  const size_t sm_at = (size_t)n_cond * head_dim * 4;
-  const size_t sm_bt = sm_at + (size_t)64 * (head_dim + 1) * 4;
+      head_dim > 128 || (J % 8) || (head_dim % 8) || (m % 8) || (ldkv % 8) || (ldwq % 8) || (ldwo % 8))
+    return set_error(FTB_EINVAL, "xattn_fold: bad arguments (n_cond <= J <= 48, J, head_dim, m, ld % 8 == 0)");
+  const size_t sm_at = ((size_t)head_dim * 128 + 48 * head_dim) * 4;
+  const size_t sm_bt = ((size_t)head_dim * 132 + 48 * head_dim + 128 * 48) * 4;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(xattn_fold_at_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    cudaFuncSetAttribute(xattn_fold_bt_kernel<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(xattn_fold_at_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(xattn_fold_bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     configured = true;
   }
-  xattn_fold_at_kernel<48><<<dim3((m + 255) / 256, heads), 256, sm_at, S(stream)>>>(
+  xattn_fold_at_kernel<<<dim3((m + 127) / 128, heads), 256, sm_at, S(stream)>>>(
       (const __nv_bfloat16*)kv, ldkv, n_cond, head_dim, J, (const __nv_bfloat16*)wqT, ldwq, m, scale,
       (__nv_bfloat16*)at);
   int rc = check_launch("xattn_fold_at_kernel");
   if (rc) return rc;
-  xattn_fold_bt_kernel<48><<<dim3((m + 63) / 64, heads), 256, sm_bt, S(stream)>>>(
+  xattn_fold_bt_kernel<<<dim3((m + 127) / 128, heads), 256, sm_bt, S(stream)>>>(
       (const __nv_bfloat16*)kv, ldkv, n_cond, head_dim, J, (const __nv_bfloat16*)woT, ldwo, m, heads,
       (__nv_bfloat16*)bt);
   return check_launch("xattn_fold_bt_kernel");
@@ -611,10 +713,19 @@ extern "C" int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int3
 
 extern "C" int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond,
                                  void* p, int64_t ldp, void* stream) {
-  if (!s || !p || rows < 0 || heads <= 0 || n_cond <= 0 || J < n_cond) return set_error(FTB_EINVAL, "xattn_softmax");
+  if (!s || !p || rows < 0 || heads <= 0 || n_cond <= 0 || J < n_cond || (lds % 4) || (ldp % 8))
+    return set_error(FTB_EINVAL, "xattn_softmax: bad arguments");
   if (rows == 0) return FTB_OK;
   const long long n = (long long)rows * heads;
-  xattn_softmax_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(s, lds, rows, heads, J, n_cond,
-                                                                          (__nv_bfloat16*)p, ldp);
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  switch (J) {
+    case 8: xattn_softmax_kernel<8><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
+    case 16: xattn_softmax_kernel<16><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
+    case 24: xattn_softmax_kernel<24><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
+    case 32: xattn_softmax_kernel<32><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
+    case 40: xattn_softmax_kernel<40><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
+    case 48: xattn_softmax_kernel<48><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
+    default: return set_error(FTB_EINVAL, "xattn_softmax: J must be a multiple of 8 <= 48");
+  }
   return check_launch("xattn_softmax_kernel");
 }

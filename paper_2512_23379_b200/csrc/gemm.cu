@@ -58,6 +58,15 @@ __device__ __forceinline__ __nv_bfloat16* qkv_dest_block(const GemmParams& p, __
   return base + (long long)dest * p.M * 3 * ((long long)p.hpr * p.head_dim);
 }
 
+// Residual epilogues read the fp32 row segment they update: pull it toward L2 as the tile
+// starts so the per-chunk loads (issued only after each TMEM chunk arrives) mostly hit L2.
+__device__ __forceinline__ void prefetch_resid_row(const GemmParams& p, int gr, int gc0, int width) {
+  if (p.kind != FTB_EPI_RESID_F32 || gr >= p.M) return;
+  const float* row = reinterpret_cast<const float*>(p.out) + (long long)gr * p.ldc + gc0;
+  const int n = min(width, p.N - gc0);
+  for (int c = 0; c < n; c += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + c));
+}
+
 // Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int gc0, float (&v)[32]) {
   const int N = p.N;
@@ -316,6 +325,7 @@ __global__ void __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const int gr = m_blk * GEMM_BM + q * 32 + lane;
+      prefetch_resid_row(p, gr, n_blk * BN, BN);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         const int gc0 = n_blk * BN + c0;
@@ -464,6 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
+      prefetch_resid_row(p, gr, n_blk * 256, 256);
 #pragma unroll 1
       for (int c0 = 0; c0 < 256; c0 += 32) {
         const int gc0 = n_blk * 256 + c0;
