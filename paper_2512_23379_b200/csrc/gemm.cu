@@ -58,13 +58,55 @@ __device__ __forceinline__ __nv_bfloat16* qkv_dest_block(const GemmParams& p, __
   return base + (long long)dest * p.M * 3 * ((long long)p.hpr * p.head_dim);
 }
 
-// Residual epilogues read the fp32 row segment they update: pull it toward L2 as the tile
-// starts so the per-chunk loads (issued only after each TMEM chunk arrives) mostly hit L2.
-__device__ __forceinline__ void prefetch_resid_row(const GemmParams& p, int gr, int gc0, int width) {
-  if (p.kind != FTB_EPI_RESID_F32 || gr >= p.M) return;
-  const float* row = reinterpret_cast<const float*>(p.out) + (long long)gr * p.ldc + gc0;
-  const int n = min(width, p.N - gc0);
-  for (int c = 0; c < n; c += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + c));
+
+
+// RESID_F32 epilogue over a whole tile row (fast path: full 32-column chunks, aligned
+// rows): the residual row segment of chunk c+1 is loaded while chunk c is finished, so two
+// chunks of loads are in flight per thread (the plain path is latency-bound on these loads).
+template <int WIDTH>
+__device__ __forceinline__ bool resid_tile_pipelined(const GemmParams& p, uint32_t tmem_row, int gr, int gc_base) {
+  if (p.kind != FTB_EPI_RESID_F32 || gc_base + WIDTH > p.N || (p.ldc & 3) || (p.group_vec && (p.group_ld & 3)))
+    return false;
+  const bool live = gr < p.M;
+  const long long g = (p.rows_per_group > 0) ? (gr + p.row_offset) / p.rows_per_group : 0;
+  float* orow = reinterpret_cast<float*>(p.out) + (long long)gr * p.ldc + gc_base;
+  float4 hb[2][8];
+  auto load = [&](int c, float4 (&dst)[8]) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      dst[q] = live ? reinterpret_cast<const float4*>(orow + c * 32)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  load(0, hb[0]);
+#pragma unroll
+  for (int c = 0; c < WIDTH / 32; ++c) {
+    if (c + 1 < WIDTH / 32) load(c + 1, hb[(c + 1) & 1]);
+    uint32_t r[32];
+    tmem_ld32(tmem_row + c * 32, r);
+    tmem_ld_wait();
+    if (!live) continue;
+    const int gc0 = gc_base + c * 32;
+    const float* gate = p.group_vec ? p.group_vec + g * p.group_ld + gc0 : nullptr;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 acc = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                               __uint_as_float(r[4 * q + 3]));
+      if (p.bias) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + gc0) + q);
+        acc.x += b.x;
+        acc.y += b.y;
+        acc.z += b.z;
+        acc.w += b.w;
+      }
+      const float4 gg = gate ? __ldg(reinterpret_cast<const float4*>(gate) + q) : make_float4(1.f, 1.f, 1.f, 1.f);
+      float4 h = hb[c & 1][q];
+      h.x += gg.x * acc.x;
+      h.y += gg.y * acc.y;
+      h.z += gg.z * acc.z;
+      h.w += gg.w * acc.w;
+      reinterpret_cast<float4*>(orow + c * 32)[q] = h;
+    }
+  }
+  return true;
 }
 
 // Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
@@ -325,7 +367,7 @@ __global__ void __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const int gr = m_blk * GEMM_BM + q * 32 + lane;
-      prefetch_resid_row(p, gr, n_blk * BN, BN);
+      if (!resid_tile_pipelined<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, gr, n_blk * BN))
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         const int gc0 = n_blk * BN + c0;
@@ -474,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
-      prefetch_resid_row(p, gr, n_blk * 256, 256);
+      if (!resid_tile_pipelined<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk * 256))
 #pragma unroll 1
       for (int c0 = 0; c0 < 256; c0 += 32) {
         const int gc0 = n_blk * 256 + c0;
