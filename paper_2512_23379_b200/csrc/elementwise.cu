@@ -134,80 +134,6 @@ __global__ void __launch_bounds__(T) norm_modulate_vec_kernel(
   }
 }
 
-// Persistent variant: each CTA walks rows blockIdx.x, +gridDim.x, ... and prefetches the next
-// row into registers while it reduces and writes the current one.
-template <int VMAX, int T>
-__global__ void __launch_bounds__(T) norm_modulate_pipe_kernel(
-    const float* __restrict__ x, long long ldx, int N, const float* __restrict__ gamma,
-    const float* __restrict__ beta, const float* __restrict__ scale, const float* __restrict__ shift,
-    long long mod_ld, int rows_per_group, long long row_offset, float eps, __nv_bfloat16* __restrict__ y,
-    long long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out, long long M) {
-  __shared__ float red[T / 32];
-  const int n4 = N >> 2;
-  float4 v[VMAX], nv[VMAX];
-  auto load = [&](long long r, float4 (&dst)[VMAX]) {
-    const float4* xr = reinterpret_cast<const float4*>(x + r * ldx);
-#pragma unroll
-    for (int i = 0; i < VMAX; ++i) {
-      const int c = threadIdx.x + i * T;
-      dst[i] = (r < M && c < n4) ? __ldcs(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  load(blockIdx.x, v);
-  for (long long row = blockIdx.x; row < M; row += gridDim.x) {
-  load(row + gridDim.x, nv);   // next row in flight during this row's reductions and stores
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < VMAX; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  const float mean = block_sum<T>(s, red) / N;
-  float ss = 0.f;
-#pragma unroll
-  for (int i = 0; i < VMAX; ++i) {
-    if (threadIdx.x + i * T < n4) {
-      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
-      ss += (a * a + b * b) + (c * c + d * d);
-    }
-  }
-  const float rstd = rsqrtf(block_sum<T>(ss, red) / N + eps);
-  const long long g = rows_per_group > 0 ? (row + row_offset) / rows_per_group : 0;
-  const float4* sc = scale ? reinterpret_cast<const float4*>(scale + g * mod_ld) : nullptr;
-  const float4* sh = shift ? reinterpret_cast<const float4*>(shift + g * mod_ld) : nullptr;
-  const float4* ga = reinterpret_cast<const float4*>(gamma);
-  const float4* be = reinterpret_cast<const float4*>(beta);
-  uint2* yr = reinterpret_cast<uint2*>(y + row * ldy);
-#pragma unroll
-  for (int i = 0; i < VMAX; ++i) {
-    const int c = threadIdx.x + i * T;
-    if (c < n4) {
-      float4 o = make_float4((v[i].x - mean) * rstd, (v[i].y - mean) * rstd, (v[i].z - mean) * rstd,
-                             (v[i].w - mean) * rstd);
-      if (gamma) {
-        const float4 t = __ldg(ga + c);
-        o = make_float4(o.x * t.x, o.y * t.y, o.z * t.z, o.w * t.w);
-      }
-      if (sc) {
-        const float4 t = __ldg(sc + c);
-        o = make_float4(o.x * (1.f + t.x), o.y * (1.f + t.y), o.z * (1.f + t.z), o.w * (1.f + t.w));
-      }
-      if (beta) {
-        const float4 t = __ldg(be + c);
-        o = make_float4(o.x + t.x, o.y + t.y, o.z + t.z, o.w + t.w);
-      }
-      if (sh) {
-        const float4 t = __ldg(sh + c);
-        o = make_float4(o.x + t.x, o.y + t.y, o.z + t.z, o.w + t.w);
-      }
-      yr[c] = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
-    }
-  }
-  if (threadIdx.x == 0) {
-    if (mean_out) mean_out[row] = mean;
-    if (rstd_out) rstd_out[row] = rstd;
-  }
-#pragma unroll
-  for (int i = 0; i < VMAX; ++i) v[i] = nv[i];
-  }
-}
 
 // Composite assembly (diffusion.py:150-179 + stacked :133-135) fused with the
 // 2x2 spatial patchify of the wan-mode token grid. One thread per output element.
@@ -378,18 +304,7 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
   norm_modulate_vec_kernel<V, 256, true><<<M, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, \
                                                                    rows_per_group, row_offset, eps,              \
                                                                    (__nv_bfloat16*)y, ldy, mean_out, rstd_out)
-    if (g_norm_variant == 2 && nv <= 5) {   // persistent, next row prefetched
-      const int grid = (int)(M < 4LL * sm_count() ? M : 4LL * sm_count());
-#define FTB_NORM_PIPE(V)                                                                                          \
-  norm_modulate_pipe_kernel<V, 256><<<grid, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld,   \
-                                                                rows_per_group, row_offset, eps, (__nv_bfloat16*)y, \
-                                                                ldy, mean_out, rstd_out, (long long)M)
-      if (nv <= 2)
-        FTB_NORM_PIPE(2);
-      else
-        FTB_NORM_PIPE(5);
-#undef FTB_NORM_PIPE
-    } else if (nv <= 2)
+    if (nv <= 2)
       FTB_NORM_VEC(2);
     else if (nv <= 4)
       FTB_NORM_VEC(4);
