@@ -442,7 +442,8 @@ __device__ __forceinline__ void stage_bf16_rows(float* dst, int dld, const __nv_
   }
 }
 
-// As stage_bf16_rows but stores transposed: dst[c * dld + r].
+// As stage_bf16_rows but stores transposed: dst[c * dld + r]. Consecutive threads take
+// consecutive rows, so the transposed smem stores hit consecutive banks.
 __device__ __forceinline__ void stage_bf16_rows_t(float* dst, int dld, const __nv_bfloat16* src, long long ld, int rows,
                                                   int cols) {
   const int c8 = (cols + 7) >> 3;
@@ -452,7 +453,7 @@ __device__ __forceinline__ void stage_bf16_rows_t(float* dst, int dld, const __n
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int i = base + u * blockDim.x + threadIdx.x;
-      const int r = i / c8, c = (i - r * c8) * 8;
+      const int r = i & 127, c = (i >> 7) * 8;
       buf[u] = (i < total && r < rows) ? __ldg(reinterpret_cast<const uint4*>(src + (long long)r * ld + c))
                                        : make_uint4(0, 0, 0, 0);
     }
@@ -460,7 +461,7 @@ __device__ __forceinline__ void stage_bf16_rows_t(float* dst, int dld, const __n
     for (int u = 0; u < 8; ++u) {
       const int i = base + u * blockDim.x + threadIdx.x;
       if (i >= total) break;
-      const int r = i / c8, c = (i - r * c8) * 8;
+      const int r = i & 127, c = (i >> 7) * 8;
       const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&buf[u]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -555,10 +556,18 @@ __global__ void __launch_bounds__(256) xattn_fold_bt_kernel(const __nv_bfloat16*
 #pragma unroll
     for (int e = 0; e < 4; ++e) osh[(4 * nq + e) * 48 + jq * 6 + q] = acc[q][e];
   __syncthreads();
-  for (int i = threadIdx.x; i < 128 * J; i += blockDim.x) {
-    const int rr = i / J, j = i - rr * J;
-    if (n0 + rr < m)
-      bt[(long long)(n0 + rr) * (heads * J) + h * J + j] = __float2bfloat16_rn(j < n_cond ? osh[rr * 48 + j] : 0.f);
+  // 8 threads per row, each a 16-byte run of the row's J (<= 48) outputs
+  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x) {
+    const int rr = i >> 3, j0 = (i & 7) * 8;
+    if (j0 >= J || n0 + rr >= m) continue;
+    uint4 w;
+    uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = j0 + 2 * e;
+      wp[e] = pack_bf16(j < n_cond ? osh[rr * 48 + j] : 0.f, j + 1 < n_cond ? osh[rr * 48 + j + 1] : 0.f);
+    }
+    *reinterpret_cast<uint4*>(bt + (long long)(n0 + rr) * (heads * J) + h * J + j0) = w;
   }
 }
 
