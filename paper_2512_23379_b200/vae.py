@@ -464,5 +464,21 @@ class DeviceVAEDecoder:
         stream.synchronize()
         return host.numpy().copy() if host.dtype == torch.uint8 else host.float().numpy()
 
+    def decode_device_async(self, z, stream, slot=0):
+        """decode_device without the host wait: decode + D2H into pinned buffer `slot` are
+        enqueued on `stream`; returns (pinned host tensor, event recorded after the copy).
+        Two slots let chunk c's frames land while chunk c+1 is being enqueued."""
+        with torch.cuda.stream(stream):
+            out = self.decode_device_tensor(z.reshape(z.shape[0], self.cfg.z_dim, *z.shape[-2:]), stream)
+            key = tuple(out.shape) + (out.dtype, int(slot))
+            host = self._host.get(key)
+            if host is None:
+                host = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+                self._host[key] = host
+            host.copy_(out, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return host, ev
+
     def encode(self, frames):  # pragma: no cover - encoder is out of scope (DESIGN.md)
         raise ConfigError("the VAE encoder is out of scope; pass reference_latent to start_stream")
