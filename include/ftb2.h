@@ -151,6 +151,19 @@ int ftb_copy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 int ftb_peer_barrier(uint32_t* const* flags, uint32_t* epoch, int32_t rank, int32_t world, double timeout_s,
                      void* stream);
 
+/* Folded cross-attention (wan mode; the cond K/V are fixed for a chunk):
+ * kv [n_cond][2m] bf16 (K | V, row stride ldkv), wqT / woT the W^T [m][ld] of the cross
+ * query / output projections. Writes at [heads*J][m] = scale * K_h . Wq_h^T and
+ * bt [m][heads*J] = Wo_h^T . V_h^T (j >= n_cond zero), J % 8 == 0, n_cond <= J <= 48.
+ * Per step: S = U . at^T (f32), ftb_xattn_softmax, h += P . bt^T (residual GEMM).
+ * Replaces net.py:259-261 (cross MHA + its residual) for the wan composition. */
+int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim, int32_t J,
+                   const void* wqT, int64_t ldwq, const void* woT, int64_t ldwo, int32_t m, float scale, void* at,
+                   void* bt, void* stream);
+/* P[r][h*J + j] = softmax_j<n_cond(S[r][h*J + j]) (bf16, padded columns 0), per head segment. */
+int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond, void* p,
+                      int64_t ldp, void* stream);
+
 /* ---------------------------------------------------------------- elementwise */
 int ftb_gelu_bf16(const void* x, void* y, int64_t n, void* stream);
 int ftb_silu_f32_to_bf16(const float* x, void* y, int64_t n, void* stream);

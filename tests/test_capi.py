@@ -23,6 +23,8 @@ def test_library_exports_header():
     for n in names:
         assert hasattr(_capi.lib, n), n
         assert n in _capi.EXPORTS, n
+    # and the other way: every entry point the host binds is declared in the public header
+    assert set(_capi.EXPORTS) <= set(names), sorted(set(_capi.EXPORTS) - set(names))
     assert _capi.lib.ftb_version() == 1
 
 
