@@ -529,7 +529,9 @@ __global__ void __launch_bounds__(384, 1)
         FTB_TL(t, j, 3);
         exp_chunks(0, 8);
         FTB_TL(t, j, 4);
-        if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) done: O_t stable, P region free
+        // PV_t(j-1) is complete here: the MMA warp committed s_full_t(j) after issuing PV_t(j-1),
+        // and a commit tracks every earlier tcgen05 op of the thread, so O_t is stable and the
+        // P region free without waiting on o_done
         FTB_TL(t, j, 5);
         tc_fence_after();
         rescale_o();
