@@ -592,13 +592,221 @@ static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const Conv
   return check_launch("conv_dxr_kernel");
 }
 
+
+// CTA-pair variant of the dx-reuse conv (cta_group::2): a pair takes two consecutive 128-pixel
+// M-tiles (CTA r owns m-tile 2*pm + r) and one UMMA M=256 covers both; each CTA stages its own
+// haloed A box and HALF of the Cout rows of the three dx-tap weight tiles, so per CTA the
+// weight bytes staged and read per FLOP halve (the single-CTA kernel is bound by shared-memory
+// operand bandwidth at BN <= 192). Completions land on the leader's barriers; MMA commits are
+// multicast to both CTAs; each CTA drains its own 128 rows of the accumulator.
+template <int BN, int BK>
+struct DxrPairCfg {
+  static constexpr int ROW = BK * 2;
+  static constexpr int A_BYTES = (DXR_AROWS * ROW + 1023) / 1024 * 1024;
+  static constexpr int B_TAP = (BN / 2) * ROW;           // this CTA's half of the Cout rows
+  static constexpr int STAGE_BYTES = A_BYTES + 3 * B_TAP;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 10 ? 10 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 4u;
+  static constexpr uint32_t SBO = 8 * ROW;
+};
+
+template <int BN, int BK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    conv_dxr_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmTop, const __grid_constant__ CUtensorMap tmBot,
+                         const ConvParams p) {
+  using C = DxrPairCfg<BN, BK>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int num_m = p.T * p.H * p.num_xt;
+  const int num_pm = (num_m + 1) / 2;
+  const int num_n = (p.Cout + BN - 1) / BN;
+  const int num_tiles = num_pm * num_n;
+  const int rows = p.KT * 3;
+  const int num_kb = rows * p.kb_per_tap;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);  // 4 epilogue warps (of the group owning this accumulator) x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        const int pm = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+        const int m_blk = min(2 * pm + (int)rank, num_m - 1);   // odd tail: the spare CTA recomputes a tile
+        const int xt = m_blk % p.num_xt;
+        const int ty = m_blk / p.num_xt;
+        const int t = ty % p.T, y = ty / p.T;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int r = kb / p.kb_per_tap, cb = kb - r * p.kb_per_tap;
+          const int dy = r % 3, dt = r / 3;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (DXR_AROWS * C::ROW + 3 * C::B_TAP));
+          const int row = y + dy - 1;
+          if (p.halo && row < 0)
+            tma_load_4d_pair(sa, &tmTop, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
+          else if (p.halo && row >= p.H)
+            tma_load_4d_pair(sa, &tmBot, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
+          else
+            tma_load_4d_pair(sa, &tmA, &full_bar[stage], cb * BK, xt * 128 - 1, row, t + dt + p.t0);
+          const int tap0 = (dt * 3 + dy) * 3;
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx)
+            tma_load_2d_pair(sb + dx * C::B_TAP, &tmB, &full_bar[stage], (tap0 + dx) * p.Cin + cb * BK,
+                             n_blk * BN + (int)rank * (BN / 2));
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // warp-converged issue on the leader, one elected lane
+      __syncwarp();
+      constexpr uint32_t idesc = idesc_bf16(256, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_ss_pair_elect(tmem_d, sdesc(sa + dx * C::ROW + k * 32, 16, C::SBO, C::LAYOUT),
+                                     sdesc(sb + dx * C::B_TAP + k * 32, 16, C::SBO, C::LAYOUT), idesc,
+                                     (kb | dx | k) ? 1u : 0u);
+          mma_commit_pair_elect(&empty_bar[stage], 0x3);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair_elect(&tfull_bar[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // two epilogue warpgroups take alternate tiles (group g drains accumulator g): the fused
+    // norm / fp32 residual epilogue is longer than one tile's mainloop at Cout = 96
+    const int q = warp & 3;
+    const int eg = (warp - 4) >> 2;
+    int it = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+      if ((it & 1) != eg) continue;
+      const int pm = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
+      const int m_raw = 2 * pm + (int)rank;
+      const int m_blk = min(m_raw, num_m - 1);
+      const int xt = m_blk % p.num_xt;
+      const int ty = m_blk / p.num_xt;
+      const int t = ty % p.T, y = ty / p.T;
+      // the spare CTA of an odd tail drains its accumulator without storing (x out of range)
+      const int x = m_raw < num_m ? xt * 128 + q * 32 + lane : p.W;
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+      conv_epilogue_tile<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, n_blk, t, y, x);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+}
+
+template <int BN, int BK>
+static int launch_conv_dxr_pair(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s,
+                                const void* halo_top = nullptr, const void* halo_bot = nullptr) {
+  using C = DxrPairCfg<BN, BK>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(conv_dxr_pair_kernel<BN, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "conv_dxr_pair smem attribute");
+    configured = true;
+  }
+  CUtensorMap ta, tb;
+  {
+    uint64_t dims[4] = {(uint64_t)p.Cin, (uint64_t)p.W, (uint64_t)p.H, (uint64_t)T_in};
+    uint64_t strides[3] = {(uint64_t)p.Cin * 2, (uint64_t)p.W * p.Cin * 2, (uint64_t)p.H * p.W * p.Cin * 2};
+    uint32_t box[4] = {BK, DXR_AROWS, 1, 1};
+    int rc = make_tmap_bf16(&ta, in, 4, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  {
+    const long long ktot = (long long)p.taps * p.Cin;
+    uint64_t dims[2] = {(uint64_t)ktot, (uint64_t)p.Cout};
+    uint64_t strides[1] = {(uint64_t)ktot * 2};
+    uint32_t box[2] = {BK, BN / 2};
+    int rc = make_tmap_bf16(&tb, w_t, 2, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  CUtensorMap ttop = ta, tbot = ta;
+  if (p.halo) {
+    uint64_t dims[4] = {(uint64_t)p.Cin, (uint64_t)p.W, 1, (uint64_t)T_in};
+    uint64_t strides[3] = {(uint64_t)p.Cin * 2, (uint64_t)p.W * p.Cin * 2, (uint64_t)p.W * p.Cin * 2};
+    uint32_t box[4] = {BK, DXR_AROWS, 1, 1};
+    int rc = make_tmap_bf16(&ttop, halo_top, 4, dims, strides, box, BK * 2);
+    if (!rc) rc = make_tmap_bf16(&tbot, halo_bot, 4, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  const int num_m = p.T * p.H * p.num_xt;
+  const int tiles = ((num_m + 1) / 2) * ((p.Cout + BN - 1) / BN);
+  const int max_pairs = sm_count() / 2;
+  const int pairs = tiles < max_pairs ? tiles : max_pairs;
+  conv_dxr_pair_kernel<BN, BK><<<2 * pairs, 384, C::SMEM, s>>>(ta, tb, ttop, tbot, p);
+  return check_launch("conv_dxr_pair_kernel");
+}
+
 }  // namespace ftb
 
 using namespace ftb;
 
-static int g_conv_variant = 0;  // 0 auto (dx reuse for 3x3 taps), 1 per-tap kernel
+static int g_conv_variant = 0;  // 0 auto, 1 per-tap kernel, 2 dx reuse on CTA pairs, 3 dx reuse single-CTA
 extern "C" int ftb_set_conv_variant(int32_t v) {
-  if (v < 0 || v > 1) return set_error(FTB_EINVAL, "conv variant must be 0 (auto) or 1 (per-tap)");
+  if (v < 0 || v > 3)
+    return set_error(FTB_EINVAL, "conv variant must be 0 (auto), 1 (per-tap), 2 (dx reuse, CTA pair) or 3 (dx reuse, 1 CTA)");
   g_conv_variant = v;
   return FTB_OK;
 }
@@ -662,6 +870,18 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
   if ((g_conv_variant != 1 || p.halo) && KH == 3 && KW == 3 && Cin % 32 == 0) {
     cudaStream_t s0 = reinterpret_cast<cudaStream_t>(stream);
     const void *ht = halo_top, *hb = halo_bot;
+    // CTA pairs halve each SM's weight traffic (auto for Cout 96 / 192: the smem-bound levels)
+    const bool pair = (g_conv_variant == 2 || g_conv_variant == 0) && (Cout == 96 || Cout == 192);
+    if (pair) {
+      if (Cin % 64 == 0) {
+        p.kb_per_tap = Cin / 64;
+        return Cout == 96 ? launch_conv_dxr_pair<96, 64>(in, T_in, w_t, p, s0, ht, hb)
+                          : launch_conv_dxr_pair<192, 64>(in, T_in, w_t, p, s0, ht, hb);
+      }
+      p.kb_per_tap = Cin / 32;
+      return Cout == 96 ? launch_conv_dxr_pair<96, 32>(in, T_in, w_t, p, s0, ht, hb)
+                        : launch_conv_dxr_pair<192, 32>(in, T_in, w_t, p, s0, ht, hb);
+    }
     if (Cin % 64 == 0) {
       p.kb_per_tap = Cin / 64;
       if (Cout <= 32) return launch_conv_dxr<32, 64>(in, T_in, w_t, p, s0, ht, hb);

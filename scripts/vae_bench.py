@@ -12,7 +12,10 @@ def main():
     dev = torch.device("cuda")
     z = torch.randn(7, 16, 52, 90, device=dev)
     s = torch.cuda.current_stream()
-    for mode in ("none", "conv1", "all", "none", "conv1", "all"):
+    from paper_2512_23379_b200 import _capi as A
+    variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [0]
+    for var, mode in [(v, "all") for v in variants] * 2:
+        A.call("ftb_set_conv_variant", var)
         dec = DeviceVAEDecoder(VAEConfig(z_dim=16), dev, params=None, seed=201, rgb8=True, fuse_norm=mode)
         for _ in range(2):
             dec.decode_device_tensor(z, s)
@@ -23,7 +26,7 @@ def main():
             dec.decode_device_tensor(z, s)
         e1.record()
         torch.cuda.synchronize()
-        print("fuse_norm=%-5s decode %.1f ms" % (mode, e0.elapsed_time(e1) / 5), flush=True)
+        print("conv variant %d fuse_norm=%-5s decode %.1f ms" % (var, mode, e0.elapsed_time(e1) / 5), flush=True)
         del dec
         torch.cuda.empty_cache()
 

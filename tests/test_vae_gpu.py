@@ -32,7 +32,7 @@ CONV_CASES = [  # T_out, H, W, Cin, Cout, k
 ]
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("T,H,W,Cin,Cout,k", CONV_CASES)
 def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k, variant):
     from paper_2512_23379_b200 import _capi as A
