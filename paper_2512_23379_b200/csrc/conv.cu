@@ -182,6 +182,48 @@ template <int BN>
 __device__ __forceinline__ void conv_epilogue_tile(const ConvParams& p, uint32_t tmem_row, int n_blk, int t, int y,
                                                    int x) {
   const bool live = x < p.W;
+  if constexpr (BN <= 96) {
+    if (p.norm_out) {   // register-resident: all BN channels of the pixel stay in registers (no read-back)
+      float vals[BN];
+      float ss = 0.f;
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        if (c * 32 >= p.Cout) break;   // Cout < BN (warp-uniform)
+        uint32_t r[32];
+        tmem_ld32(tmem_row + c * 32, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (live) {
+          conv_epilogue_values(p, t, y, x, c * 32, v);
+          if (p.write_main) conv_store(p, t, y, x, c * 32, v);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          ss += v[j] * v[j];
+          vals[c * 32 + j] = v[j];
+        }
+      }
+      if (!live) return;
+      const float inv = sqrtf((float)p.Cout) / fmaxf(sqrtf(ss), 1e-12f);
+      const long long pix = ((long long)t * p.H + y) * p.W + x;
+      uint4* o = reinterpret_cast<uint4*>(p.norm_out + pix * p.norm_ld);
+#pragma unroll
+      for (int q = 0; q < BN / 8; ++q) {
+        if (q * 8 >= p.Cout) break;
+        float a[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float f = vals[8 * q + e] * inv * __ldg(p.norm_gamma + 8 * q + e);
+          if (p.norm_silu) f = f * fmaf(0.5f, tanh_fast(0.5f * f), 0.5f);
+          a[e] = f;
+        }
+        o[q] = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]), pack_bf16(a[6], a[7]));
+      }
+      return;
+    }
+  }
   float ss = 0.f;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 32) {
