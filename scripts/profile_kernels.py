@@ -1,5 +1,5 @@
 """Run each hot kernel at its 14B-shape size a few times (for ncu capture).
-usage: python scripts/profile_kernels.py [gemm|oproj|ffn2|norm|fmha|cross|conv|all]"""
+usage: python scripts/profile_kernels.py [gemm|oproj|ffn2|xpb|norm|fmha|cross|conv|all]"""
 import math
 import sys
 
@@ -22,8 +22,8 @@ def main(which):
             A.call("ftb_set_gemm_group", g)
             for _ in range(3):
                 ops.gemm(a, w, out, "bf16")
-    if which in ("oproj", "ffn2", "all"):
-        K = m if which != "ffn2" else 13824
+    if which in ("oproj", "ffn2", "xpb", "all"):
+        K = {"ffn2": 13824, "xpb": 1600}.get(which, m)   # xpb: folded cross-attention output GEMM
         a = torch.randn(L, K, device=dev).to(torch.bfloat16)
         w = (torch.randn(m, K, device=dev) / 70).to(torch.bfloat16)
         h = torch.randn(L, m, device=dev)

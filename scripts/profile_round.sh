@@ -10,11 +10,11 @@ mkdir -p $OUT
 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/plain_bench.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$R.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1 || true
-for w in gemm fmha cross conv norm; do
+for w in gemm fmha xpb conv norm; do
   python scripts/profile_kernels.py $w > /dev/null
 done
-declare -A K=([gemm]=gemm_tc [fmha]=fmha2 [cross]=xattn [conv]=conv_ [norm]=norm_modulate)
-for w in gemm fmha cross conv norm; do
+declare -A K=([gemm]=gemm_tc [fmha]=fmha2 [xpb]=gemm_tc [conv]=conv_ [norm]=norm_modulate)
+for w in gemm fmha xpb conv norm; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:${K[$w]} -s 1 -c 1 \
     -o $OUT/full_${R}_$w python scripts/profile_kernels.py $w > $OUT/full_${R}_$w.log 2>&1 || true
 done
