@@ -39,6 +39,7 @@ struct GemmParams {
   int group_m;                  // pair kernel: m-blocks per raster group (B reuse in L2)
   int n_peers;                  // > 0: QKV_ROPE / F32 stores go to peer-mapped buffers
   void* peers[FTB_MAX_PEERS];
+  int staged;                   // pair kernel: residual epilogue through the per-warp smem tile
 };
 
 template <int BN>
@@ -107,6 +108,70 @@ __device__ __forceinline__ bool resid_tile_pipelined(const GemmParams& p, uint32
     }
   }
   return true;
+}
+
+// Staged residual epilogue (RESID_F32, full-width tile, 16-byte aligned rows). tcgen05.ld
+// hands each thread one row; the thread parks a chunk's 32 accumulators in the warp's 4 KB
+// smem tile (16-byte slots XOR-swizzled by row, conflict-free both ways) and the warp then
+// walks its 32 rows row-contiguously: lane = (row % 4, float4 column), so every global
+// float4 load/store of h covers four full 128-byte lines (the row-per-thread path touches
+// 32 lines per instruction and is L1-wavefront bound at short K). h of chunk c+1 is loaded
+// before chunk c is combined. Same arithmetic as epilogue_chunk: h += gate * (acc + bias).
+template <int WIDTH>
+__device__ __forceinline__ void resid_tile_staged(const GemmParams& p, uint32_t tmem_row, int gr0, int gc_base,
+                                                  float4* stg) {
+  const int lane = lane_id();
+  const int sub = lane >> 3, j = lane & 7;
+  float* out = reinterpret_cast<float*>(p.out) + (long long)(gr0 + sub) * p.ldc + gc_base + 4 * j;
+  const long long step = 4 * p.ldc;
+  const int rows_left = p.M - gr0 - sub;  // row 4i+sub is live while 4i < rows_left
+  float4 hb[2][8];
+  auto load = [&](int c, float4 (&dst)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      dst[i] = 4 * i < rows_left ? *reinterpret_cast<const float4*>(out + i * step + c * 32)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  load(0, hb[0]);
+#pragma unroll
+  for (int c = 0; c < WIDTH / 32; ++c) {
+    if (c + 1 < WIDTH / 32) load(c + 1, hb[(c + 1) & 1]);
+    uint32_t r[32];
+    tmem_ld32(tmem_row + c * 32, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      stg[lane * 8 + (q ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+    __syncwarp();
+    const int gc = gc_base + c * 32 + 4 * j;
+    const float4 b = p.bias ? __ldg(reinterpret_cast<const float4*>(p.bias + gc)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int rr = 4 * i + sub, row = gr0 + rr;
+      float4 a = stg[rr * 8 + (j ^ (rr & 7))];
+      if (4 * i < rows_left) {
+        if (p.bias) {
+          a.x += b.x;
+          a.y += b.y;
+          a.z += b.z;
+          a.w += b.w;
+        }
+        float4 gg = make_float4(1.f, 1.f, 1.f, 1.f);
+        if (p.group_vec) {
+          const long long g = (p.rows_per_group > 0) ? (row + p.row_offset) / p.rows_per_group : 0;
+          gg = __ldg(reinterpret_cast<const float4*>(p.group_vec + g * p.group_ld + gc));
+        }
+        float4 h = hb[c & 1][i];
+        h.x += gg.x * a.x;
+        h.y += gg.y * a.y;
+        h.z += gg.z * a.z;
+        h.w += gg.w * a.w;
+        *reinterpret_cast<float4*>(out + i * step + c * 32) = h;
+      }
+    }
+    __syncwarp();
+  }
 }
 
 // Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
@@ -400,7 +465,8 @@ constexpr int PAIR_STAGES = 6;
 constexpr int PAIR_A_BYTES = 128 * GEMM_BK * 2;
 constexpr int PAIR_B_BYTES = 128 * GEMM_BK * 2;
 constexpr int PAIR_STAGE_BYTES = PAIR_A_BYTES + PAIR_B_BYTES;
-constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 1024 + 256;
+constexpr int PAIR_EPI_STAGE = 8 * 4096;  // per-epilogue-warp 32 x 32 fp32 staging tiles
+constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 1024 + 256 + PAIR_EPI_STAGE;
 
 __device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int group_m, int& m_blk, int& n_blk) {
   const int group = group_m * num_n;
@@ -412,7 +478,7 @@ __device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int 
   n_blk = local / gm;
 }
 
-template <int EPG>
+template <int EPG, bool STAGED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmParams p) {
@@ -516,7 +582,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
-      if (!resid_tile_pipelined<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk * 256))
+      if (STAGED) {  // host guarantees RESID_F32, N % 256 == 0 and aligned rows / gate / bias
+        float4* stg = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
+        resid_tile_staged<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr - lane, n_blk * 256, stg);
+      } else if (!resid_tile_pipelined<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk * 256))
 #pragma unroll 1
       for (int c0 = 0; c0 < 256; c0 += 32) {
         const int gc0 = n_blk * 256 + c0;
@@ -540,18 +609,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
   if (warp == 2) tmem_dealloc_pair<512>(tmem_base);
 }
 
-template <int EPG>
+template <int EPG, bool STAGED>
 static int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_pair_kernel<EPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_tc_pair_kernel<EPG, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
     configured = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.N + 255) / 256);
   const int max_pairs = sm_count() / 2;
   const int pairs = tiles < max_pairs ? tiles : max_pairs;
-  gemm_tc_pair_kernel<EPG><<<2 * pairs, GEMM_THREADS + (EPG - 1) * 128, PAIR_SMEM, stream>>>(ta, tb, p);
+  gemm_tc_pair_kernel<EPG, STAGED><<<2 * pairs, GEMM_THREADS + (EPG - 1) * 128, PAIR_SMEM, stream>>>(ta, tb, p);
   return check_launch("gemm_tc_pair_kernel");
 }
 
@@ -575,10 +645,13 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
 using namespace ftb;
 
 static int g_gemm_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
+static int g_gemm_staged = 1;   // pair kernel residual epilogue through smem (flag 4 turns it off)
 
 extern "C" int ftb_set_gemm_variant(int32_t v) {
-  if (v < 0 || v > 2) return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair)");
-  g_gemm_variant = v;
+  if ((v & 3) > 2 || v < 0 || v > 6)
+    return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair), plus 4 = row-per-thread residual epilogue");
+  g_gemm_variant = v & 3;
+  g_gemm_staged = (v & 4) ? 0 : 1;
   return FTB_OK;
 }
 
@@ -615,6 +688,7 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   }
   GemmParams p{};
   p.n_peers = epi->n_peers;
+  p.staged = g_gemm_staged;
   for (int i = 0; i < epi->n_peers; ++i) p.peers[i] = epi->peer_out[i];
   p.M = M;
   p.N = N;
@@ -663,7 +737,13 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // short K: the per-tile mainloop is shorter than one epilogue warpgroup's drain -> two groups
   const bool epg2 = K <= 2048;
-  if (pair) return epg2 ? launch_gemm_pair<2>(ta, tb, p, s) : launch_gemm_pair<1>(ta, tb, p, s);
+  if (pair) {
+    auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    const bool staged = p.staged && p.kind == FTB_EPI_RESID_F32 && N % 256 == 0 && !(p.ldc & 3) && al16(p.out) &&
+                        (!p.group_vec || (!(p.group_ld & 3) && al16(p.group_vec))) && (!p.bias || al16(p.bias));
+    if (staged) return epg2 ? launch_gemm_pair<2, true>(ta, tb, p, s) : launch_gemm_pair<1, true>(ta, tb, p, s);
+    return epg2 ? launch_gemm_pair<2, false>(ta, tb, p, s) : launch_gemm_pair<1, false>(ta, tb, p, s);
+  }
   if (BN == 64) return epg2 ? launch_gemm<64, 2>(ta, tb, p, s) : launch_gemm<64, 1>(ta, tb, p, s);
   if (BN == 128) return epg2 ? launch_gemm<128, 2>(ta, tb, p, s) : launch_gemm<128, 1>(ta, tb, p, s);
   return epg2 ? launch_gemm<256, 2>(ta, tb, p, s) : launch_gemm<256, 1>(ta, tb, p, s);

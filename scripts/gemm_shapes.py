@@ -21,12 +21,17 @@ def timeit(fn, reps=20, warm=3):
 
 
 def main():
+    only = sys.argv[1].split(",") if len(sys.argv) > 1 else None
     dev = torch.device("cuda")
     L = 10530
     for (N, K, kind, tag) in [(8960, 1536, "gelu_bf16", "ffn1_1.3b"), (1536, 1536, "resid_f32", "o_1.3b"),
                               (4608, 1536, "bf16", "qkv_1.3b"), (1536, 8960, "resid_f32", "ffn2_1.3b"),
                               (13824, 5120, "gelu_bf16", "ffn1_14b"), (5120, 5120, "resid_f32", "o_14b"),
-                              (15360, 5120, "bf16", "qkv_14b"), (5120, 13824, "resid_f32", "ffn2_14b")]:
+                              (15360, 5120, "bf16", "qkv_14b"), (5120, 13824, "resid_f32", "ffn2_14b"),
+                              (480, 1536, "f32", "xs_1.3b"), (1536, 480, "resid_f32", "xpb_1.3b"),
+                              (1600, 5120, "f32", "xs_14b"), (5120, 1600, "resid_f32", "xpb_14b")]:
+        if only and tag not in only:
+            continue
         a = torch.randn(L, K, device=dev).to(torch.bfloat16)
         w = (torch.randn(N, K, device=dev) / K ** 0.5).to(torch.bfloat16)
         out = torch.zeros(L, N, device=dev, dtype=torch.float32 if kind.endswith("f32") else torch.bfloat16)

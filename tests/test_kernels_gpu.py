@@ -84,6 +84,31 @@ def test_gemm_resid_gate_and_rowadd(ops, cuda):
     assert rel(out, a.float() @ w.float().t() + b + gate[grp]) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(1000, 512, 1600), (300, 1536, 64), (10530 // 8, 5120, 256)])
+def test_gemm_resid_staged_matches_row_per_thread(ops, cuda, M, N, K):
+    """The smem-staged residual epilogue of the pair kernel is bit-identical to the
+    row-per-thread one (ragged M, gate groups that straddle 32-row warp spans)."""
+    from paper_2512_23379_b200 import _capi as A
+    g = torch.Generator().manual_seed(M + K)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    b = torch.randn(N, generator=g).to(cuda)
+    gate = torch.randn(7, N, generator=g).to(cuda)
+    h0 = torch.randn(M, N, generator=g).to(cuda)
+    outs = []
+    for variant in (0, 6):
+        h = h0.clone()
+        A.call("ftb_set_gemm_variant", variant)
+        try:
+            ops.gemm(a, w, h, "resid_f32", bias=b, group_vec=gate, rows_per_group=(M + 6) // 7)
+        finally:
+            A.call("ftb_set_gemm_variant", 0)
+        outs.append(h)
+    assert torch.equal(outs[0], outs[1])
+    grp = torch.arange(M, device=cuda) // ((M + 6) // 7)
+    assert rel(outs[0], h0 + gate[grp] * (a.float() @ w.float().t() + b)) < 1e-5
+
+
 def test_gemm_chunked_a(ops, cuda):
     """Ulysses gather layout: A's K dim arrives as g head-group slices."""
     g = torch.Generator().manual_seed(9)
