@@ -12,7 +12,8 @@ from scripts.gemm_shapes import timeit  # noqa: E402
 
 def main():
     dev = torch.device("cuda")
-    variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [0, 1]
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    variants = [int(v) for v in args[0].split(",")] if args else [0, 1]
     L = 10530
     for m in (5120, 1536):
         h = torch.randn(L, m, device=dev) * 3 + 0.5
@@ -23,8 +24,15 @@ def main():
         for var in variants:
             A.call("ftb_set_norm_variant", var)
             u = torch.empty(L, m, device=dev, dtype=torch.bfloat16)
-            for tag, kw in (("adaln", dict(shift=mod[:, :m], scale=mod[:, m:], rows_per_group=1170)),
-                            ("affine", dict(gamma=g, beta=b))):
+            cases = [("adaln", dict(shift=mod[:, :m], scale=mod[:, m:], rows_per_group=1170)),
+                     ("affine", dict(gamma=g, beta=b))]
+            if "--diag" in sys.argv:
+                cases += [("adaln1g", dict(shift=mod[:, :m], scale=mod[:, m:], rows_per_group=L)),
+                          ("scale", dict(scale=mod[:, m:], rows_per_group=1170)),
+                          ("shift", dict(shift=mod[:, :m], rows_per_group=1170)),
+                          ("plain", dict()),
+                          ("gamma", dict(gamma=g))]
+            for tag, kw in cases:
                 fn = lambda: ops.norm_modulate(h, u, **kw)  # noqa: E731
                 t = timeit(fn, reps=50)
                 byt = L * m * 6
