@@ -227,8 +227,9 @@ int ftb_conv3d_norm_bf16(const void* in, const void* halo_top, const void* halo_
                          int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW,
                          int32_t t0, const float* bias, const void* resid, int64_t resid_ld, void* out,
                          int64_t out_ld, int32_t T_out, int32_t mode, const ftb_conv_norm* norm, void* stream);
-/* Conv kernel variant: 0 auto (one haloed TMA box per (dt,dy) feeds the 3 dx taps when KH=KW=3 and
- * Cin % 64 == 0), 1 per-tap boxes. */
+/* Conv kernel variant: 0 auto, 1 per-tap boxes, 2 dx reuse (one haloed TMA box per (dt,dy) feeds
+ * the 3 dx taps) on CTA pairs, 3 dx reuse on single CTAs, 4 CTA pairs with one 128-pixel M-subtile
+ * per CTA (auto uses two at Cout 96). */
 int ftb_set_conv_variant(int32_t variant);
 /* y = [silu](x / max(||x||_2, eps) * sqrt(C) * gamma) per pixel, channel-last bf16. */
 int ftb_rmsnorm_silu_bf16(const void* x, int64_t n_pix, int32_t C, const float* gamma, float eps,

@@ -641,25 +641,31 @@ static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const Conv
 // weight bytes staged and read per FLOP halve (the single-CTA kernel is bound by shared-memory
 // operand bandwidth at BN <= 192). Completions land on the leader's barriers; MMA commits are
 // multicast to both CTAs; each CTA drains its own 128 rows of the accumulator.
-template <int BN, int BK>
+//
+// MSUB = 2 (Cout 96): each CTA owns two 128-pixel M-subtiles that share every weight stage
+// (two A boxes, one set of B taps, two accumulators per TMEM buffer), halving the weight
+// bytes each SM pulls from L2 per FLOP. At Cout 96 one subtile's MMAs take 48 clk per K=16
+// step against ~61 B/clk of A+B operand fill, which outruns the L2->SM feed.
+template <int BN, int BK, int MSUB = 1>
 struct DxrPairCfg {
   static constexpr int ROW = BK * 2;
   static constexpr int A_BYTES = (DXR_AROWS * ROW + 1023) / 1024 * 1024;
   static constexpr int B_TAP = (BN / 2) * ROW;           // this CTA's half of the Cout rows
-  static constexpr int STAGE_BYTES = A_BYTES + 3 * B_TAP;
+  static constexpr int STAGE_BYTES = MSUB * A_BYTES + 3 * B_TAP;
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 10 ? 10 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = (2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512);
+  static constexpr int TMEM_COLS = (2 * MSUB * BN <= 128) ? 128 : ((2 * MSUB * BN <= 256) ? 256 : 512);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 4u;
   static constexpr uint32_t SBO = 8 * ROW;
 };
 
-template <int BN, int BK>
+template <int BN, int BK, int MSUB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     conv_dxr_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ CUtensorMap tmTop, const __grid_constant__ CUtensorMap tmBot,
                          const ConvParams p) {
-  using C = DxrPairCfg<BN, BK>;
+  static_assert(2 * MSUB * BN <= 512, "TMEM: two buffers of MSUB accumulators");
+  using C = DxrPairCfg<BN, BK, MSUB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -672,7 +678,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const uint32_t rank = cluster_ctarank();
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int num_m = p.T * p.H * p.num_xt;
-  const int num_pm = (num_m + 1) / 2;
+  const int num_pm = (num_m + 2 * MSUB - 1) / (2 * MSUB);
   const int num_n = (p.Cout + BN - 1) / BN;
   const int num_tiles = num_pm * num_n;
   const int rows = p.KT * 3;
@@ -703,24 +709,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
         const int pm = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
-        const int m_blk = min(2 * pm + (int)rank, num_m - 1);   // odd tail: the spare CTA recomputes a tile
-        const int xt = m_blk % p.num_xt;
-        const int ty = m_blk / p.num_xt;
-        const int t = ty % p.T, y = ty / p.T;
+        int xt[MSUB], t[MSUB], y[MSUB];
+#pragma unroll
+        for (int sub = 0; sub < MSUB; ++sub) {
+          // m-tile 2*MSUB*pm + 2*sub + rank; a ragged tail recomputes the last tile (not stored)
+          const int m_blk = min(2 * MSUB * pm + 2 * sub + (int)rank, num_m - 1);
+          xt[sub] = m_blk % p.num_xt;
+          const int ty = m_blk / p.num_xt;
+          t[sub] = ty % p.T;
+          y[sub] = ty / p.T;
+        }
         for (int kb = 0; kb < num_kb; ++kb) {
           const int r = kb / p.kb_per_tap, cb = kb - r * p.kb_per_tap;
           const int dy = r % 3, dt = r / 3;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
-          uint8_t* sb = sa + C::A_BYTES;
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (DXR_AROWS * C::ROW + 3 * C::B_TAP));
-          const int row = y + dy - 1;
-          if (p.halo && row < 0)
-            tma_load_4d_pair(sa, &tmTop, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
-          else if (p.halo && row >= p.H)
-            tma_load_4d_pair(sa, &tmBot, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
-          else
-            tma_load_4d_pair(sa, &tmA, &full_bar[stage], cb * BK, xt * 128 - 1, row, t + dt + p.t0);
+          uint8_t* sb = sa + MSUB * C::A_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (MSUB * DXR_AROWS * C::ROW + 3 * C::B_TAP));
+#pragma unroll
+          for (int sub = 0; sub < MSUB; ++sub) {
+            const int row = y[sub] + dy - 1;
+            uint8_t* dst = sa + sub * C::A_BYTES;
+            if (p.halo && row < 0)
+              tma_load_4d_pair(dst, &tmTop, &full_bar[stage], cb * BK, xt[sub] * 128 - 1, 0, t[sub] + dt + p.t0);
+            else if (p.halo && row >= p.H)
+              tma_load_4d_pair(dst, &tmBot, &full_bar[stage], cb * BK, xt[sub] * 128 - 1, 0, t[sub] + dt + p.t0);
+            else
+              tma_load_4d_pair(dst, &tmA, &full_bar[stage], cb * BK, xt[sub] * 128 - 1, row, t[sub] + dt + p.t0);
+          }
           const int tap0 = (dt * 3 + dy) * 3;
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx)
@@ -744,19 +760,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
+        const uint32_t tmem_d = tmem_base + acc * MSUB * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
-          const uint32_t sb = sa + C::A_BYTES;
+          const uint32_t sb = sa + MSUB * C::A_BYTES;
 #pragma unroll
-          for (int dx = 0; dx < 3; ++dx)
+          for (int sub = 0; sub < MSUB; ++sub)
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              mma_bf16_ss_pair_elect(tmem_d, sdesc(sa + dx * C::ROW + k * 32, 16, C::SBO, C::LAYOUT),
-                                     sdesc(sb + dx * C::B_TAP + k * 32, 16, C::SBO, C::LAYOUT), idesc,
-                                     (kb | dx | k) ? 1u : 0u);
+            for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                mma_bf16_ss_pair_elect(tmem_d + sub * BN,
+                                       sdesc(sa + sub * C::A_BYTES + dx * C::ROW + k * 32, 16, C::SBO, C::LAYOUT),
+                                       sdesc(sb + dx * C::B_TAP + k * 32, 16, C::SBO, C::LAYOUT), idesc,
+                                       (kb | dx | k) ? 1u : 0u);
           mma_commit_pair_elect(&empty_bar[stage], 0x3);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -775,17 +794,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
       if ((it & 1) != eg) continue;
       const int pm = tile / num_n, n_blk = tile - (tile / num_n) * num_n;
-      const int m_raw = 2 * pm + (int)rank;
-      const int m_blk = min(m_raw, num_m - 1);
-      const int xt = m_blk % p.num_xt;
-      const int ty = m_blk / p.num_xt;
-      const int t = ty % p.T, y = ty / p.T;
-      // the spare CTA of an odd tail drains its accumulator without storing (x out of range)
-      const int x = m_raw < num_m ? xt * 128 + q * 32 + lane : p.W;
       const int acc = it & 1;
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
-      conv_epilogue_tile<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, n_blk, t, y, x);
+#pragma unroll 1
+      for (int sub = 0; sub < MSUB; ++sub) {
+        const int m_raw = 2 * MSUB * pm + 2 * sub + (int)rank;
+        const int m_blk = min(m_raw, num_m - 1);
+        const int xt = m_blk % p.num_xt;
+        const int ty = m_blk / p.num_xt;
+        const int t = ty % p.T, y = ty / p.T;
+        // a recomputed tail tile drains its accumulator without storing (x out of range)
+        const int x = m_raw < num_m ? xt * 128 + q * 32 + lane : p.W;
+        conv_epilogue_tile<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + (acc * MSUB + sub) * BN, n_blk, t, y, x);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
@@ -797,14 +819,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
 }
 
-template <int BN, int BK>
+template <int BN, int BK, int MSUB = 1>
 static int launch_conv_dxr_pair(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s,
                                 const void* halo_top = nullptr, const void* halo_bot = nullptr) {
-  using C = DxrPairCfg<BN, BK>;
+  using C = DxrPairCfg<BN, BK, MSUB>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(conv_dxr_pair_kernel<BN, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(conv_dxr_pair_kernel<BN, BK, MSUB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "conv_dxr_pair smem attribute");
     configured = true;
   }
@@ -834,10 +856,10 @@ static int launch_conv_dxr_pair(const void* in, int T_in, const void* w_t, const
     if (rc) return rc;
   }
   const int num_m = p.T * p.H * p.num_xt;
-  const int tiles = ((num_m + 1) / 2) * ((p.Cout + BN - 1) / BN);
+  const int tiles = ((num_m + 2 * MSUB - 1) / (2 * MSUB)) * ((p.Cout + BN - 1) / BN);
   const int max_pairs = sm_count() / 2;
   const int pairs = tiles < max_pairs ? tiles : max_pairs;
-  conv_dxr_pair_kernel<BN, BK><<<2 * pairs, 384, C::SMEM, s>>>(ta, tb, ttop, tbot, p);
+  conv_dxr_pair_kernel<BN, BK, MSUB><<<2 * pairs, 384, C::SMEM, s>>>(ta, tb, ttop, tbot, p);
   return check_launch("conv_dxr_pair_kernel");
 }
 
@@ -845,10 +867,11 @@ static int launch_conv_dxr_pair(const void* in, int T_in, const void* w_t, const
 
 using namespace ftb;
 
-static int g_conv_variant = 0;  // 0 auto, 1 per-tap kernel, 2 dx reuse on CTA pairs, 3 dx reuse single-CTA
+static int g_conv_variant = 0;  // 0 auto, 1 per-tap kernel, 2 dx reuse on CTA pairs, 3 dx reuse single-CTA,
+                                // 4 CTA pairs with one M-subtile per CTA
 extern "C" int ftb_set_conv_variant(int32_t v) {
-  if (v < 0 || v > 3)
-    return set_error(FTB_EINVAL, "conv variant must be 0 (auto), 1 (per-tap), 2 (dx reuse, CTA pair) or 3 (dx reuse, 1 CTA)");
+  if (v < 0 || v > 4)
+    return set_error(FTB_EINVAL, "conv variant must be 0 (auto), 1 (per-tap), 2 (dx reuse, CTA pair), 3 (dx reuse, 1 CTA) or 4 (pair, one subtile)");
   g_conv_variant = v;
   return FTB_OK;
 }
@@ -913,16 +936,24 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
     cudaStream_t s0 = reinterpret_cast<cudaStream_t>(stream);
     const void *ht = halo_top, *hb = halo_bot;
     // CTA pairs halve each SM's weight traffic (auto for Cout 96 / 192: the smem-bound levels)
-    const bool pair = (g_conv_variant == 2 || g_conv_variant == 0) && (Cout == 96 || Cout == 192);
+    // (Cout 96 / multiples of 192: the smem- and L2-feed-bound levels); variant 4 = pair
+    // without the two-subtile weight sharing at Cout 96 (A/B)
+    const bool pair = (g_conv_variant == 2 || g_conv_variant == 4 || g_conv_variant == 0) &&
+                      (Cout == 96 || Cout % 192 == 0) && !(norm && Cout > 192);
     if (pair) {
+      const bool msub = g_conv_variant != 4;
       if (Cin % 64 == 0) {
         p.kb_per_tap = Cin / 64;
-        return Cout == 96 ? launch_conv_dxr_pair<96, 64>(in, T_in, w_t, p, s0, ht, hb)
-                          : launch_conv_dxr_pair<192, 64>(in, T_in, w_t, p, s0, ht, hb);
+        if (Cout == 96)
+          return msub ? launch_conv_dxr_pair<96, 64, 2>(in, T_in, w_t, p, s0, ht, hb)
+                      : launch_conv_dxr_pair<96, 64>(in, T_in, w_t, p, s0, ht, hb);
+        return launch_conv_dxr_pair<192, 64>(in, T_in, w_t, p, s0, ht, hb);
       }
       p.kb_per_tap = Cin / 32;
-      return Cout == 96 ? launch_conv_dxr_pair<96, 32>(in, T_in, w_t, p, s0, ht, hb)
-                        : launch_conv_dxr_pair<192, 32>(in, T_in, w_t, p, s0, ht, hb);
+      if (Cout == 96)
+        return msub ? launch_conv_dxr_pair<96, 32, 2>(in, T_in, w_t, p, s0, ht, hb)
+                    : launch_conv_dxr_pair<96, 32>(in, T_in, w_t, p, s0, ht, hb);
+      return launch_conv_dxr_pair<192, 32>(in, T_in, w_t, p, s0, ht, hb);
     }
     if (Cin % 64 == 0) {
       p.kb_per_tap = Cin / 64;

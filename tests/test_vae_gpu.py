@@ -29,10 +29,11 @@ CONV_CASES = [  # T_out, H, W, Cin, Cout, k
     (3, 6, 150, 64, 96, (3, 3, 3)),      # dx-reuse kernel (Cin % 64 == 0, 3x3 taps)
     (2, 4, 90, 128, 192, (1, 3, 3)),
     (2, 3, 33, 384, 384, (3, 3, 3)),
+    (1, 3, 130, 96, 96, (3, 3, 3)),      # 6 m-tiles: ragged for the two-subtile pair kernel
 ]
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("T,H,W,Cin,Cout,k", CONV_CASES)
 def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k, variant):
     from paper_2512_23379_b200 import _capi as A
