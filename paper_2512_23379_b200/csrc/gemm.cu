@@ -40,6 +40,7 @@ struct GemmParams {
   int n_peers;                  // > 0: QKV_ROPE / F32 stores go to peer-mapped buffers
   void* peers[FTB_MAX_PEERS];
   int staged;                   // pair kernel: residual epilogue through the per-warp smem tile
+  int prefetch;                 // staged residual epilogue: L2 prefetch of the tile's h rows
 };
 
 template <int BN>
@@ -579,9 +580,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       int m_blk, n_blk;
       pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
       const int acc = it & 1;
+      const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
+      if (STAGED && p.prefetch && gr < p.M) {
+        // pull this thread's 1 KB row of h into L2 while the tile's MMAs run, so the epilogue's
+        // h loads hit L2 (DRAM latency x the few loads in flight per warp otherwise bound it)
+        const float* hrow = reinterpret_cast<const float*>(p.out) + (long long)gr * p.ldc + n_blk * 256;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 1024;" ::"l"(hrow) : "memory");
+      }
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
       if (STAGED) {  // host guarantees RESID_F32, N % 256 == 0 and aligned rows / gate / bias
         float4* stg = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
         resid_tile_staged<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr - lane, n_blk * 256, stg);
@@ -646,12 +653,15 @@ using namespace ftb;
 
 static int g_gemm_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
 static int g_gemm_staged = 1;   // pair kernel residual epilogue through smem (flag 4 turns it off)
+static int g_gemm_prefetch = 1; // ... with an L2 prefetch of the h rows (flag 8 turns it off)
 
 extern "C" int ftb_set_gemm_variant(int32_t v) {
-  if ((v & 3) > 2 || v < 0 || v > 6)
-    return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair), plus 4 = row-per-thread residual epilogue");
+  if ((v & 3) > 2 || v < 0 || v > 14)
+    return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair), plus 4 = row-per-thread "
+                                 "residual epilogue, 8 = no h prefetch");
   g_gemm_variant = v & 3;
   g_gemm_staged = (v & 4) ? 0 : 1;
+  g_gemm_prefetch = (v & 8) ? 0 : 1;
   return FTB_OK;
 }
 
@@ -689,6 +699,9 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   GemmParams p{};
   p.n_peers = epi->n_peers;
   p.staged = g_gemm_staged;
+  // short K only: there the h rows must stream at DRAM rate behind a short mainloop; at long K
+  // the prefetched rows just displace A/B panels from L2 (measured -3..-4 % at K >= 5120)
+  p.prefetch = g_gemm_prefetch && K <= 2048;
   for (int i = 0; i < epi->n_peers; ++i) p.peers[i] = epi->peer_out[i];
   p.M = M;
   p.N = N;
