@@ -111,18 +111,21 @@ __device__ __forceinline__ bool resid_tile_pipelined(const GemmParams& p, uint32
   return true;
 }
 
-// Staged residual epilogue (RESID_F32, full-width tile, 16-byte aligned rows). tcgen05.ld
-// hands each thread one row; the thread parks a chunk's 32 accumulators in the warp's 4 KB
-// smem tile (16-byte slots XOR-swizzled by row, conflict-free both ways) and the warp then
-// walks its 32 rows row-contiguously: lane = (row % 4, float4 column), so every global
-// float4 load/store of h covers four full 128-byte lines (the row-per-thread path touches
-// 32 lines per instruction and is L1-wavefront bound at short K). h of chunk c+1 is loaded
-// before chunk c is combined. Same arithmetic as epilogue_chunk: h += gate * (acc + bias).
+// Staged fp32 epilogue of the pair kernel (RESID_F32: h += gate * (acc + bias); F32:
+// out = acc + bias; N % 32 == 0, 16-byte aligned rows). tcgen05.ld hands each thread one row;
+// the thread parks a chunk's 32 accumulators in the warp's 4 KB smem tile (16-byte slots
+// XOR-swizzled by row, conflict-free both ways) and the warp then walks its 32 rows
+// row-contiguously: lane = (row % 4, float4 column), so every global float4 access covers
+// four full 128-byte lines (the row-per-thread path touches 32 lines per instruction and is
+// L1-wavefront bound at short K). For RESID, h of chunk c+1 is loaded before chunk c is
+// combined. Same arithmetic as epilogue_chunk.
 template <int WIDTH>
-__device__ __forceinline__ void resid_tile_staged(const GemmParams& p, uint32_t tmem_row, int gr0, int gc_base,
-                                                  float4* stg) {
+__device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tmem_row, int gr0, int gc_base,
+                                                float4* stg) {
   const int lane = lane_id();
   const int sub = lane >> 3, j = lane & 7;
+  const bool resid = p.kind == FTB_EPI_RESID_F32;
+  const int nch = min(WIDTH, p.N - gc_base) >> 5;  // chunks of 32 columns in this tile
   float* out = reinterpret_cast<float*>(p.out) + (long long)(gr0 + sub) * p.ldc + gc_base + 4 * j;
   const long long step = 4 * p.ldc;
   const int rows_left = p.M - gr0 - sub;  // row 4i+sub is live while 4i < rows_left
@@ -130,13 +133,14 @@ __device__ __forceinline__ void resid_tile_staged(const GemmParams& p, uint32_t 
   auto load = [&](int c, float4 (&dst)[8]) {
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      dst[i] = 4 * i < rows_left ? *reinterpret_cast<const float4*>(out + i * step + c * 32)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      dst[i] = (resid && 4 * i < rows_left) ? *reinterpret_cast<const float4*>(out + i * step + c * 32)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
   };
   load(0, hb[0]);
 #pragma unroll
   for (int c = 0; c < WIDTH / 32; ++c) {
-    if (c + 1 < WIDTH / 32) load(c + 1, hb[(c + 1) & 1]);
+    if (c >= nch) break;  // warp-uniform
+    if (c + 1 < nch) load(c + 1, hb[(c + 1) & 1]);
     uint32_t r[32];
     tmem_ld32(tmem_row + c * 32, r);
     tmem_ld_wait();
@@ -158,17 +162,22 @@ __device__ __forceinline__ void resid_tile_staged(const GemmParams& p, uint32_t 
           a.z += b.z;
           a.w += b.w;
         }
-        float4 gg = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (p.group_vec) {
-          const long long g = (p.rows_per_group > 0) ? (row + p.row_offset) / p.rows_per_group : 0;
-          gg = __ldg(reinterpret_cast<const float4*>(p.group_vec + g * p.group_ld + gc));
+        float4* dst = reinterpret_cast<float4*>(out + i * step + c * 32);
+        if (resid) {
+          float4 gg = make_float4(1.f, 1.f, 1.f, 1.f);
+          if (p.group_vec) {
+            const long long g = (p.rows_per_group > 0) ? (row + p.row_offset) / p.rows_per_group : 0;
+            gg = __ldg(reinterpret_cast<const float4*>(p.group_vec + g * p.group_ld + gc));
+          }
+          float4 h = hb[c & 1][i];
+          h.x += gg.x * a.x;
+          h.y += gg.y * a.y;
+          h.z += gg.z * a.z;
+          h.w += gg.w * a.w;
+          *dst = h;
+        } else {
+          *dst = a;
         }
-        float4 h = hb[c & 1][i];
-        h.x += gg.x * a.x;
-        h.y += gg.y * a.y;
-        h.z += gg.z * a.z;
-        h.w += gg.w * a.w;
-        *reinterpret_cast<float4*>(out + i * step + c * 32) = h;
       }
     }
     __syncwarp();
@@ -581,17 +590,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
       const int acc = it & 1;
       const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
-      if (STAGED && p.prefetch && gr < p.M) {
-        // pull this thread's 1 KB row of h into L2 while the tile's MMAs run, so the epilogue's
-        // h loads hit L2 (DRAM latency x the few loads in flight per warp otherwise bound it)
+      if (STAGED && p.prefetch && p.kind == FTB_EPI_RESID_F32 && gr < p.M) {
+        // pull this thread's row of h (<= 1 KB) into L2 while the tile's MMAs run, so the
+        // epilogue's h loads hit L2 (DRAM latency x the few loads in flight per warp otherwise bound it)
         const float* hrow = reinterpret_cast<const float*>(p.out) + (long long)gr * p.ldc + n_blk * 256;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 1024;" ::"l"(hrow) : "memory");
+        const uint32_t bytes = (uint32_t)min(256, p.N - n_blk * 256) * 4;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(hrow), "r"(bytes) : "memory");
       }
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
-      if (STAGED) {  // host guarantees RESID_F32, N % 256 == 0 and aligned rows / gate / bias
+      if (STAGED) {  // host guarantees RESID_F32 / F32 (no peers), N % 32 == 0, aligned rows / gate / bias
         float4* stg = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
-        resid_tile_staged<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr - lane, n_blk * 256, stg);
+        staged_tile_f32<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr - lane, n_blk * 256, stg);
       } else if (!resid_tile_pipelined<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk * 256))
 #pragma unroll 1
       for (int c0 = 0; c0 < 256; c0 += 32) {
@@ -721,8 +731,11 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   p.has_rope = epi->rope != nullptr;
   if (epi->rope) p.rope = *epi->rope;
 
-  const int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   const bool pair = g_gemm_variant == 2 || (g_gemm_variant == 0 && M >= 256 && N >= 256);
+  int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  // few m-blocks (cond-token K/V projections, M = 37): narrower tiles until the grid covers
+  // the SMs, so the weight stream is spread over every SM's load path
+  while (!pair && BN > 64 && (long long)((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) < sm_count()) BN >>= 1;
   {
     // raster group: enough 256-row m-blocks that their A panels (~40 MB) stay in L2 while
     // the B panel streams past once per group
@@ -752,7 +765,8 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   const bool epg2 = K <= 2048;
   if (pair) {
     auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-    const bool staged = p.staged && p.kind == FTB_EPI_RESID_F32 && N % 256 == 0 && !(p.ldc & 3) && al16(p.out) &&
+    const bool staged = p.staged && (p.kind == FTB_EPI_RESID_F32 || (p.kind == FTB_EPI_F32 && !p.n_peers)) &&
+                        N % 32 == 0 && !(p.ldc & 3) && al16(p.out) &&
                         (!p.group_vec || (!(p.group_ld & 3) && al16(p.group_vec))) && (!p.bias || al16(p.bias));
     if (staged) return epg2 ? launch_gemm_pair<2, true>(ta, tb, p, s) : launch_gemm_pair<1, true>(ta, tb, p, s);
     return epg2 ? launch_gemm_pair<2, false>(ta, tb, p, s) : launch_gemm_pair<1, false>(ta, tb, p, s);

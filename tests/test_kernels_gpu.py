@@ -84,7 +84,7 @@ def test_gemm_resid_gate_and_rowadd(ops, cuda):
     assert rel(out, a.float() @ w.float().t() + b + gate[grp]) < 1e-5
 
 
-@pytest.mark.parametrize("M,N,K", [(1000, 512, 1600), (300, 1536, 64), (10530 // 8, 5120, 256)])
+@pytest.mark.parametrize("M,N,K", [(1000, 512, 1600), (300, 1536, 64), (10530 // 8, 5120, 256), (600, 1600, 320)])
 def test_gemm_resid_staged_matches_row_per_thread(ops, cuda, M, N, K):
     """The smem-staged residual epilogue of the pair kernel is bit-identical to the
     row-per-thread one (ragged M, gate groups that straddle 32-row warp spans)."""
@@ -107,6 +107,29 @@ def test_gemm_resid_staged_matches_row_per_thread(ops, cuda, M, N, K):
     assert torch.equal(outs[0], outs[1])
     grp = torch.arange(M, device=cuda) // ((M + 6) // 7)
     assert rel(outs[0], h0 + gate[grp] * (a.float() @ w.float().t() + b)) < 1e-5
+    # plain fp32 output (+ bias) through the same staged path, ragged last N tile included
+    f32 = []
+    for variant in (0, 6):
+        o = torch.full((M, N), float("nan"), device=cuda)
+        A.call("ftb_set_gemm_variant", variant)
+        try:
+            ops.gemm(a, w, o, "f32", bias=b)
+        finally:
+            A.call("ftb_set_gemm_variant", 0)
+        f32.append(o)
+    assert torch.equal(f32[0], f32[1])
+    assert rel(f32[0], a.float() @ w.float().t() + b) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(37, 10240, 512), (1, 5120, 16), (100, 4096, 256)])
+def test_gemm_few_rows(ops, cuda, M, N, K):
+    """Few m-blocks: narrowed single-CTA tiles (grid spread over the SMs)."""
+    g = torch.Generator().manual_seed(M * 7 + K)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    ops.gemm(a, w, out, "bf16")
+    assert rel(out.float(), a.float() @ w.float().t()) < 5e-3
 
 
 def test_gemm_chunked_a(ops, cuda):
