@@ -132,3 +132,11 @@ def stream_ptr(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+# Kernel-variant overrides for same-box A/B runs of bench.py (benchmarking only; the defaults
+# are the product configuration): FTB_GEMM_VARIANT / FTB_CONV_VARIANT / FTB_NORM_VARIANT.
+for _env, _fn in (("FTB_GEMM_VARIANT", "ftb_set_gemm_variant"), ("FTB_CONV_VARIANT", "ftb_set_conv_variant"),
+                  ("FTB_NORM_VARIANT", "ftb_set_norm_variant")):
+    if os.environ.get(_env):
+        check(getattr(lib, _fn)(int(os.environ[_env])), _env)
