@@ -162,6 +162,13 @@ int ftb_peer_barrier(uint32_t* const* flags, uint32_t* epoch, int32_t rank, int3
 int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim, int32_t J,
                    const void* wqT, int64_t ldwq, const void* woT, int64_t ldwo, int32_t m, float scale, void* at,
                    void* bt, void* stream);
+/* Block-diagonal operands for folding the cross-attention projections on the tensor cores
+ * (net.py:259-261 composed with the chunk's fixed cond K/V): kbd[(h,j)][h*hd+d] = scale*K[j][h*hd+d],
+ * vbd[(h,j)][h*hd+d] = V[j][h*hd+d], kv = [n_cond][K | V] bf16. Only the diagonal blocks are
+ * written (caller zero-fills kbd / vbd once). Then At = kbd . Wq^T and Bt = Wo^T . vbd^T are two
+ * ftb_gemm_bf16 calls. */
+int ftb_xattn_blockdiag(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim, int32_t J,
+                        float scale, void* kbd, void* vbd, int64_t ld, void* stream);
 /* P[r][h*J + j] = softmax_j<n_cond(S[r][h*J + j]) (bf16, padded columns 0), per head segment. */
 int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond, void* p,
                       int64_t ldp, void* stream);

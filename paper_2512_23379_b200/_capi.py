@@ -60,6 +60,7 @@ _SIGS = {
     "ftb_copy_d2d": ([vp, vp, C.c_size_t, vp], i32),
     "ftb_xattn_fold": ([vp, i64, i32, i32, i32, i32, vp, i64, vp, i64, i32, f32, vp, vp, vp], i32),
     "ftb_xattn_softmax": ([vp, i64, i32, i32, i32, i32, vp, i64, vp], i32),
+    "ftb_xattn_blockdiag": ([vp, i64, i32, i32, i32, i32, f32, vp, vp, i64, vp], i32),
     "ftb_gelu_bf16": ([vp, vp, i64, vp], i32),
     "ftb_silu_f32_to_bf16": ([vp, vp, i64, vp], i32),
     "ftb_cast_f32_bf16": ([vp, vp, i64, vp], i32),

@@ -608,6 +608,35 @@ __global__ void xattn_softmax_kernel(const float* __restrict__ s, long long lds,
                        pack_bf16(v[8 * q + 4] * inv, v[8 * q + 5] * inv), pack_bf16(v[8 * q + 6] * inv, v[8 * q + 7] * inv));
 }
 
+// Block-diagonal operands of the tensor-core fold: kbd[(h,j)][h*hd + d] = scale * K[j][h*hd + d],
+// vbd[(h,j)][h*hd + d] = V[j][h*hd + d] for j < n_cond (kv = [n_cond][K | V]). Only the diagonal
+// blocks are written; the caller keeps the rest (and rows j >= n_cond) zero.
+__global__ void xattn_blockdiag_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv, int n_cond, int heads,
+                                       int hd, int J, float scale, __nv_bfloat16* __restrict__ kbd,
+                                       __nv_bfloat16* __restrict__ vbd, long long ld) {
+  const int m = heads * hd, v8 = hd / 8;
+  const long long total = (long long)heads * n_cond * v8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int d8 = (int)(i % v8);
+    const long long hj = i / v8;
+    const int j = (int)(hj % n_cond), h = (int)(hj / n_cond);
+    const int col = h * hd + d8 * 8;
+    const uint4 kq = *reinterpret_cast<const uint4*>(kv + (long long)j * ldkv + col);
+    const uint4 vq = *reinterpret_cast<const uint4*>(kv + (long long)j * ldkv + m + col);
+    const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kq);
+    uint4 ks;
+    uint32_t* ko = reinterpret_cast<uint32_t*>(&ks);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(k2[e]);
+      ko[e] = pack_bf16(f.x * scale, f.y * scale);
+    }
+    const long long row = (long long)h * J + j;
+    *reinterpret_cast<uint4*>(kbd + row * ld + col) = ks;
+    *reinterpret_cast<uint4*>(vbd + row * ld + col) = vq;
+  }
+}
+
 }  // namespace ftb
 
 extern "C" int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim,
@@ -633,6 +662,18 @@ extern "C" int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int3
       (const __nv_bfloat16*)kv, ldkv, n_cond, head_dim, J, (const __nv_bfloat16*)woT, ldwo, m, heads,
       (__nv_bfloat16*)bt);
   return check_launch("xattn_fold_bt_kernel");
+}
+
+extern "C" int ftb_xattn_blockdiag(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim,
+                                   int32_t J, float scale, void* kbd, void* vbd, int64_t ld, void* stream) {
+  if (!kv || !kbd || !vbd || n_cond <= 0 || J < n_cond || heads <= 0 || head_dim <= 0 || (head_dim % 8) ||
+      (ldkv % 8) || (ld % 8) || ld < (int64_t)heads * head_dim)
+    return set_error(FTB_EINVAL, "xattn_blockdiag: bad arguments (n_cond <= J, head_dim / ldkv / ld % 8 == 0)");
+  const long long total = (long long)heads * n_cond * (head_dim / 8);
+  xattn_blockdiag_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>((const __nv_bfloat16*)kv, ldkv, n_cond, heads,
+                                                                     head_dim, J, scale, (__nv_bfloat16*)kbd,
+                                                                     (__nv_bfloat16*)vbd, ld);
+  return check_launch("xattn_blockdiag_kernel");
 }
 
 extern "C" int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond,

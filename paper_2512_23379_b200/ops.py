@@ -69,7 +69,7 @@ class RopeTables:
 
 def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=0, row_offset=0,
          M=None, K=None, lda=None, a_chunks=1, a_chunk_stride=0, heads=0, head_dim=0,
-         heads_per_rank=0, rope=None, peers=None, stream=None):
+         heads_per_rank=0, rope=None, peers=None, stream=None, algo_flops=None):
     """out <- epilogue(a[M,K] @ w_t[N,K]^T). `a` may be a raw buffer when
     a_chunks > 1 (Ulysses gather: M, K, lda, a_chunk_stride explicit).
     peers: device addresses (ints) for the peer-store epilogues (qkv_rope: one
@@ -103,7 +103,10 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
         epi.n_peers = len(peers)
         for i, pp in enumerate(peers):
             epi.peer_out[i] = int(pp)
-    with _Prof("gemm" if PROFILE_DETAIL is None else "gemm:%s:%dx%dx%d" % (kind, M, N, K), 2.0 * M * N * K, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
+    # algo_flops: the algorithmic FLOPs when the operands are structurally sparse (the
+    # block-diagonal fold GEMMs), so the profile's TFLOP/s do not count multiplications by zero
+    fl = 2.0 * M * N * K if algo_flops is None else float(algo_flops)
+    with _Prof("gemm" if PROFILE_DETAIL is None else "gemm:%s:%dx%dx%d" % (kind, M, N, K), fl, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
         A.call("ftb_gemm_bf16", A.ptr(a), lda, a_chunks, a_chunk_stride, A.ptr(w_t), _ld(w_t), M, N, K,
                C.byref(epi), A.stream_ptr(stream))
     return out
@@ -234,6 +237,17 @@ def xattn_fold(kv, wq_t, wo_t, at, bt, n_cond, heads, head_dim, J, scale, *, str
     with _Prof("xattn_fold", 4.0 * n_cond * m * m, 0.0, stream):
         A.call("ftb_xattn_fold", A.ptr(kv), _ld(kv), n_cond, heads, head_dim, J, A.ptr(wq_t), _ld(wq_t), A.ptr(wo_t),
                _ld(wo_t), m, float(scale), A.ptr(at), A.ptr(bt), A.stream_ptr(stream))
+
+
+def xattn_blockdiag(kv, kbd, vbd, n_cond, heads, head_dim, J, scale, *, stream=None):
+    """Diagonal blocks of the tensor-core fold operands (elementwise.cu): kbd[(h,j)][h*hd+d] =
+    scale * K[j][h*hd+d], vbd likewise from V; the rest of kbd / vbd must already be zero."""
+    for t, nm in ((kv, "kv"), (kbd, "kbd"), (vbd, "vbd")):
+        _need(t, torch.bfloat16, nm)
+    if kbd.shape != vbd.shape or kbd.stride(0) != vbd.stride(0) or kbd.shape[0] < heads * J:
+        raise ConfigError("xattn_blockdiag: kbd / vbd must be [heads*J][m] with one row stride")
+    A.call("ftb_xattn_blockdiag", A.ptr(kv), _ld(kv), n_cond, heads, head_dim, J, float(scale), A.ptr(kbd),
+           A.ptr(vbd), _ld(kbd), A.stream_ptr(stream))
 
 
 def xattn_softmax(s, p, heads, J, n_cond, *, stream=None):

@@ -128,15 +128,21 @@ def test_wan_folded_cross_attention_matches_projections(cuda):
     Lc, Lm = x["audio"].shape[0], x["motion"].shape[0]
     H, W = x["ref"].shape[1:]
     w = DeviceWeights.from_host(cfg, store.params, cuda)
-    outs = []
-    for fold in (True, False):
-        d = DeviceDenoiser(w, Lc, Lm, (H, W), fold_cross=fold)
+    outs, folds = [], []
+    for fold, tc in ((True, True), (False, False), (True, False)):
+        d = DeviceDenoiser(w, Lc, Lm, (H, W), fold_cross=fold, fold_tc=tc)
         assert d.fold == fold
         d.prepare_cond(x["audio"], x["ref"])
         fv = d.frame_vectors(np.where(np.arange(Lc) < Lm, 0.0, 0.75))
         args = [torch.as_tensor(x[k], dtype=torch.float32, device=cuda) for k in ("motion", "z", "ref")]
         outs.append(d.tokens_to_frames(d.step(*args, fv)).double().cpu().numpy())
+        if fold:
+            folds.append((d.buf["xat"].float().clone(), d.buf["xbt"].float().clone()))
     assert rel(outs[0], outs[1]) < 5e-3
+    assert rel(outs[2], outs[1]) < 5e-3
+    # tensor-core fold (block-diagonal GEMMs) == CUDA-core fold kernel, operand for operand
+    for a, b in zip(folds[0], folds[1]):
+        assert float((a - b).norm() / b.norm()) < 5e-3
     ref = WO.denoise(store.bf16_rounded().params, ocfg, x["motion"], x["z"], x["ref"], x["audio"],
                      np.where(np.arange(Lc) < Lm, 0.0, 0.75))
     assert rel(outs[0], ref) < BUDGET
