@@ -18,6 +18,7 @@ def main():
     for m in (5120, 1536):
         h = torch.randn(L, m, device=dev) * 3 + 0.5
         mod = torch.randn(10, 2 * m, device=dev)
+        mod2 = torch.randn(91, 2 * m, device=dev)
         g = torch.randn(m, device=dev)
         b = torch.randn(m, device=dev)
         ref = None
@@ -30,6 +31,9 @@ def main():
                 cases += [("adaln1g", dict(shift=mod[:, :m], scale=mod[:, m:], rows_per_group=L)),
                           ("scale", dict(scale=mod[:, m:], rows_per_group=1170)),
                           ("shift", dict(shift=mod[:, :m], rows_per_group=1170)),
+                          ("adaln_ld0", dict(shift=mod[:1, :m].expand(10, m), scale=mod[:1, m:].expand(10, m),
+                                             rows_per_group=1170)),
+                          ("adaln_g117", dict(shift=mod2[:, :m], scale=mod2[:, m:], rows_per_group=117)),
                           ("plain", dict()),
                           ("gamma", dict(gamma=g))]
             for tag, kw in cases:
