@@ -55,7 +55,8 @@ enum {
   FTB_EPI_F32 = 2,        /* out_f32  = acc + bias                                  */
   FTB_EPI_RESID_F32 = 3,  /* out_f32 += gate[g] * (acc + bias)   (gate NULL -> 1)   */
   FTB_EPI_ROWADD_F32 = 4, /* out_f32  = acc + bias + vec[g]                         */
-  FTB_EPI_QKV_ROPE = 5    /* bf16 q|k|v with 3D RoPE on q,k; Ulysses send layout    */
+  FTB_EPI_QKV_ROPE = 5,   /* bf16 q|k|v with 3D RoPE on q,k; Ulysses send layout    */
+  FTB_EPI_SEG_SOFTMAX = 6 /* bf16 per-segment softmax of the logits (folded cross-attn) */
 };
 
 /* 3D rotary tables (wan mode): per-token float32 cos/sin [token][head_dim/2]
@@ -78,6 +79,10 @@ typedef struct ftb_epilogue {
   /* FTB_EPI_QKV_ROPE only: column c of [0,3*heads*head_dim) -> (which, head, d);
    * stored at ((dest*M + row)*3 + which)*hpr*hd + (head%hpr)*hd + d, dest = head/hpr. */
   int32_t heads, head_dim, heads_per_rank;
+  /* FTB_EPI_SEG_SOFTMAX reuses them: heads = segments S, head_dim = segment width J (multiple of
+   * 8, <= 48), heads_per_rank = n_cond. GEMM column t*256 + s*J + j (s < 256/J) is key j of
+   * segment t*(256/J) + s; out[row][seg*J + j] = softmax over j < n_cond (0 for j >= n_cond);
+   * N = 256 * ceil(S / (256/J)). */
   const ftb_rope3d* rope;  /* NULL: no rotation */
   /* Peer stores (Ulysses over NVLink; 0 = local `out`):
    *  QKV_ROPE: n_peers = heads/heads_per_rank; head group `dest`'s block [M][3][hpr][hd]
@@ -166,9 +171,10 @@ int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, 
  * (net.py:259-261 composed with the chunk's fixed cond K/V): kbd[(h,j)][h*hd+d] = scale*K[j][h*hd+d],
  * vbd[(h,j)][h*hd+d] = V[j][h*hd+d], kv = [n_cond][K | V] bf16. Only the diagonal blocks are
  * written (caller zero-fills kbd / vbd once). Then At = kbd . Wq^T and Bt = Wo^T . vbd^T are two
- * ftb_gemm_bf16 calls. */
+ * ftb_gemm_bf16 calls. k_tile_segs > 0 puts kbd row (h,j) at (h / k_tile_segs) * 256 +
+ * (h % k_tile_segs) * J + j: the FTB_EPI_SEG_SOFTMAX column order for the logits GEMM. */
 int ftb_xattn_blockdiag(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim, int32_t J,
-                        float scale, void* kbd, void* vbd, int64_t ld, void* stream);
+                        float scale, void* kbd, void* vbd, int64_t ld, int32_t k_tile_segs, void* stream);
 /* P[r][h*J + j] = softmax_j<n_cond(S[r][h*J + j]) (bf16, padded columns 0), per head segment. */
 int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond, void* p,
                       int64_t ldp, void* stream);

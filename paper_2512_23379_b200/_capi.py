@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("FTB_LIB") or os.path.join(HERE, "_lib", "libftb2.so")
 
 FTB_OK, FTB_EINVAL, FTB_ECUDA, FTB_ENCCL, FTB_ENONFINITE = 0, 1, 2, 3, 4
 MAX_PEERS, IPC_HANDLE_BYTES = 8, 64
-EPI_BF16, EPI_GELU_BF16, EPI_F32, EPI_RESID_F32, EPI_ROWADD_F32, EPI_QKV_ROPE = range(6)
+EPI_BF16, EPI_GELU_BF16, EPI_F32, EPI_RESID_F32, EPI_ROWADD_F32, EPI_QKV_ROPE, EPI_SEG_SOFTMAX = range(7)
 
 vp, i32, i64, f32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint64
 
@@ -60,7 +60,7 @@ _SIGS = {
     "ftb_copy_d2d": ([vp, vp, C.c_size_t, vp], i32),
     "ftb_xattn_fold": ([vp, i64, i32, i32, i32, i32, vp, i64, vp, i64, i32, f32, vp, vp, vp], i32),
     "ftb_xattn_softmax": ([vp, i64, i32, i32, i32, i32, vp, i64, vp], i32),
-    "ftb_xattn_blockdiag": ([vp, i64, i32, i32, i32, i32, f32, vp, vp, i64, vp], i32),
+    "ftb_xattn_blockdiag": ([vp, i64, i32, i32, i32, i32, f32, vp, vp, i64, i32, vp], i32),
     "ftb_gelu_bf16": ([vp, vp, i64, vp], i32),
     "ftb_silu_f32_to_bf16": ([vp, vp, i64, vp], i32),
     "ftb_cast_f32_bf16": ([vp, vp, i64, vp], i32),

@@ -613,7 +613,7 @@ __global__ void xattn_softmax_kernel(const float* __restrict__ s, long long lds,
 // blocks are written; the caller keeps the rest (and rows j >= n_cond) zero.
 __global__ void xattn_blockdiag_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv, int n_cond, int heads,
                                        int hd, int J, float scale, __nv_bfloat16* __restrict__ kbd,
-                                       __nv_bfloat16* __restrict__ vbd, long long ld) {
+                                       __nv_bfloat16* __restrict__ vbd, long long ld, int k_tile_segs) {
   const int m = heads * hd, v8 = hd / 8;
   const long long total = (long long)heads * n_cond * v8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -632,7 +632,9 @@ __global__ void xattn_blockdiag_kernel(const __nv_bfloat16* __restrict__ kv, lon
       ko[e] = pack_bf16(f.x * scale, f.y * scale);
     }
     const long long row = (long long)h * J + j;
-    *reinterpret_cast<uint4*>(kbd + row * ld + col) = ks;
+    // kbd rows optionally in the SEG_SOFTMAX tile order (k_tile_segs heads per 256-row tile)
+    const long long krow = k_tile_segs > 0 ? (long long)(h / k_tile_segs) * 256 + (h % k_tile_segs) * J + j : row;
+    *reinterpret_cast<uint4*>(kbd + krow * ld + col) = ks;
     *reinterpret_cast<uint4*>(vbd + row * ld + col) = vq;
   }
 }
@@ -665,14 +667,16 @@ extern "C" int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int3
 }
 
 extern "C" int ftb_xattn_blockdiag(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim,
-                                   int32_t J, float scale, void* kbd, void* vbd, int64_t ld, void* stream) {
+                                   int32_t J, float scale, void* kbd, void* vbd, int64_t ld, int32_t k_tile_segs,
+                                   void* stream) {
   if (!kv || !kbd || !vbd || n_cond <= 0 || J < n_cond || heads <= 0 || head_dim <= 0 || (head_dim % 8) ||
-      (ldkv % 8) || (ld % 8) || ld < (int64_t)heads * head_dim)
-    return set_error(FTB_EINVAL, "xattn_blockdiag: bad arguments (n_cond <= J, head_dim / ldkv / ld % 8 == 0)");
+      (ldkv % 8) || (ld % 8) || ld < (int64_t)heads * head_dim || k_tile_segs < 0 || k_tile_segs * J > 256)
+    return set_error(FTB_EINVAL, "xattn_blockdiag: bad arguments (n_cond <= J, head_dim / ldkv / ld % 8 == 0, "
+                                 "k_tile_segs * J <= 256)");
   const long long total = (long long)heads * n_cond * (head_dim / 8);
   xattn_blockdiag_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>((const __nv_bfloat16*)kv, ldkv, n_cond, heads,
                                                                      head_dim, J, scale, (__nv_bfloat16*)kbd,
-                                                                     (__nv_bfloat16*)vbd, ld);
+                                                                     (__nv_bfloat16*)vbd, ld, k_tile_segs);
   return check_launch("xattn_blockdiag_kernel");
 }
 

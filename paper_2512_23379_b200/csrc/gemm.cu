@@ -184,6 +184,57 @@ __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tm
   }
 }
 
+// FTB_EPI_SEG_SOFTMAX (folded cross-attention logits): a 256-column tile holds 256 / J whole
+// J-column segments (one head's keys each; the rest of the tile is padding); the thread owns
+// one row and turns each segment into softmax probabilities over its first n_cond columns
+// (padded columns -> 0), written bf16 at column seg * J of `out`. Same arithmetic as
+// xattn_softmax_kernel (elementwise.cu), so the fused and two-pass results agree bit for bit.
+template <int J>
+__device__ __forceinline__ void segsoftmax_tile(const GemmParams& p, uint32_t tmem_row, int gr, int n_blk) {
+  constexpr int SPT = 256 / J;
+  const int n_cond = p.hpr;
+#pragma unroll 1
+  for (int s = 0; s < SPT; ++s) {
+    const int seg = n_blk * SPT + s;
+    if (seg >= p.heads) break;  // warp-uniform
+    uint32_t r[J];
+#pragma unroll
+    for (int k = 0; k < J / 8; ++k) tmem_ld8(tmem_row + s * J + 8 * k, *reinterpret_cast<uint32_t(*)[8]>(r + 8 * k));
+    tmem_ld_wait();
+    if (gr >= p.M) continue;
+    float v[J];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      v[j] = __uint_as_float(r[j]);
+      if (j < n_cond) mx = fmaxf(mx, v[j]);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      v[j] = j < n_cond ? __expf(v[j] - mx) : 0.f;
+      sum += v[j];
+    }
+    const float inv = 1.f / sum;
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + (long long)gr * p.ldc + seg * J);
+#pragma unroll
+    for (int q = 0; q < J / 8; ++q)
+      dst[q] = make_uint4(pack_bf16(v[8 * q] * inv, v[8 * q + 1] * inv), pack_bf16(v[8 * q + 2] * inv, v[8 * q + 3] * inv),
+                          pack_bf16(v[8 * q + 4] * inv, v[8 * q + 5] * inv), pack_bf16(v[8 * q + 6] * inv, v[8 * q + 7] * inv));
+  }
+}
+
+__device__ __forceinline__ void segsoftmax_dispatch(const GemmParams& p, uint32_t tmem_row, int gr, int n_blk) {
+  switch (p.head_dim) {  // J
+    case 8: segsoftmax_tile<8>(p, tmem_row, gr, n_blk); break;
+    case 16: segsoftmax_tile<16>(p, tmem_row, gr, n_blk); break;
+    case 24: segsoftmax_tile<24>(p, tmem_row, gr, n_blk); break;
+    case 32: segsoftmax_tile<32>(p, tmem_row, gr, n_blk); break;
+    case 40: segsoftmax_tile<40>(p, tmem_row, gr, n_blk); break;
+    default: segsoftmax_tile<48>(p, tmem_row, gr, n_blk); break;
+  }
+}
+
 // Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int gc0, float (&v)[32]) {
   const int N = p.N;
@@ -442,7 +493,9 @@ __global__ void __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const int gr = m_blk * GEMM_BM + q * 32 + lane;
-      if (!resid_tile_pipelined<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, gr, n_blk * BN))
+      if (BN == 256 && p.kind == FTB_EPI_SEG_SOFTMAX)
+        segsoftmax_dispatch(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, gr, n_blk);
+      else if (!resid_tile_pipelined<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, gr, n_blk * BN))
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         const int gc0 = n_blk * BN + c0;
@@ -602,6 +655,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       if (STAGED) {  // host guarantees RESID_F32 / F32 (no peers), N % 32 == 0, aligned rows / gate / bias
         float4* stg = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
         staged_tile_f32<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr - lane, n_blk * 256, stg);
+      } else if (p.kind == FTB_EPI_SEG_SOFTMAX) {
+        segsoftmax_dispatch(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk);
       } else if (!resid_tile_pipelined<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk * 256))
 #pragma unroll 1
       for (int c0 = 0; c0 < 256; c0 += 32) {
@@ -691,7 +746,14 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   const int kc = K / a_chunks;
   if (a_chunks > 1 && (kc % GEMM_BK)) return set_error(FTB_EINVAL, "gemm: K/a_chunks must be a multiple of 64");
   if (a_chunks > 1 && (a_chunk_stride & 7)) return set_error(FTB_EINVAL, "gemm: chunk stride alignment");
-  if (epi->kind < FTB_EPI_BF16 || epi->kind > FTB_EPI_QKV_ROPE) return set_error(FTB_EINVAL, "gemm: bad epilogue");
+  if (epi->kind < FTB_EPI_BF16 || epi->kind > FTB_EPI_SEG_SOFTMAX) return set_error(FTB_EINVAL, "gemm: bad epilogue");
+  if (epi->kind == FTB_EPI_SEG_SOFTMAX) {
+    const int J = epi->head_dim, segs = epi->heads, n_cond = epi->heads_per_rank;
+    if (J < 8 || J > 48 || (J % 8) || segs <= 0 || n_cond <= 0 || n_cond > J || epi->bias || epi->n_peers ||
+        (epi->ldc % 8) || epi->ldc < (int64_t)segs * J || N != (segs + 256 / J - 1) / (256 / J) * 256)
+      return set_error(FTB_EINVAL, "gemm: SEG_SOFTMAX needs J % 8 == 0 <= 48, 0 < n_cond <= J, no bias/peers, "
+                                   "N = 256 * ceil(segments / (256 / J)), ldc >= segments * J");
+  }
   if (epi->kind == FTB_EPI_QKV_ROPE) {
     if (epi->heads <= 0 || epi->head_dim <= 0 || (epi->head_dim & 1) || epi->heads_per_rank <= 0 ||
         epi->heads % epi->heads_per_rank || N != 3 * epi->heads * epi->head_dim)
@@ -735,7 +797,9 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   // few m-blocks (cond-token K/V projections, M = 37): narrower tiles until the grid covers
   // the SMs, so the weight stream is spread over every SM's load path
-  while (!pair && BN > 64 && (long long)((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) < sm_count()) BN >>= 1;
+  while (!pair && BN > 64 && epi->kind != FTB_EPI_SEG_SOFTMAX &&
+         (long long)((M + GEMM_BM - 1) / GEMM_BM) * ((N + BN - 1) / BN) < sm_count())
+    BN >>= 1;
   {
     // raster group: enough 256-row m-blocks that their A panels (~40 MB) stay in L2 while
     // the B panel streams past once per group

@@ -58,18 +58,25 @@ __global__ void rmsnorm_silu_kernel(const __nv_bfloat16* __restrict__ x, long lo
 }
 
 // Nearest 2x spatial upsample: y[t, 2i+a, 2j+b, :] = x[t, i, j, :] (16-byte vectors).
-__global__ void upsample2x_kernel(const uint4* __restrict__ x, int T, int H, int W, int cv, uint4* __restrict__ y) {
-  const long long total = (long long)T * (2 * H) * (2 * W) * cv;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    long long r = i;
-    const int c = (int)(r % cv);
-    r /= cv;
-    const int xo = (int)(r % (2 * W));
-    r /= (2 * W);
-    const int yo = (int)(r % (2 * H));
-    const int t = (int)(r / (2 * H));
-    y[i] = x[(((long long)t * H + (yo >> 1)) * W + (xo >> 1)) * cv + c];
+// Nearest 2x spatial upsample, channel-last. blockIdx.y = input row (t, y); each thread reads
+// one 16-byte input vector once and writes it to the 2x2 output positions (32-bit index math
+// per input vector instead of 64-bit div/mod chains per output vector).
+__global__ void upsample2x_kernel(const uint4* __restrict__ x, int H, int W, int cv, uint4* __restrict__ y) {
+  const long long ty = blockIdx.y;               // t * H + yi
+  const int yi = (int)(ty % H);
+  const long long t = ty / H;
+  const int n = W * cv;
+  const uint4* xr = x + ty * n;
+  const long long orow = 2LL * W * cv;           // output row length in vectors
+  uint4* y0 = y + ((t * (2 * H) + 2 * yi) * orow);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int xi = i / cv, c = i - xi * cv;
+    const uint4 v = xr[i];
+    const long long o = 2LL * xi * cv + c;
+    y0[o] = v;
+    y0[o + cv] = v;
+    y0[orow + o] = v;
+    y0[orow + o + cv] = v;
   }
 }
 }  // namespace ftb
@@ -89,11 +96,11 @@ extern "C" int ftb_rmsnorm_silu_bf16(const void* x, int64_t n_pix, int32_t C, co
 
 extern "C" int ftb_upsample2x_bf16(const void* x, int32_t T, int32_t H, int32_t W, int32_t C, void* y, void* stream) {
   if (!x || !y || (C % 8)) return set_error(FTB_EINVAL, "upsample2x: bad arguments");
-  const long long total = (long long)T * 4 * H * W * (C / 8);
-  if (total <= 0) return FTB_OK;
-  long long blocks = (total + 255) / 256, cap = (long long)sm_count() * 8;
-  upsample2x_kernel<<<(int)(blocks < cap ? blocks : cap), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      (const uint4*)x, T, H, W, C / 8, (uint4*)y);
+  if ((long long)T * H * W <= 0) return FTB_OK;
+  if ((long long)T * H > 65535) return set_error(FTB_EINVAL, "upsample2x: T * H > 65535");
+  const int n = W * (C / 8);
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)((long long)T * H));
+  upsample2x_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>((const uint4*)x, H, W, C / 8, (uint4*)y);
   return check_launch("upsample2x_kernel");
 }
 
@@ -162,20 +169,24 @@ __global__ void rmsnorm_silu_f32_kernel(const float* __restrict__ x, long long n
   }
 }
 
-__global__ void upsample2x_f32_kernel(const float4* __restrict__ x, int T, int H, int W, int cv,
-                                      uint2* __restrict__ y) {
-  const long long total = (long long)T * (2 * H) * (2 * W) * cv;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    long long r = i;
-    const int c = (int)(r % cv);
-    r /= cv;
-    const int xo = (int)(r % (2 * W));
-    r /= (2 * W);
-    const int yo = (int)(r % (2 * H));
-    const int t = (int)(r / (2 * H));
-    const float4 f = x[(((long long)t * H + (yo >> 1)) * W + (xo >> 1)) * cv + c];
-    y[i] = make_uint2(pack_bf16(f.x, f.y), pack_bf16(f.z, f.w));
+// fp32 -> bf16 variant of upsample2x_kernel (one float4 read, four 8-byte writes).
+__global__ void upsample2x_f32_kernel(const float4* __restrict__ x, int H, int W, int cv, uint2* __restrict__ y) {
+  const long long ty = blockIdx.y;
+  const int yi = (int)(ty % H);
+  const long long t = ty / H;
+  const int n = W * cv;
+  const float4* xr = x + ty * n;
+  const long long orow = 2LL * W * cv;
+  uint2* y0 = y + ((t * (2 * H) + 2 * yi) * orow);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int xi = i / cv, c = i - xi * cv;
+    const float4 f = xr[i];
+    const uint2 v = make_uint2(pack_bf16(f.x, f.y), pack_bf16(f.z, f.w));
+    const long long o = 2LL * xi * cv + c;
+    y0[o] = v;
+    y0[o + cv] = v;
+    y0[orow + o] = v;
+    y0[orow + o + cv] = v;
   }
 }
 }  // namespace ftb
@@ -193,10 +204,11 @@ extern "C" int ftb_rmsnorm_silu_f32(const float* x, int64_t n_pix, int32_t C, co
 extern "C" int ftb_upsample2x_f32_bf16(const float* x, int32_t T, int32_t H, int32_t W, int32_t C, void* y,
                                        void* stream) {
   if (!x || !y || (C % 4)) return set_error(FTB_EINVAL, "upsample2x_f32: bad arguments");
-  const long long total = (long long)T * 4 * H * W * (C / 4);
-  if (total <= 0) return FTB_OK;
-  long long blocks = (total + 255) / 256, cap = (long long)sm_count() * 8;
-  upsample2x_f32_kernel<<<(int)(blocks < cap ? blocks : cap), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      (const float4*)x, T, H, W, C / 4, (uint2*)y);
+  if ((long long)T * H * W <= 0) return FTB_OK;
+  if ((long long)T * H > 65535) return set_error(FTB_EINVAL, "upsample2x_f32: T * H > 65535");
+  const int n = W * (C / 4);
+  dim3 grid((unsigned)((n + 255) / 256), (unsigned)((long long)T * H));
+  upsample2x_f32_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>((const float4*)x, H, W, C / 4,
+                                                                                  (uint2*)y);
   return check_launch("upsample2x_f32_kernel");
 }

@@ -191,14 +191,19 @@ class DeviceDenoiser:
         if self.fold:
             self.J = round8(self.n_cond)
             HJ = cfg.heads * self.J
-            self.buf["xat"] = torch.empty(cfg.layers, HJ, m, dtype=bf, device=d)
-            self.buf["xbt"] = torch.empty(cfg.layers, m, HJ, dtype=bf, device=d)
-            self.buf["xs"] = torch.empty(Ls, HJ, dtype=f32, device=d)
-            self.buf["xp"] = torch.empty(Ls, HJ, dtype=bf, device=d)
-            # tensor-core fold (default): block-diagonal K / V operands, zero off the diagonal
+            # tensor-core fold (default): block-diagonal K / V operands, zero off the diagonal;
+            # At rows in the SEG_SOFTMAX tile order, so the logits GEMM's epilogue does the
+            # per-head softmax (no fp32 logits round trip, no separate softmax pass)
             self.fold_tc = fold_tc and m % 8 == 0
+            spt = 256 // self.J
+            at_rows = (cfg.heads + spt - 1) // spt * 256 if self.fold_tc else HJ
+            self.buf["xat"] = torch.zeros(cfg.layers, at_rows, m, dtype=bf, device=d)
+            self.buf["xbt"] = torch.empty(cfg.layers, m, HJ, dtype=bf, device=d)
+            if not self.fold_tc:
+                self.buf["xs"] = torch.empty(Ls, HJ, dtype=f32, device=d)
+            self.buf["xp"] = torch.empty(Ls, HJ, dtype=bf, device=d)
             if self.fold_tc:
-                self.buf["xkbd"] = torch.zeros(HJ, m, dtype=bf, device=d)
+                self.buf["xkbd"] = torch.zeros(at_rows, m, dtype=bf, device=d)
                 self.buf["xvbd"] = torch.zeros(HJ, m, dtype=bf, device=d)
         self.peer = g > 1 and getattr(self.comm, "peer", False)
         if self.peer:
@@ -310,7 +315,7 @@ class DeviceDenoiser:
                 # GEMMs over the zero-padded block-diagonal operands (40x the algebraic FLOPs,
                 # still ~2x faster than the CUDA-core fold)
                 ops.xattn_blockdiag(B["ckv"][i], B["xkbd"], B["xvbd"], self.n_cond, cfg.heads, cfg.head_dim, self.J,
-                                    self.scale, stream=self.stream)
+                                    self.scale, k_tiled=True, stream=self.stream)
                 fl = 2.0 * cfg.heads * self.J * cfg.head_dim * cfg.model_dim   # non-zero blocks only
                 ops.gemm(B["xkbd"], W.cross_wq_io(i), B["xat"][i], "bf16", stream=self.stream, algo_flops=fl)
                 ops.gemm(W.mats["layers.%d.cross.wo" % i][0], B["xvbd"], B["xbt"][i], "bf16", stream=self.stream,
@@ -388,8 +393,11 @@ class DeviceDenoiser:
                 ops.gemm(o_in.pop("a"), W.mats[p + "self.wo"][0], h, "resid_f32", stream=s, **o_in)
             ops.norm_modulate(h, u, gamma=W.vecs[p + "ln2.g"], beta=W.vecs[p + "ln2.b"], stream=s)
             if self.fold:   # S = U.At^T (f32) -> per-head softmax -> h += P.Bt^T
-                ops.gemm(u, B["xat"][i], B["xs"], "f32", stream=s)
-                ops.xattn_softmax(B["xs"], B["xp"], H_, self.J, self.n_cond, stream=s)
+                if self.fold_tc:   # logits GEMM with the per-head softmax in its epilogue
+                    ops.xattn_logits_softmax(u, B["xat"][i], B["xp"], H_, self.J, self.n_cond, stream=s)
+                else:
+                    ops.gemm(u, B["xat"][i], B["xs"], "f32", stream=s)
+                    ops.xattn_softmax(B["xs"], B["xp"], H_, self.J, self.n_cond, stream=s)
                 ops.gemm(B["xp"], B["xbt"][i], h, "resid_f32", stream=s)
             else:
                 ops.gemm(u, W.mats[p + "cross.wq"][0], qkv[:, 0:m], "bf16", stream=s)

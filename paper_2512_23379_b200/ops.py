@@ -41,7 +41,8 @@ class _Prof:
 
 
 KINDS = {"bf16": A.EPI_BF16, "gelu_bf16": A.EPI_GELU_BF16, "f32": A.EPI_F32,
-         "resid_f32": A.EPI_RESID_F32, "rowadd_f32": A.EPI_ROWADD_F32, "qkv_rope": A.EPI_QKV_ROPE}
+         "resid_f32": A.EPI_RESID_F32, "rowadd_f32": A.EPI_ROWADD_F32, "qkv_rope": A.EPI_QKV_ROPE,
+         "seg_softmax": A.EPI_SEG_SOFTMAX}
 
 
 def _ld(t):
@@ -85,7 +86,7 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
         raise ConfigError("gemm: K mismatch %d vs %d" % (K, Kw))
     k = KINDS[kind]
     ldc = 0 if k == A.EPI_QKV_ROPE else _ld(out)
-    if k in (A.EPI_BF16, A.EPI_GELU_BF16, A.EPI_QKV_ROPE):
+    if k in (A.EPI_BF16, A.EPI_GELU_BF16, A.EPI_QKV_ROPE, A.EPI_SEG_SOFTMAX):
         _need(out, torch.bfloat16, "out")
     else:
         _need(out, torch.float32, "out")
@@ -239,15 +240,41 @@ def xattn_fold(kv, wq_t, wo_t, at, bt, n_cond, heads, head_dim, J, scale, *, str
                _ld(wo_t), m, float(scale), A.ptr(at), A.ptr(bt), A.stream_ptr(stream))
 
 
-def xattn_blockdiag(kv, kbd, vbd, n_cond, heads, head_dim, J, scale, *, stream=None):
+def xattn_blockdiag(kv, kbd, vbd, n_cond, heads, head_dim, J, scale, *, k_tiled=False, stream=None):
     """Diagonal blocks of the tensor-core fold operands (elementwise.cu): kbd[(h,j)][h*hd+d] =
-    scale * K[j][h*hd+d], vbd likewise from V; the rest of kbd / vbd must already be zero."""
+    scale * K[j][h*hd+d], vbd likewise from V; the rest of kbd / vbd must already be zero.
+    k_tiled: kbd rows in the SEG_SOFTMAX tile order (tiled_seg_rows)."""
     for t, nm in ((kv, "kv"), (kbd, "kbd"), (vbd, "vbd")):
         _need(t, torch.bfloat16, nm)
-    if kbd.shape != vbd.shape or kbd.stride(0) != vbd.stride(0) or kbd.shape[0] < heads * J:
-        raise ConfigError("xattn_blockdiag: kbd / vbd must be [heads*J][m] with one row stride")
+    spt = 256 // J if k_tiled else 0
+    need_k = (heads + spt - 1) // spt * 256 if k_tiled else heads * J
+    if kbd.shape[1] != vbd.shape[1] or kbd.stride(0) != vbd.stride(0) or kbd.shape[0] < need_k or \
+            vbd.shape[0] < heads * J:
+        raise ConfigError("xattn_blockdiag: kbd / vbd must be [rows][m] with one row stride")
     A.call("ftb_xattn_blockdiag", A.ptr(kv), _ld(kv), n_cond, heads, head_dim, J, float(scale), A.ptr(kbd),
-           A.ptr(vbd), _ld(kbd), A.stream_ptr(stream))
+           A.ptr(vbd), _ld(kbd), spt, A.stream_ptr(stream))
+
+
+def xattn_logits_softmax(u, at_tiled, p, heads, J, n_cond, *, M=None, stream=None):
+    """Folded cross-attention logits with the per-head softmax fused into the GEMM epilogue:
+    p[r][h*J + j] = softmax_j<n_cond((u . at^T)[r][h*J + j]). at_tiled holds the rows of at in
+    the epilogue's tile layout (tiled_seg_rows): 256 // J heads per 256-row tile, padded."""
+    spt = 256 // J
+    n_pad = (heads + spt - 1) // spt * 256
+    if at_tiled.shape[0] != n_pad:
+        raise ConfigError("xattn_logits_softmax: at_tiled must have %d rows" % n_pad)
+    return gemm(u, at_tiled, p, "seg_softmax", heads=heads, head_dim=J, heads_per_rank=n_cond, M=M,
+                K=at_tiled.shape[1] if M is not None else None, lda=u.stride(0) if M is not None else None,
+                stream=stream, algo_flops=2.0 * (u.shape[0] if M is None else M) * heads * J * at_tiled.shape[1])
+
+
+def tiled_seg_rows(heads, J):
+    """Row of the padded tile layout for each (head, j): head h -> tile h // (256 // J), slot
+    h % (256 // J), row tile * 256 + slot * J + j (the SEG_SOFTMAX epilogue's column order)."""
+    spt = 256 // J
+    h = torch.arange(heads).repeat_interleave(J)
+    j = torch.arange(J).repeat(heads)
+    return (h // spt) * 256 + (h % spt) * J + j
 
 
 def xattn_softmax(s, p, heads, J, n_cond, *, stream=None):

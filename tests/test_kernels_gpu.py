@@ -132,6 +132,26 @@ def test_gemm_few_rows(ops, cuda, M, N, K):
     assert rel(out.float(), a.float() @ w.float().t()) < 5e-3
 
 
+@pytest.mark.parametrize("M,heads,J,n_cond,K", [(700, 13, 40, 37, 256), (100, 40, 40, 37, 128), (300, 7, 48, 48, 64),
+                                                 (513, 3, 8, 5, 512)])
+def test_seg_softmax_epilogue_matches_two_pass(ops, cuda, M, heads, J, n_cond, K):
+    """Logits GEMM with the per-head softmax in its epilogue == fp32 logits GEMM followed by
+    xattn_softmax, bit for bit (pair kernel at M >= 256, single-CTA tiles below)."""
+    g = torch.Generator().manual_seed(M + J)
+    u = bf(torch.randn(M, K, generator=g)).to(cuda)
+    at = bf(torch.randn(heads * J, K, generator=g) / math.sqrt(K) * 4).to(cuda)
+    s = torch.empty(M, heads * J, device=cuda)
+    ops.gemm(u, at, s, "f32")
+    p_ref = torch.empty(M, heads * J, device=cuda, dtype=torch.bfloat16)
+    ops.xattn_softmax(s, p_ref, heads, J, n_cond)
+    spt = 256 // J
+    at_t = torch.zeros((heads + spt - 1) // spt * 256, K, device=cuda, dtype=torch.bfloat16)
+    at_t[ops.tiled_seg_rows(heads, J).to(cuda)] = at
+    p = torch.full((M, heads * J), float("nan"), device=cuda, dtype=torch.bfloat16)
+    ops.xattn_logits_softmax(u, at_t, p, heads, J, n_cond)
+    assert torch.equal(p, p_ref)
+
+
 def test_gemm_chunked_a(ops, cuda):
     """Ulysses gather layout: A's K dim arrives as g head-group slices."""
     g = torch.Generator().manual_seed(9)

@@ -137,7 +137,11 @@ def test_wan_folded_cross_attention_matches_projections(cuda):
         args = [torch.as_tensor(x[k], dtype=torch.float32, device=cuda) for k in ("motion", "z", "ref")]
         outs.append(d.tokens_to_frames(d.step(*args, fv)).double().cpu().numpy())
         if fold:
-            folds.append((d.buf["xat"].float().clone(), d.buf["xbt"].float().clone()))
+            at = d.buf["xat"].float()
+            if tc:   # At rows are stored in the SEG_SOFTMAX tile order
+                from paper_2512_23379_b200 import ops
+                at = at[:, ops.tiled_seg_rows(cfg.heads, d.J).to(at.device)]
+            folds.append((at.clone(), d.buf["xbt"].float().clone()))
     assert rel(outs[0], outs[1]) < 5e-3
     assert rel(outs[2], outs[1]) < 5e-3
     # tensor-core fold (block-diagonal GEMMs) == CUDA-core fold kernel, operand for operand

@@ -95,6 +95,12 @@ def test_rmsnorm_and_upsample(cuda):
     up = torch.empty(2, 6, 10, 96, dtype=torch.bfloat16, device=cuda)
     A.call("ftb_upsample2x_bf16", A.ptr(xd), 2, 3, 5, 96, A.ptr(up), A.stream_ptr())
     assert np.array_equal(up.float().cpu().numpy(), x.repeat(2, 1).repeat(2, 2))
+    # fp32 input -> bf16 output, wider rows (several blocks per row)
+    xf = r.standard_normal((3, 4, 700, 12)).astype(np.float32)
+    upf = torch.empty(3, 8, 1400, 12, dtype=torch.bfloat16, device=cuda)
+    A.call("ftb_upsample2x_f32_bf16", A.ptr(torch.as_tensor(xf).to(cuda)), 3, 4, 700, 12, A.ptr(upf), A.stream_ptr())
+    want = torch.as_tensor(xf.repeat(2, 1).repeat(2, 2)).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(upf.float().cpu().numpy(), want)
 
 
 SMALL = dict(z_dim=16, base_dim=32, dim_mult=(1, 2, 4, 4), num_res_blocks=2, temporal_upsample=(True, True, False))
