@@ -863,6 +863,226 @@ static int launch_conv_dxr_pair(const void* in, int T_in, const void* w_t, const
   return check_launch("conv_dxr_pair_kernel");
 }
 
+// Vertical-reuse pair kernel (Cout 96, BK 32, 3x3 spatial taps): a CTA's two 128-pixel
+// M-subtiles are vertically adjacent output rows (y0, y0+1) of one x range, so a stage
+// (dt, channel block) stages the 4 input rows y0-1 .. y0+2 once (instead of 3 rows per
+// subtile) plus all 9 (dy, dx) weight taps, and subtile s reads input row s + dy for tap dy.
+// Operand bytes through the L2->SM fabric per output pixel drop from 3 A rows + half a weight
+// set to 2 A rows + half a weight set (the 96-channel convs are bound by that feed).
+template <int BN, int BK>
+struct DxrVertCfg {
+  static constexpr int ROW = BK * 2;
+  static constexpr int A_BYTES = (DXR_AROWS * ROW + 1023) / 1024 * 1024;
+  static constexpr int B_TAP = (BN / 2) * ROW;
+  static constexpr int STAGE_BYTES = 4 * A_BYTES + 9 * B_TAP;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (4 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 4u;
+  static constexpr uint32_t SBO = 8 * ROW;
+};
+
+template <int BN, int BK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    conv_dxr_vert_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmTop, const __grid_constant__ CUtensorMap tmBot,
+                         const ConvParams p) {
+  using C = DxrVertCfg<BN, BK>;
+  static_assert(C::STAGES >= 2, "stage ring");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + C::STAGES;
+  uint64_t* tfull_bar = empty_bar + C::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int num_xp = (p.num_xt + 1) / 2;      // x-tile pairs (CTA rank r takes x tile 2*xp + r)
+  const int num_yy = (p.H + 1) / 2;           // output row pairs (subtile s takes row 2*yy + s)
+  const int num_n = (p.Cout + BN - 1) / BN;
+  const int num_tiles = num_xp * p.T * num_yy * num_n;
+  const int num_kb = p.KT * p.kb_per_tap;     // stages per tile: (dt, channel block)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto decode = [&](int tile, int& xt, int& t, int& yy, int& n_blk) {
+    n_blk = tile % num_n;
+    int r = tile / num_n;
+    const int xp = r % num_xp;
+    r /= num_xp;
+    t = r % p.T;
+    yy = r / p.T;
+    xt = 2 * xp + (int)rank;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        int xt, t, yy, n_blk;
+        decode(tile, xt, t, yy, n_blk);
+        xt = min(xt, p.num_xt - 1);  // odd x-tile count: the spare CTA recomputes (not stored)
+        const int y0 = 2 * yy;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int dt = kb / p.kb_per_tap, cb = kb - dt * p.kb_per_tap;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + 4 * C::A_BYTES;
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * (4 * DXR_AROWS * C::ROW + 9 * C::B_TAP));
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int row = y0 - 1 + i;
+            uint8_t* dst = sa + i * C::A_BYTES;
+            if (p.halo && row < 0)
+              tma_load_4d_pair(dst, &tmTop, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
+            else if (p.halo && row >= p.H)
+              tma_load_4d_pair(dst, &tmBot, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
+            else
+              tma_load_4d_pair(dst, &tmA, &full_bar[stage], cb * BK, xt * 128 - 1, row, t + dt + p.t0);
+          }
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap)   // (dy, dx)
+            tma_load_2d_pair(sb + tap * C::B_TAP, &tmB, &full_bar[stage], (dt * 9 + tap) * p.Cin + cb * BK,
+                             n_blk * BN + (int)rank * (BN / 2));
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      __syncwarp();
+      constexpr uint32_t idesc = idesc_bf16(256, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * 2 * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + 4 * C::A_BYTES;
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub)
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  mma_bf16_ss_pair_elect(tmem_d + sub * BN,
+                                         sdesc(sa + (sub + dy) * C::A_BYTES + dx * C::ROW + k * 32, 16, C::SBO, C::LAYOUT),
+                                         sdesc(sb + (dy * 3 + dx) * C::B_TAP + k * 32, 16, C::SBO, C::LAYOUT), idesc,
+                                         (kb | dy | dx | k) ? 1u : 0u);
+          mma_commit_pair_elect(&empty_bar[stage], 0x3);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair_elect(&tfull_bar[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int eg = (warp - 4) >> 2;
+    int it = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+      if ((it & 1) != eg) continue;
+      int xt, t, yy, n_blk;
+      decode(tile, xt, t, yy, n_blk);
+      const int acc = it & 1;
+      mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int sub = 0; sub < 2; ++sub) {
+        const int y = 2 * yy + sub;
+        // spare x tile or a row past an odd H: drain without storing (x out of range)
+        const int x = (xt < p.num_xt && y < p.H) ? xt * 128 + q * 32 + lane : p.W;
+        conv_epilogue_tile<BN>(p, tmem_base + ((uint32_t)(q * 32) << 16) + (acc * 2 + sub) * BN, n_blk, t,
+                               min(y, p.H - 1), x);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+}
+
+template <int BN, int BK>
+static int launch_conv_dxr_vert(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s,
+                                const void* halo_top = nullptr, const void* halo_bot = nullptr) {
+  using C = DxrVertCfg<BN, BK>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(conv_dxr_vert_kernel<BN, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e, "conv_dxr_vert smem attribute");
+    configured = true;
+  }
+  CUtensorMap ta, tb;
+  {
+    uint64_t dims[4] = {(uint64_t)p.Cin, (uint64_t)p.W, (uint64_t)p.H, (uint64_t)T_in};
+    uint64_t strides[3] = {(uint64_t)p.Cin * 2, (uint64_t)p.W * p.Cin * 2, (uint64_t)p.H * p.W * p.Cin * 2};
+    uint32_t box[4] = {BK, DXR_AROWS, 1, 1};
+    int rc = make_tmap_bf16(&ta, in, 4, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  {
+    const long long ktot = (long long)p.taps * p.Cin;
+    uint64_t dims[2] = {(uint64_t)ktot, (uint64_t)p.Cout};
+    uint64_t strides[1] = {(uint64_t)ktot * 2};
+    uint32_t box[2] = {BK, BN / 2};
+    int rc = make_tmap_bf16(&tb, w_t, 2, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  CUtensorMap ttop = ta, tbot = ta;
+  if (p.halo) {
+    uint64_t dims[4] = {(uint64_t)p.Cin, (uint64_t)p.W, 1, (uint64_t)T_in};
+    uint64_t strides[3] = {(uint64_t)p.Cin * 2, (uint64_t)p.W * p.Cin * 2, (uint64_t)p.W * p.Cin * 2};
+    uint32_t box[4] = {BK, DXR_AROWS, 1, 1};
+    int rc = make_tmap_bf16(&ttop, halo_top, 4, dims, strides, box, BK * 2);
+    if (!rc) rc = make_tmap_bf16(&tbot, halo_bot, 4, dims, strides, box, BK * 2);
+    if (rc) return rc;
+  }
+  const int tiles = ((p.num_xt + 1) / 2) * p.T * ((p.H + 1) / 2) * ((p.Cout + BN - 1) / BN);
+  const int max_pairs = sm_count() / 2;
+  const int pairs = tiles < max_pairs ? tiles : max_pairs;
+  conv_dxr_vert_kernel<BN, BK><<<2 * pairs, 384, C::SMEM, s>>>(ta, tb, ttop, tbot, p);
+  return check_launch("conv_dxr_vert_kernel");
+}
+
 }  // namespace ftb
 
 using namespace ftb;
@@ -950,6 +1170,9 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
         return launch_conv_dxr_pair<192, 64>(in, T_in, w_t, p, s0, ht, hb);
       }
       p.kb_per_tap = Cin / 32;
+      if (Cout == 96 && g_conv_variant != 2)   // vertical row reuse (variant 2 keeps two x-subtiles)
+        return msub ? launch_conv_dxr_vert<96, 32>(in, T_in, w_t, p, s0, ht, hb)
+                    : launch_conv_dxr_pair<96, 32>(in, T_in, w_t, p, s0, ht, hb);
       if (Cout == 96)
         return msub ? launch_conv_dxr_pair<96, 32, 2>(in, T_in, w_t, p, s0, ht, hb)
                     : launch_conv_dxr_pair<96, 32>(in, T_in, w_t, p, s0, ht, hb);

@@ -30,6 +30,7 @@ CONV_CASES = [  # T_out, H, W, Cin, Cout, k
     (2, 4, 90, 128, 192, (1, 3, 3)),
     (2, 3, 33, 384, 384, (3, 3, 3)),
     (1, 3, 130, 96, 96, (3, 3, 3)),      # 6 m-tiles: ragged for the two-subtile pair kernel
+    (2, 5, 260, 96, 96, (1, 3, 3)),      # KT = 1, odd H and odd x-tile count (vertical-reuse spares)
 ]
 
 
@@ -53,6 +54,35 @@ def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k, variant):
     A.call("ftb_conv3d_bf16", A.ptr(xd), T + kt - 1, H, W, Cin, A.ptr(wt), Cout, *k, 0, A.ptr(bd), A.ptr(rd),
            Cout, A.ptr(out), Cout, T, 0, A.stream_ptr())
     A.call("ftb_set_conv_variant", 0)
+    assert rel(out.float().cpu().numpy(), want) < 8e-3
+
+
+@pytest.mark.parametrize("variant", [0, 2, 3, 4])
+@pytest.mark.parametrize("H,r0,r1,C", [(7, 2, 5, 96), (6, 0, 3, 96), (6, 3, 6, 96), (5, 1, 4, 192)])
+def test_conv3d_halo_rows_match_full_image(cuda, variant, H, r0, r1, C):
+    """Row slab [r0, r1) with one halo row above / below (zeros at the image border) == the
+    same rows of the unsplit conv (spatially split VAE), for every dx-reuse kernel variant."""
+    from paper_2512_23379_b200 import _capi as A
+    r = np.random.default_rng(H * 10 + r0)
+    T, W, kt = 2, 150, 3
+    x = bfr(r.standard_normal((T + kt - 1, H, W, C)))
+    w = bfr(r.standard_normal((C, C, 3, 3, 3)) / np.sqrt(C * 27))
+    b = r.standard_normal(C)
+    want = VO.conv3d(x, w, b)[:, r0:r1]
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(torch.bfloat16).to(cuda)  # noqa: E731
+    zero = np.zeros((T + kt - 1, 1, W, C))
+    top = dev(x[:, r0 - 1:r0] if r0 > 0 else zero)
+    bot = dev(x[:, r1:r1 + 1] if r1 < H else zero)
+    xd = dev(x[:, r0:r1])
+    wt = torch.as_tensor(np.transpose(w, (0, 2, 3, 4, 1)).reshape(C, -1)).to(torch.bfloat16).to(cuda).contiguous()
+    bd = torch.as_tensor(b, dtype=torch.float32).to(cuda)
+    out = torch.empty(T, r1 - r0, W, C, dtype=torch.bfloat16, device=cuda)
+    A.call("ftb_set_conv_variant", variant)
+    try:
+        A.call("ftb_conv3d_halo_bf16", A.ptr(xd), A.ptr(top), A.ptr(bot), T + kt - 1, r1 - r0, W, C, A.ptr(wt), C,
+               3, 3, 3, 0, A.ptr(bd), None, 0, A.ptr(out), C, T, 0, A.stream_ptr())
+    finally:
+        A.call("ftb_set_conv_variant", 0)
     assert rel(out.float().cpu().numpy(), want) < 8e-3
 
 
