@@ -1178,13 +1178,17 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
                     : launch_conv_dxr_pair<96, 32>(in, T_in, w_t, p, s0, ht, hb);
       return launch_conv_dxr_pair<192, 32>(in, T_in, w_t, p, s0, ht, hb);
     }
+    // Cout <= 16 (the RGB head): 16-row weight boxes; a 32-row box moved 29 zero-filled rows
+    // per tap through the L2->SM fabric (11.6 of the head conv's 27 GB)
     if (Cin % 64 == 0) {
       p.kb_per_tap = Cin / 64;
+      if (Cout <= 16) return launch_conv_dxr<16, 64>(in, T_in, w_t, p, s0, ht, hb);
       if (Cout <= 32) return launch_conv_dxr<32, 64>(in, T_in, w_t, p, s0, ht, hb);
       if (Cout <= 96) return launch_conv_dxr<96, 64>(in, T_in, w_t, p, s0, ht, hb);
       return launch_conv_dxr<192, 64>(in, T_in, w_t, p, s0, ht, hb);
     }
     p.kb_per_tap = Cin / 32;
+    if (Cout <= 16) return launch_conv_dxr<16, 32>(in, T_in, w_t, p, s0, ht, hb);
     if (Cout <= 32) return launch_conv_dxr<32, 32>(in, T_in, w_t, p, s0, ht, hb);
     if (Cout <= 96) return launch_conv_dxr<96, 32>(in, T_in, w_t, p, s0, ht, hb);
     return launch_conv_dxr<192, 32>(in, T_in, w_t, p, s0, ht, hb);

@@ -112,6 +112,24 @@ def test_conv3d_time_split_and_rgb8(cuda):
     assert np.abs(got - VO.to_rgb8(f).astype(int)).max() <= 1
 
 
+@pytest.mark.parametrize("C,W", [(96, 150), (32, 300)])
+def test_conv3d_rgb8_head_wide(cuda, C, W):
+    """RGB8 head conv (Cout 3 on 16-row weight boxes) over several x tiles, BK 32 and 64."""
+    from paper_2512_23379_b200 import _capi as A
+    r = np.random.default_rng(C + W)
+    T, H = 2, 3
+    x = bfr(r.standard_normal((T + 2, H, W, C)))
+    w3 = bfr(r.standard_normal((3, C, 3, 3, 3)) / 40)
+    f = VO.conv3d(x, w3, np.zeros(3))
+    wt3 = torch.zeros(32, 27 * C, dtype=torch.bfloat16)
+    wt3[:3] = torch.as_tensor(np.transpose(w3, (0, 2, 3, 4, 1)).reshape(3, -1)).to(torch.bfloat16)
+    rgb = torch.empty(T, H, W, 3, dtype=torch.uint8, device=cuda)
+    xd = torch.as_tensor(x).to(torch.bfloat16).to(cuda)
+    A.call("ftb_conv3d_bf16", A.ptr(xd), T + 2, H, W, C, A.ptr(wt3.to(cuda)), 3, 3, 3, 3, 0, None, None, 0,
+           A.ptr(rgb), 3, T, 2, A.stream_ptr())
+    assert np.abs(rgb.cpu().numpy().astype(int) - VO.to_rgb8(f).astype(int)).max() <= 1
+
+
 def test_rmsnorm_and_upsample(cuda):
     from paper_2512_23379_b200 import _capi as A
     r = np.random.default_rng(1)
