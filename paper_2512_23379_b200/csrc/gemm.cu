@@ -126,6 +126,7 @@ __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tm
   const int sub = lane >> 3, j = lane & 7;
   const bool resid = p.kind == FTB_EPI_RESID_F32;
   const int nch = min(WIDTH, p.N - gc_base) >> 5;  // chunks of 32 columns in this tile
+  if (nch <= 0) return;                              // warp-uniform (column half past N)
   float* out = reinterpret_cast<float*>(p.out) + (long long)(gr0 + sub) * p.ldc + gc_base + 4 * j;
   const long long step = 4 * p.ldc;
   const int rows_left = p.M - gr0 - sub;  // row 4i+sub is live while 4i < rows_left
@@ -190,11 +191,13 @@ __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tm
 // (padded columns -> 0), written bf16 at column seg * J of `out`. Same arithmetic as
 // xattn_softmax_kernel (elementwise.cu), so the fused and two-pass results agree bit for bit.
 template <int J>
-__device__ __forceinline__ void segsoftmax_tile(const GemmParams& p, uint32_t tmem_row, int gr, int n_blk) {
+__device__ __forceinline__ void segsoftmax_tile(const GemmParams& p, uint32_t tmem_row, int gr, int n_blk, int part,
+                                                int parts) {
   constexpr int SPT = 256 / J;
   const int n_cond = p.hpr;
+  const int per = (SPT + parts - 1) / parts;
 #pragma unroll 1
-  for (int s = 0; s < SPT; ++s) {
+  for (int s = part * per; s < min(SPT, (part + 1) * per); ++s) {
     const int seg = n_blk * SPT + s;
     if (seg >= p.heads) break;  // warp-uniform
     uint32_t r[J];
@@ -224,14 +227,16 @@ __device__ __forceinline__ void segsoftmax_tile(const GemmParams& p, uint32_t tm
   }
 }
 
-__device__ __forceinline__ void segsoftmax_dispatch(const GemmParams& p, uint32_t tmem_row, int gr, int n_blk) {
+// part / parts: this epilogue warpgroup's share of the tile's segments
+__device__ __forceinline__ void segsoftmax_dispatch(const GemmParams& p, uint32_t tmem_row, int gr, int n_blk,
+                                                    int part = 0, int parts = 1) {
   switch (p.head_dim) {  // J
-    case 8: segsoftmax_tile<8>(p, tmem_row, gr, n_blk); break;
-    case 16: segsoftmax_tile<16>(p, tmem_row, gr, n_blk); break;
-    case 24: segsoftmax_tile<24>(p, tmem_row, gr, n_blk); break;
-    case 32: segsoftmax_tile<32>(p, tmem_row, gr, n_blk); break;
-    case 40: segsoftmax_tile<40>(p, tmem_row, gr, n_blk); break;
-    default: segsoftmax_tile<48>(p, tmem_row, gr, n_blk); break;
+    case 8: segsoftmax_tile<8>(p, tmem_row, gr, n_blk, part, parts); break;
+    case 16: segsoftmax_tile<16>(p, tmem_row, gr, n_blk, part, parts); break;
+    case 24: segsoftmax_tile<24>(p, tmem_row, gr, n_blk, part, parts); break;
+    case 32: segsoftmax_tile<32>(p, tmem_row, gr, n_blk, part, parts); break;
+    case 40: segsoftmax_tile<40>(p, tmem_row, gr, n_blk, part, parts); break;
+    default: segsoftmax_tile<48>(p, tmem_row, gr, n_blk, part, parts); break;
   }
 }
 
@@ -570,7 +575,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+      // epilogue warps x 2 CTAs arrive (leader's copy is the one used): 4 per CTA, or all 8 when
+      // both warpgroups drain every tile (EPG=2 column split)
+      mbar_init(&tempty_bar[s], EPG == 2 ? 16 : 8);
     }
     fence_barrier_init();
   }
@@ -635,31 +642,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
-    const int eg = (warp - 4) >> 2;  // EPG=2: epilogue warpgroup eg drains accumulator eg
+    const int eg = (warp - 4) >> 2;  // epilogue warpgroup
+    // EPG=2 column split: each warpgroup drains 128 of every tile's 256 columns, so a tile's
+    // epilogue takes half as long (with two TMEM accumulators an epilogue must finish within
+    // one mainloop whichever warpgroup runs it); otherwise warpgroup eg drains accumulator eg
+    constexpr bool split = EPG == 2;
+    const int col0 = split ? eg * 128 : 0;
     int it = 0;
     for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
-      if (EPG == 2 && (it & 1) != eg) continue;
+      if (EPG == 2 && !split && (it & 1) != eg) continue;
       int m_blk, n_blk;
       pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
       const int acc = it & 1;
       const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
-      if (STAGED && p.prefetch && p.kind == FTB_EPI_RESID_F32 && gr < p.M) {
-        // pull this thread's row of h (<= 1 KB) into L2 while the tile's MMAs run, so the
-        // epilogue's h loads hit L2 (DRAM latency x the few loads in flight per warp otherwise bound it)
-        const float* hrow = reinterpret_cast<const float*>(p.out) + (long long)gr * p.ldc + n_blk * 256;
-        const uint32_t bytes = (uint32_t)min(256, p.N - n_blk * 256) * 4;
+      const int width = split ? 128 : 256;
+      const int gcb = n_blk * 256 + col0;
+      if (STAGED && p.prefetch && p.kind == FTB_EPI_RESID_F32 && gr < p.M && gcb < p.N) {
+        // pull this thread's row segment of h (<= 1 KB) into L2 while the tile's MMAs run, so
+        // the epilogue's h loads hit L2 (DRAM latency x the few loads in flight per warp otherwise bound it)
+        const float* hrow = reinterpret_cast<const float*>(p.out) + (long long)gr * p.ldc + gcb;
+        const uint32_t bytes = (uint32_t)min(width, p.N - gcb) * 4;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(hrow), "r"(bytes) : "memory");
       }
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256 + col0;
       if (STAGED) {  // host guarantees RESID_F32 / F32 (no peers), N % 32 == 0, aligned rows / gate / bias
         float4* stg = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
-        staged_tile_f32<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr - lane, n_blk * 256, stg);
+        staged_tile_f32<split ? 128 : 256>(p, trow, gr - lane, gcb, stg);
       } else if (p.kind == FTB_EPI_SEG_SOFTMAX) {
-        segsoftmax_dispatch(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk);
-      } else if (!resid_tile_pipelined<256>(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk * 256))
+        segsoftmax_dispatch(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk, split ? eg : 0,
+                            split ? 2 : 1);
+      } else if (!resid_tile_pipelined<split ? 128 : 256>(p, trow, gr, gcb))
 #pragma unroll 1
-      for (int c0 = 0; c0 < 256; c0 += 32) {
+      for (int c0 = col0; c0 < col0 + width; c0 += 32) {
         const int gc0 = n_blk * 256 + c0;
         if (gc0 >= p.N) break;
         uint32_t r[32];
