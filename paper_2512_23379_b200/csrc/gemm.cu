@@ -735,14 +735,16 @@ using namespace ftb;
 static int g_gemm_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
 static int g_gemm_staged = 1;   // pair kernel residual epilogue through smem (flag 4 turns it off)
 static int g_gemm_prefetch = 1; // ... with an L2 prefetch of the h rows (flag 8 turns it off)
+static int g_gemm_epg2_resid = 1;  // residual GEMMs: two epilogue warpgroups at every K (flag 16: K <= 2048 only)
 
 extern "C" int ftb_set_gemm_variant(int32_t v) {
-  if ((v & 3) > 2 || v < 0 || v > 14)
+  if ((v & 3) > 2 || v < 0 || v > 30)
     return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair), plus 4 = row-per-thread "
-                                 "residual epilogue, 8 = no h prefetch");
+                                 "residual epilogue, 8 = no h prefetch, 16 = one epilogue warpgroup for long-K residual GEMMs");
   g_gemm_variant = v & 3;
   g_gemm_staged = (v & 4) ? 0 : 1;
   g_gemm_prefetch = (v & 8) ? 0 : 1;
+  g_gemm_epg2_resid = (v & 16) ? 0 : 1;
   return FTB_OK;
 }
 
@@ -842,7 +844,9 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // short K: the per-tile mainloop is shorter than one epilogue warpgroup's drain -> two groups
-  const bool epg2 = K <= 2048;
+  // (+ residual GEMMs at any K: the column-split fp32 epilogue drains h in half the time; FFN2
+  // K=13824 1232-1281 -> 1408 TFLOP/s, chunk GEMM time -4.5 ms; bf16 epilogues lose at long K)
+  const bool epg2 = K <= 2048 || (g_gemm_epg2_resid && epi->kind == FTB_EPI_RESID_F32);
   if (pair) {
     auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     const bool staged = p.staged && (p.kind == FTB_EPI_RESID_F32 || (p.kind == FTB_EPI_F32 && !p.n_peers)) &&
