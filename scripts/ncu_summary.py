@@ -58,12 +58,13 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 SHAPES = {"gemm": "QKV-shape GEMM 10530x15360x5120 (bf16 epilogue)", "fmha": "self-attn L=10530, 40 heads, hd 128",
           "cross": "cross-attn Lq=10530, Lk=37, 40 heads", "conv": "VAE conv 96->96 3x3x3, 28x416x720 (fp32 out)",
           "xpb": "folded cross-attn output GEMM 10530x5120x1600 (fp32 residual + gate)",
-          "norm": "norm+AdaLN 10530x5120 f32 -> bf16"}
+          "norm": "norm+AdaLN 10530x5120 f32 -> bf16",
+          "xs": "folded cross-attn logits GEMM 10530x1792x5120 + per-head softmax epilogue (bf16 P)"}
 
 
 def full():
     res = {}
-    for w in ("gemm", "fmha", "xpb", "cross", "conv", "norm"):
+    for w in ("gemm", "fmha", "xpb", "xs", "cross", "conv", "norm"):
         rep = os.path.join(D, "full_%s_%s.ncu-rep" % (R, w))
         if not os.path.exists(rep):
             continue

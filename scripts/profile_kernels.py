@@ -1,5 +1,5 @@
 """Run each hot kernel at its 14B-shape size a few times (for ncu capture).
-usage: python scripts/profile_kernels.py [gemm|oproj|ffn2|xpb|norm|fmha|cross|conv|all]"""
+usage: python scripts/profile_kernels.py [gemm|oproj|ffn2|xpb|xs|norm|fmha|cross|conv|all]"""
 import math
 import sys
 
@@ -30,6 +30,12 @@ def main(which):
         gate = torch.randn(10, m, device=dev)
         for _ in range(3):
             ops.gemm(a, w, h, "resid_f32", group_vec=gate, rows_per_group=1170)
+    if which in ("xs", "all"):   # folded cross-attn logits GEMM with the per-head softmax epilogue
+        u = torch.randn(L, m, device=dev).to(torch.bfloat16)
+        at = (torch.randn(7 * 256, m, device=dev) / 70).to(torch.bfloat16)
+        pbuf = torch.empty(L, 40 * 40, device=dev, dtype=torch.bfloat16)
+        for _ in range(3):
+            ops.xattn_logits_softmax(u, at, pbuf, 40, 40, 37)
     if which in ("norm", "all"):
         h = torch.randn(L, m, device=dev)
         u = torch.empty(L, m, device=dev, dtype=torch.bfloat16)
