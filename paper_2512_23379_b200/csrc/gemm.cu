@@ -241,13 +241,27 @@ __device__ __forceinline__ void segsoftmax_dispatch(const GemmParams& p, uint32_
 }
 
 // Epilogue for one thread: row `gr`, 32 fp32 accumulators for columns [gc0, gc0+32).
+// Every loop over the 32 accumulators is fully unrolled with per-element predicates (no
+// data-dependent trip counts), so v[] stays in registers: a dynamic index anywhere in this
+// function puts the whole array in local memory (seen as STL/LDL on the short-K 1.3B GEMMs).
 __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int gc0, float (&v)[32]) {
   const int N = p.N;
   const bool full = (gc0 + 32 <= N);
   if (p.bias) {
+    if (full && !(reinterpret_cast<uintptr_t>(p.bias + gc0) & 15)) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (full || gc0 + j < N) v[j] += __ldg(p.bias + gc0 + j);
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + gc0) + q);
+        v[4 * q] += b.x;
+        v[4 * q + 1] += b.y;
+        v[4 * q + 2] += b.z;
+        v[4 * q + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (gc0 + j < N) v[j] += __ldg(p.bias + gc0 + j);
+    }
   }
   const long long g = (p.rows_per_group > 0) ? (gr + p.row_offset) / p.rows_per_group : 0;
   switch (p.kind) {
@@ -269,7 +283,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
           o4[q] = w;
         }
       } else {
-        for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (gc0 + j < N) o[j] = __float2bfloat16_rn(v[j]);
       }
       break;
     }
@@ -277,7 +293,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
       if (p.n_peers) {  // replicated store: the all-gather of the result rides the epilogue
         for (int r = 0; r < p.n_peers; ++r) {
           float* o = reinterpret_cast<float*>(p.peers[r]) + (long long)gr * p.ldc + gc0;
-          for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] = v[j];
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (gc0 + j < N) o[j] = v[j];
         }
         break;
       }
@@ -287,7 +305,9 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
         for (int q = 0; q < 8; ++q)
           reinterpret_cast<float4*>(o)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       } else {
-        for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] = v[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (gc0 + j < N) o[j] = v[j];
       }
       break;
     }
@@ -306,17 +326,18 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
           reinterpret_cast<float4*>(o)[q] = r;
         }
       } else {
-        for (int j = 0; j < 32 && gc0 + j < N; ++j) o[j] += (gate ? gate[j] : 1.f) * v[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (gc0 + j < N) o[j] += (gate ? gate[j] : 1.f) * v[j];
       }
       break;
     }
     case FTB_EPI_ROWADD_F32: {
       float* o = reinterpret_cast<float*>(p.out) + (long long)gr * p.ldc + gc0;
       const float* add = p.group_vec ? p.group_vec + g * p.group_ld + gc0 : nullptr;
-      for (int j = 0; j < 32; ++j) {
-        if (!full && gc0 + j >= N) break;
-        o[j] = v[j] + (add ? __ldg(add + j) : 0.f);
-      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (gc0 + j < N) o[j] = v[j] + (add ? __ldg(add + j) : 0.f);
       break;
     }
     case FTB_EPI_QKV_ROPE: {
@@ -363,26 +384,28 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int gr, int 
         }
         break;
       }
-#pragma unroll 4
+#pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        int c = gc0 + j;
-        if (c >= N) break;
-        int which = c / m;
-        int cm = c - which * m;
-        int h = cm / p.head_dim;
-        int d = cm - h * p.head_dim;
-        float x0 = v[j], x1 = v[j + 1];
-        if (which < 2 && p.has_rope) {
-          const long long ix = token * (p.head_dim >> 1) + (d >> 1);
-          const float cr = __ldg(p.rope.cos_full + ix), sr = __ldg(p.rope.sin_full + ix);
-          const float a = x0 * cr - x1 * sr;
-          x1 = x0 * sr + x1 * cr;
-          x0 = a;
+        const int c = gc0 + j;
+        if (c < N) {
+          const int which = c / m;
+          const int cm = c - which * m;
+          const int h = cm / p.head_dim;
+          const int d = cm - h * p.head_dim;
+          float x0 = v[j], x1 = v[j + 1];
+          if (which < 2 && p.has_rope) {
+            const long long ix = token * (p.head_dim >> 1) + (d >> 1);
+            const float cr = __ldg(p.rope.cos_full + ix), sr = __ldg(p.rope.sin_full + ix);
+            const float a = x0 * cr - x1 * sr;
+            x1 = x0 * sr + x1 * cr;
+            x0 = a;
+          }
+          const int dest = h / p.hpr;
+          const int hl = h - dest * p.hpr;
+          const long long idx =
+              ((long long)gr * 3 + which) * ((long long)p.hpr * p.head_dim) + (long long)hl * p.head_dim + d;
+          *reinterpret_cast<uint32_t*>(qkv_dest_block(p, base, dest) + idx) = pack_bf16(x0, x1);
         }
-        int dest = h / p.hpr;
-        int hl = h - dest * p.hpr;
-        long long idx = ((long long)gr * 3 + which) * ((long long)p.hpr * p.head_dim) + (long long)hl * p.head_dim + d;
-        *reinterpret_cast<uint32_t*>(qkv_dest_block(p, base, dest) + idx) = pack_bf16(x0, x1);
       }
       break;
     }
