@@ -120,7 +120,8 @@ int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t N,
                       void* y, int64_t ldy, float* mean_out, float* rstd_out, void* stream);
 
 /* Norm kernel variant (benchmarks): 0 auto (register-resident vector kernel when the row
- * fits), 1 generic three-pass kernel. */
+ * fits: 128 threads per row up to 2048 columns, else 256), 1 generic three-pass kernel,
+ * 3 vector kernel with 256 threads at every width, 4 with 128 threads up to 5120 columns. */
 int ftb_set_norm_variant(int32_t variant);
 
 /* ---------------------------------------------------------------- attention */

@@ -298,7 +298,25 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
   const bool vec = (N % 4 == 0) && N <= 4 * 256 * 8 && (ldx % 4 == 0) && (ldy % 4 == 0) && (!scale || mod_ld % 4 == 0) &&
                    al16(x) && (reinterpret_cast<uintptr_t>(y) & 7) == 0 && (!gamma || al16(gamma)) &&
                    (!beta || al16(beta)) && (!scale || al16(scale)) && (!shift || al16(shift)) && N >= 512;
-  if (vec && g_norm_variant != 1) {
+  const bool narrow = N <= 4 * 128 * 4 || g_norm_variant == 4;   // variant 4: 128-thread rows at any width (A/B)
+  if (vec && g_norm_variant != 1 && g_norm_variant != 3 && narrow && N <= 4 * 128 * 10 && (N / 4) % 128 == 0) {
+    // narrow rows (1.3B: m = 1536): 128 threads x 3 float4, every lane busy, twice the rows
+    // resident per SM (at 256 threads half the lanes idled in the second float4)
+    const int nv = N / 4 / 128;
+#define FTB_NORM_VEC128(V)                                                                                          \
+  norm_modulate_vec_kernel<V, 128, true><<<M, 128, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, \
+                                                                   rows_per_group, row_offset, eps,              \
+                                                                   (__nv_bfloat16*)y, ldy, mean_out, rstd_out)
+    if (nv <= 2)
+      FTB_NORM_VEC128(2);
+    else if (nv <= 3)
+      FTB_NORM_VEC128(3);
+    else if (nv <= 4)
+      FTB_NORM_VEC128(4);
+    else
+      FTB_NORM_VEC128(10);
+#undef FTB_NORM_VEC128
+  } else if (vec && g_norm_variant != 1) {
     const int nv = (N / 4 + 255) / 256;   // float4 per thread at 256 threads
 #define FTB_NORM_VEC(V)                                                                                             \
   norm_modulate_vec_kernel<V, 256, true><<<M, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, \
