@@ -449,33 +449,40 @@ static int launch_conv(const void* in, int T_in, const void* w_t, const ConvPara
 // the A-operand L2 traffic 3x. BK = 64 (SWIZZLE_128B); B holds the three taps' weights.
 constexpr int DXR_AROWS = 130;
 
-template <int BN, int BK>
+// BRES: the whole weight tensor (one N block) stays resident in smem, loaded once per CTA;
+// the ring stages only the haloed A rows (the RGB head: 16 weight rows x 27 taps x Cin).
+constexpr int DXR_BRES_MAX = 96 * 1024;
+template <int BN, int BK, bool BRES = false>
 struct DxrCfg {
   static constexpr int ROW = BK * 2;                      // bytes per pixel row of a k-block
   static constexpr int A_BYTES = (DXR_AROWS * ROW + 1023) / 1024 * 1024;
   static constexpr int B_TAP = BN * ROW;
-  static constexpr int STAGE_BYTES = A_BYTES + 3 * B_TAP;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGE_BYTES = BRES ? A_BYTES : A_BYTES + 3 * B_TAP;
+  static constexpr int RING = (200 * 1024) - (BRES ? DXR_BRES_MAX : 0);
+  static constexpr int STAGES = RING / STAGE_BYTES > 8 ? 8 : RING / STAGE_BYTES;
+  static constexpr int OFF_BRES = STAGES * STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 64) ? 64 : ((2 * BN <= 128) ? 128 : ((2 * BN <= 256) ? 256 : 512));
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + (BRES ? DXR_BRES_MAX : 0) + 1024 + 256;
   static constexpr uint32_t LAYOUT = (BK == 64) ? 2u : 4u;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr uint32_t SBO = 8 * ROW;
 };
 
 
-template <int BN, int BK>
+template <int BN, int BK, bool BRES>
 __global__ void __launch_bounds__(256, 1)
     conv_dxr_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmTop, const __grid_constant__ CUtensorMap tmBot,
                     const ConvParams p) {
-  using C = DxrCfg<BN, BK>;
+  using C = DxrCfg<BN, BK, BRES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + (BRES ? DXR_BRES_MAX : 0));
   uint64_t* empty_bar = full_bar + C::STAGES;
   uint64_t* tfull_bar = empty_bar + C::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* bres_bar = tempty_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 3);
+  uint8_t* bres = smem + C::OFF_BRES;
 
   const int warp = warp_id(), lane = lane_id();
   const int num_m = p.T * p.H * p.num_xt;
@@ -495,6 +502,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 4);
     }
+    mbar_init(bres_bar, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -505,6 +513,14 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      if (BRES) {  // all (kb, dx) weight tiles of the single N block, once
+        mbar_arrive_expect_tx(bres_bar, num_kb * 3 * C::B_TAP);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          const int r = kb / p.kb_per_tap, cb = kb - r * p.kb_per_tap;
+          for (int dx = 0; dx < 3; ++dx)
+            tma_load_2d(bres + (kb * 3 + dx) * C::B_TAP, &tmB, bres_bar, (r * 3 + dx) * p.Cin + cb * BK, 0);
+        }
+      }
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -518,7 +534,7 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], DXR_AROWS * C::ROW + 3 * C::B_TAP);
+          mbar_arrive_expect_tx(&full_bar[stage], DXR_AROWS * C::ROW + (BRES ? 0 : 3 * C::B_TAP));
           const int row = y + dy - 1;
           if (p.halo && row < 0)          // neighbour's last row (or zeros at the global edge)
             tma_load_4d(sa, &tmTop, &full_bar[stage], cb * BK, xt * 128 - 1, 0, t + dt + p.t0);
@@ -527,9 +543,10 @@ __global__ void __launch_bounds__(256, 1)
           else
             tma_load_4d(sa, &tmA, &full_bar[stage], cb * BK, xt * 128 - 1, row, t + dt + p.t0);
           const int tap0 = (dt * 3 + dy) * 3;
+          if (!BRES)
 #pragma unroll
-          for (int dx = 0; dx < 3; ++dx)
-            tma_load_2d(sb + dx * C::B_TAP, &tmB, &full_bar[stage], (tap0 + dx) * p.Cin + cb * BK, n_blk * BN);
+            for (int dx = 0; dx < 3; ++dx)
+              tma_load_2d(sb + dx * C::B_TAP, &tmB, &full_bar[stage], (tap0 + dx) * p.Cin + cb * BK, n_blk * BN);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -544,6 +561,7 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
+      if (BRES) mbar_wait(bres_bar, 0);
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
@@ -553,7 +571,7 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
-          const uint32_t sb = sa + C::A_BYTES;
+          const uint32_t sb = BRES ? smem_u32(bres) + kb * 3 * C::B_TAP : sa + C::A_BYTES;
 #pragma unroll
           for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
@@ -593,13 +611,13 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
-template <int BN, int BK>
+template <int BN, int BK, bool BRES = false>
 static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const ConvParams& p, cudaStream_t s,
                            const void* halo_top = nullptr, const void* halo_bot = nullptr) {
-  using C = DxrCfg<BN, BK>;
+  using C = DxrCfg<BN, BK, BRES>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_dxr_kernel<BN, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(conv_dxr_kernel<BN, BK, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "conv_dxr smem attribute");
     configured = true;
   }
@@ -630,7 +648,7 @@ static int launch_conv_dxr(const void* in, int T_in, const void* w_t, const Conv
     if (!rc) rc = make_tmap_bf16(&tbot, halo_bot, 4, dims, strides, box, BK * 2);
     if (rc) return rc;
   }
-  conv_dxr_kernel<BN, BK><<<grid, 256, C::SMEM, s>>>(ta, tb, ttop, tbot, p);
+  conv_dxr_kernel<BN, BK, BRES><<<grid, 256, C::SMEM, s>>>(ta, tb, ttop, tbot, p);
   return check_launch("conv_dxr_kernel");
 }
 
@@ -1182,13 +1200,19 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
     // per tap through the L2->SM fabric (11.6 of the head conv's 27 GB)
     if (Cin % 64 == 0) {
       p.kb_per_tap = Cin / 64;
-      if (Cout <= 16) return launch_conv_dxr<16, 64>(in, T_in, w_t, p, s0, ht, hb);
+      if (Cout <= 16)
+        return (long long)KT * 3 * p.kb_per_tap * 3 * 16 * 128 <= DXR_BRES_MAX
+                   ? launch_conv_dxr<16, 64, true>(in, T_in, w_t, p, s0, ht, hb)
+                   : launch_conv_dxr<16, 64>(in, T_in, w_t, p, s0, ht, hb);
       if (Cout <= 32) return launch_conv_dxr<32, 64>(in, T_in, w_t, p, s0, ht, hb);
       if (Cout <= 96) return launch_conv_dxr<96, 64>(in, T_in, w_t, p, s0, ht, hb);
       return launch_conv_dxr<192, 64>(in, T_in, w_t, p, s0, ht, hb);
     }
     p.kb_per_tap = Cin / 32;
-    if (Cout <= 16) return launch_conv_dxr<16, 32>(in, T_in, w_t, p, s0, ht, hb);
+    if (Cout <= 16)   // weights resident in smem when they fit (the RGB head: 81 KB at Cin 96)
+      return (long long)KT * 3 * p.kb_per_tap * 3 * 16 * 64 <= DXR_BRES_MAX
+                 ? launch_conv_dxr<16, 32, true>(in, T_in, w_t, p, s0, ht, hb)
+                 : launch_conv_dxr<16, 32>(in, T_in, w_t, p, s0, ht, hb);
     if (Cout <= 32) return launch_conv_dxr<32, 32>(in, T_in, w_t, p, s0, ht, hb);
     if (Cout <= 96) return launch_conv_dxr<96, 32>(in, T_in, w_t, p, s0, ht, hb);
     return launch_conv_dxr<192, 32>(in, T_in, w_t, p, s0, ht, hb);
