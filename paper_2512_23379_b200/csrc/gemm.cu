@@ -13,6 +13,10 @@
 // descriptors use SBO = 1024 B (8 rows x 128 B), K advance +32 B per UMMA_K.
 // Replaces the reference's dense_forward (backends/reference.py:17-18) and the
 // adds/activations that follow it in net.py:230-274.
+#include <algorithm>
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "ftb_internal.h"
 
@@ -41,6 +45,9 @@ struct GemmParams {
   void* peers[FTB_MAX_PEERS];
   int staged;                   // pair kernel: residual epilogue through the per-warp smem tile
   int prefetch;                 // staged residual epilogue: L2 prefetch of the tile's h rows
+  int tail_split;               // pair kernel, staged RESID: the partial last wave's tiles run as
+                                // tail_split K-slices on separate pairs (1 = off)
+  unsigned* tail_flags;         // per (tail tile, epilogue warp) slice counters, zero between launches
 };
 
 template <int BN>
@@ -121,7 +128,7 @@ __device__ __forceinline__ bool resid_tile_pipelined(const GemmParams& p, uint32
 // combined. Same arithmetic as epilogue_chunk.
 template <int WIDTH>
 __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tmem_row, int gr0, int gc_base,
-                                                float4* stg) {
+                                                float4* stg, bool add_bias = true) {
   const int lane = lane_id();
   const int sub = lane >> 3, j = lane & 7;
   const bool resid = p.kind == FTB_EPI_RESID_F32;
@@ -151,13 +158,14 @@ __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tm
                                                      __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
     __syncwarp();
     const int gc = gc_base + c * 32 + 4 * j;
-    const float4 b = p.bias ? __ldg(reinterpret_cast<const float4*>(p.bias + gc)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool use_bias = add_bias && p.bias;
+    const float4 b = use_bias ? __ldg(reinterpret_cast<const float4*>(p.bias + gc)) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int rr = 4 * i + sub, row = gr0 + rr;
       float4 a = stg[rr * 8 + (j ^ (rr & 7))];
       if (4 * i < rows_left) {
-        if (p.bias) {
+        if (use_bias) {
           a.x += b.x;
           a.y += b.y;
           a.z += b.z;
@@ -569,6 +577,40 @@ __device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int 
   n_blk = local / gm;
 }
 
+// Work items of the pair kernel. With tail_split = s > 1 the R = num_tiles % n_clusters tiles
+// of the partial last wave run as s K-slices each on s different pairs (items F + s*t + part,
+// F = num_tiles - R, all in the last round since s*R <= n_clusters). Slice `part` adds its
+// partial product into h after slice part-1 has (per epilogue warp counter), and only slice 0
+// adds the bias: h + g*(a0 + b) + g*a1 ..., fixed order, so the result is deterministic.
+struct PairItem {
+  int tile, kb0, kb1, part, slot;  // slot: tail tile index (-1 for a whole tile)
+};
+__device__ __forceinline__ PairItem pair_item(int i, int num_tiles, int n_clusters, int s, int num_kb) {
+  const int R = s > 1 ? num_tiles % n_clusters : 0;
+  const int F = num_tiles - R;
+  if (i < F) return PairItem{i, 0, num_kb, 0, -1};
+  const int t = (i - F) / s, part = (i - F) - t * s;
+  return PairItem{F + t, part * num_kb / s, (part + 1) * num_kb / s, part, t};
+}
+__device__ __forceinline__ int pair_num_items(int num_tiles, int n_clusters, int s) {
+  return s > 1 ? num_tiles + (s - 1) * (num_tiles % n_clusters) : num_tiles;
+}
+
+__device__ __forceinline__ void tail_wait(const unsigned* flag, unsigned want) {
+  if (lane_id() == 0) {
+    const long long t0 = clock64();
+    unsigned v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if (v >= want) break;
+      __nanosleep(64);
+      if (clock64() - t0 > (1LL << 33)) __trap();  // ~4 s: a lost slice would hang the box
+    }
+  }
+  __syncwarp();
+  __threadfence();
+}
+
 template <int EPG, bool STAGED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -588,6 +630,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
   const int num_n = (p.N + 255) / 256;
   const int num_tiles = num_m * num_n;
   const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
+  const int num_items = pair_num_items(num_tiles, n_clusters, p.tail_split);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -614,10 +657,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+      for (int item = cluster; item < num_items; item += n_clusters) {
+        const PairItem w = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);
         int m_blk, n_blk;
-        pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        pair_raster(w.tile, num_m, num_n, p.group_m, m_blk, n_blk);
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * PAIR_STAGE_BYTES;
           uint8_t* sb = sa + PAIR_A_BYTES;
@@ -640,12 +684,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+      for (int item = cluster; item < num_items; item += n_clusters, ++it) {
+        const PairItem w = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * 256;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * PAIR_STAGE_BYTES);
@@ -653,7 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k)
             mma_bf16_ss_pair_elect(tmem_d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
-                             (kb | k) ? 1u : 0u);
+                             (kb != w.kb0 || k) ? 1u : 0u);
           mma_commit_pair_elect(&empty_bar[stage], 0x3);
           if (++stage == PAIR_STAGES) {
             stage = 0;
@@ -672,10 +717,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
     constexpr bool split = EPG == 2;
     const int col0 = split ? eg * 128 : 0;
     int it = 0;
-    for (int tile = cluster; tile < num_tiles; tile += n_clusters, ++it) {
+    for (int item = cluster; item < num_items; item += n_clusters, ++it) {
       if (EPG == 2 && !split && (it & 1) != eg) continue;
+      const PairItem w = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);
       int m_blk, n_blk;
-      pair_raster(tile, num_m, num_n, p.group_m, m_blk, n_blk);
+      pair_raster(w.tile, num_m, num_n, p.group_m, m_blk, n_blk);
       const int acc = it & 1;
       const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
       const int width = split ? 128 : 256;
@@ -692,7 +738,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256 + col0;
       if (STAGED) {  // host guarantees RESID_F32 / F32 (no peers), N % 32 == 0, aligned rows / gate / bias
         float4* stg = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
-        staged_tile_f32<split ? 128 : 256>(p, trow, gr - lane, gcb, stg);
+        // K-slice of a tail tile: this warp's rows/columns of slice part-1 must be in h first
+        if (w.slot >= 0 && w.part > 0)
+          tail_wait(p.tail_flags + w.slot * 16 + rank * 8 + eg * 4 + q, (unsigned)w.part);
+        staged_tile_f32<split ? 128 : 256>(p, trow, gr - lane, gcb, stg, w.part == 0);
+        const PairItem w2 = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);  // cheaper than live regs
+        if (w2.slot >= 0) {
+          __threadfence();
+          __syncwarp();
+          // the last slice is the only reader left: it re-arms the counter for the next launch
+          unsigned* flag = p.tail_flags + w2.slot * 16 + rank * 8 + eg * 4 + q;
+          if (lane == 0) {
+            if (w2.part + 1 < p.tail_split) atomicAdd(flag, 1u);
+            else atomicExch(flag, 0u);
+          }
+        }
       } else if (p.kind == FTB_EPI_SEG_SOFTMAX) {
         segsoftmax_dispatch(p, tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256, gr, n_blk, split ? eg : 0,
                             split ? 2 : 1);
@@ -758,17 +818,51 @@ using namespace ftb;
 static int g_gemm_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
 static int g_gemm_staged = 1;   // pair kernel residual epilogue through smem (flag 4 turns it off)
 static int g_gemm_prefetch = 1; // ... with an L2 prefetch of the h rows (flag 8 turns it off)
+static int g_gemm_tail = 1;  // split-K tail wave for staged residual pair GEMMs (flag 32 turns it off)
 static int g_gemm_epg2_resid = 1;  // residual GEMMs: two epilogue warpgroups at every K (flag 16: K <= 2048 only)
 
 extern "C" int ftb_set_gemm_variant(int32_t v) {
-  if ((v & 3) > 2 || v < 0 || v > 30)
+  if ((v & 3) > 2 || v < 0 || v > 62)
     return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair), plus 4 = row-per-thread "
-                                 "residual epilogue, 8 = no h prefetch, 16 = one epilogue warpgroup for long-K residual GEMMs");
+                                 "residual epilogue, 8 = no h prefetch, 16 = one epilogue warpgroup for long-K residual "
+                                 "GEMMs, 32 = no split-K tail wave");
   g_gemm_variant = v & 3;
   g_gemm_staged = (v & 4) ? 0 : 1;
   g_gemm_prefetch = (v & 8) ? 0 : 1;
   g_gemm_epg2_resid = (v & 16) ? 0 : 1;
+  g_gemm_tail = (v & 32) ? 0 : 1;
   return FTB_OK;
+}
+
+// Slice counters of the split tail: one block of FTB_TAIL_SLOTS x 16 words per stream (launches
+// on one stream are ordered, so they can share a block; concurrent streams, e.g. emulated
+// ranks, must not). Statically zeroed; every launch leaves its counters at zero.
+constexpr int FTB_TAIL_SLOTS = 128;  // >= n_clusters (74 on B200)
+constexpr int FTB_TAIL_STREAMS = 64;
+__device__ unsigned g_tail_flags[FTB_TAIL_STREAMS * FTB_TAIL_SLOTS * 16];
+
+static unsigned* tail_flags_for(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, int> slot_of;
+  static std::map<int, unsigned*> base_of;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto b = base_of.find(dev);
+  if (b == base_of.end()) {
+    void* ptr = nullptr;
+    if (cudaGetSymbolAddress(&ptr, g_tail_flags) != cudaSuccess) return nullptr;
+    b = base_of.emplace(dev, static_cast<unsigned*>(ptr)).first;
+  }
+  auto key = std::make_pair(dev, stream);
+  auto it = slot_of.find(key);
+  if (it == slot_of.end()) {
+    int used = 0;
+    for (auto& kv : slot_of) used += kv.first.first == dev;
+    if (used >= FTB_TAIL_STREAMS) return nullptr;  // caller runs the tail unsplit
+    it = slot_of.emplace(key, used).first;
+  }
+  return b->second + (size_t)it->second * FTB_TAIL_SLOTS * 16;
 }
 
 static int g_gemm_group = 0;
@@ -875,6 +969,24 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
     const bool staged = p.staged && (p.kind == FTB_EPI_RESID_F32 || (p.kind == FTB_EPI_F32 && !p.n_peers)) &&
                         N % 32 == 0 && !(p.ldc & 3) && al16(p.out) &&
                         (!p.group_vec || (!(p.group_ld & 3) && al16(p.group_vec))) && (!p.bias || al16(p.bias));
+    p.tail_split = 1;
+    if (staged && g_gemm_tail && p.kind == FTB_EPI_RESID_F32) {
+      // partial last wave of R < n_clusters / 2 tiles: run them as K-slices on the idle pairs
+      // (FFN2 / O-proj at M = 10530, N = 5120: 840 tiles = 11.35 waves of 74 pairs -> 11.5)
+      const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+      const int n_clusters = std::min(tiles, sm_count() / 2);
+      const int R = tiles % n_clusters;
+      const int num_kb = (K + GEMM_BK - 1) / GEMM_BK;
+      // long K only: slice p's epilogue waits for slice p-1's, so the tail costs K/s of mainloop
+      // plus s epilogues; measured (scripts/gemm_tail_ab.py, interleaved medians) FFN2 K = 13824
+      // -3.7 %, K = 8960 -2.7 %, but K = 5120 +7 % and K <= 1600 +8..15 % (epilogue-heavy)
+      int sp = (R && num_kb >= 128) ? std::min(4, n_clusters / R) : 1;
+      while (sp > 1 && num_kb / sp < 8) --sp;
+      if (sp > 1 && n_clusters <= FTB_TAIL_SLOTS) {
+        p.tail_flags = tail_flags_for(s);
+        if (p.tail_flags) p.tail_split = sp;
+      }
+    }
     if (staged) return epg2 ? launch_gemm_pair<2, true>(ta, tb, p, s) : launch_gemm_pair<1, true>(ta, tb, p, s);
     return epg2 ? launch_gemm_pair<2, false>(ta, tb, p, s) : launch_gemm_pair<1, false>(ta, tb, p, s);
   }

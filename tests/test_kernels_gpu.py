@@ -96,7 +96,7 @@ def test_gemm_resid_staged_matches_row_per_thread(ops, cuda, M, N, K):
     gate = torch.randn(7, N, generator=g).to(cuda)
     h0 = torch.randn(M, N, generator=g).to(cuda)
     outs = []
-    for variant in (0, 6):
+    for variant in (32, 6):  # staged (no split-K tail) vs row-per-thread
         h = h0.clone()
         A.call("ftb_set_gemm_variant", variant)
         try:
@@ -119,6 +119,42 @@ def test_gemm_resid_staged_matches_row_per_thread(ops, cuda, M, N, K):
         f32.append(o)
     assert torch.equal(f32[0], f32[1])
     assert rel(f32[0], a.float() @ w.float().t() + b) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(10530, 5120, 8192),   # 840 tiles: 26-tile tail in 2 K-slices
+                                   (10530, 1536, 8960),   # 1.3B FFN2 shape: 252 tiles, 30 in 2 slices
+                                   (47 * 256 - 100, 512, 8192),  # 94 tiles: 20 in 3 slices
+                                   (46 * 256 - 7, 512, 8320)])   # 92 tiles: 18 in 4 slices
+def test_gemm_resid_split_tail(ops, cuda, M, N, K):
+    """Residual pair GEMM whose partial last wave runs as K-slices on the idle pairs: matches
+    the fp32 reference, is deterministic launch to launch (the slices add into h in a fixed
+    order, counters re-armed by each launch) and agrees with the unsplit kernel to rounding."""
+    from paper_2512_23379_b200 import _capi as A
+    g = torch.Generator().manual_seed(M + N + K)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    b = torch.randn(N, generator=g).to(cuda)
+    gate = torch.randn(28, N, generator=g).to(cuda)
+    h0 = torch.randn(M, N, generator=g).to(cuda)
+    rpg = (M + 27) // 28
+    outs = []
+    for variant in (0, 0, 0, 32):
+        h = h0.clone()
+        A.call("ftb_set_gemm_variant", variant)
+        try:
+            ops.gemm(a, w, h, "resid_f32", bias=b, group_vec=gate, rows_per_group=rpg)
+        finally:
+            A.call("ftb_set_gemm_variant", 0)
+        outs.append(h)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    grp = torch.arange(M, device=cuda) // rpg
+    ref = h0 + gate[grp] * (a.float() @ w.float().t() + b)
+    assert rel(outs[0], ref) < 1e-5
+    assert rel(outs[0], outs[3]) < 5e-6
+    # the tail tiles really were split: the last m-blocks differ from the unsplit result
+    # only by fp32 rounding of the slice sums (not bit-identical)
+    assert not torch.equal(outs[0], outs[3])
 
 
 @pytest.mark.parametrize("M,N,K", [(37, 10240, 512), (1, 5120, 16), (100, 4096, 256)])
