@@ -90,6 +90,13 @@ typedef struct ftb_epilogue {
    *  F32:      every peer_out[i] receives the full [M][ldc] result (fused all-gather). */
   int32_t n_peers;
   void* peer_out[FTB_MAX_PEERS];
+  /* Block-diagonal operand (zero-initialise for a dense GEMM): band_k > 0 declares that row r
+   * of A (band_side 0) or of B (band_side 1) is non-zero only in K columns [b*band_k,
+   * (b+1)*band_k), b = (r / band_tile) * band_per_tile + (r % band_tile) / band_rows (band_tile 0:
+   * b = r / band_rows). The CTA-pair kernel then runs each tile's K loop over the union of its
+   * rows' bands only (the skipped products are exact zeros; the folded cross-attention's
+   * At = blockdiag(K) . Wq^T and Bt = Wo^T . blockdiag(V)^T). */
+  int32_t band_side, band_rows, band_tile, band_per_tile, band_k;
 } ftb_epilogue;
 
 /* C[M,N] = A[M,K] . B[N,K]^T (bf16 in, fp32 accumulate, tcgen05 + TMEM, TMA-fed).

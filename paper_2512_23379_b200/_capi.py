@@ -30,7 +30,8 @@ class Epilogue(C.Structure):
     _fields_ = [("kind", i32), ("rows_per_group", i32), ("row_offset", i64), ("bias", vp),
                 ("group_vec", vp), ("group_ld", i64), ("out", vp), ("ldc", i64),
                 ("heads", i32), ("head_dim", i32), ("heads_per_rank", i32), ("rope", C.POINTER(Rope3D)),
-                ("n_peers", i32), ("peer_out", vp * MAX_PEERS)]
+                ("n_peers", i32), ("peer_out", vp * MAX_PEERS),
+                ("band_side", i32), ("band_rows", i32), ("band_tile", i32), ("band_per_tile", i32), ("band_k", i32)]
 
 
 class ConvNorm(C.Structure):

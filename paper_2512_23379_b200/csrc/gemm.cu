@@ -48,7 +48,27 @@ struct GemmParams {
   int tail_split;               // pair kernel, staged RESID: the partial last wave's tiles run as
                                 // tail_split K-slices on separate pairs (1 = off)
   unsigned* tail_flags;         // per (tail tile, epilogue warp) slice counters, zero between launches
+  int band_side, band_rows, band_tile, band_per_tile, band_k;  // block-diagonal operand (ftb_epilogue)
 };
+
+// K-block range of one pair tile: all of K, or (block-diagonal operand) the union of the bands
+// of the tile's rows on the banded side; products outside it are exact zeros.
+__device__ __forceinline__ void band_krange(const GemmParams& p, int m_blk, int n_blk, int num_kb, int& kb0, int& kb1) {
+  kb0 = 0;
+  kb1 = num_kb;
+  if (p.band_k <= 0) return;
+  const int r0 = (p.band_side ? n_blk : m_blk) * 256;
+  const int r1 = min(r0 + 256, p.band_side ? p.N : p.M) - 1;
+  auto band = [&](int r) {
+    return p.band_tile > 0 ? (r / p.band_tile) * p.band_per_tile + (r % p.band_tile) / p.band_rows : r / p.band_rows;
+  };
+  const long long k0 = (long long)band(r0) * p.band_k, k1 = (long long)(band(r1) + 1) * p.band_k;
+  const int a = (int)(k0 / GEMM_BK), b = (int)min((long long)num_kb, (k1 + GEMM_BK - 1) / GEMM_BK);
+  if (a < b) {
+    kb0 = a;
+    kb1 = b;
+  }
+}
 
 template <int BN>
 struct GemmCfg {
@@ -658,9 +678,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       int stage = 0;
       uint32_t phase = 0;
       for (int item = cluster; item < num_items; item += n_clusters) {
-        const PairItem w = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);
+        PairItem w = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);
         int m_blk, n_blk;
         pair_raster(w.tile, num_m, num_n, p.group_m, m_blk, n_blk);
+        if (p.band_k > 0) band_krange(p, m_blk, n_blk, num_kb, w.kb0, w.kb1);  // host: no tail split then
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * PAIR_STAGE_BYTES;
@@ -685,7 +706,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       uint32_t phase = 0;
       int it = 0;
       for (int item = cluster; item < num_items; item += n_clusters, ++it) {
-        const PairItem w = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);
+        PairItem w = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);
+        if (p.band_k > 0) {
+          int m_blk, n_blk;
+          pair_raster(w.tile, num_m, num_n, p.group_m, m_blk, n_blk);
+          band_krange(p, m_blk, n_blk, num_kb, w.kb0, w.kb1);
+        }
         const int acc = it & 1;
         mbar_wait(&tempty_bar[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -926,6 +952,16 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   p.head_dim = epi->head_dim;
   p.hpr = epi->heads_per_rank;
   p.has_rope = epi->rope != nullptr;
+  if (epi->band_k > 0) {
+    if (epi->band_rows <= 0 || epi->band_side < 0 || epi->band_side > 1 ||
+        (epi->band_tile > 0 && (epi->band_per_tile <= 0 || epi->band_tile < epi->band_rows)) || a_chunks > 1)
+      return set_error(FTB_EINVAL, "gemm: bad block-diagonal band description");
+    p.band_side = epi->band_side;
+    p.band_rows = epi->band_rows;
+    p.band_tile = epi->band_tile;
+    p.band_per_tile = epi->band_per_tile;
+    p.band_k = epi->band_k;
+  }
   if (epi->rope) p.rope = *epi->rope;
 
   const bool pair = g_gemm_variant == 2 || (g_gemm_variant == 0 && M >= 256 && N >= 256);
@@ -970,7 +1006,7 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
                         N % 32 == 0 && !(p.ldc & 3) && al16(p.out) &&
                         (!p.group_vec || (!(p.group_ld & 3) && al16(p.group_vec))) && (!p.bias || al16(p.bias));
     p.tail_split = 1;
-    if (staged && g_gemm_tail && p.kind == FTB_EPI_RESID_F32) {
+    if (staged && g_gemm_tail && p.kind == FTB_EPI_RESID_F32 && p.band_k <= 0) {
       // partial last wave of R < n_clusters / 2 tiles: run them as K-slices on the idle pairs
       // (FFN2 / O-proj at M = 10530, N = 5120: 840 tiles = 11.35 waves of 74 pairs -> 11.5)
       const int tiles = ((M + 255) / 256) * ((N + 255) / 256);

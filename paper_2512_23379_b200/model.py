@@ -141,7 +141,7 @@ class DeviceDenoiser:
     (dist.py): this rank owns tokens [start, start + Ls) of the padded chunk."""
 
     def __init__(self, weights: DeviceWeights, chunk_len, motion_len, latent_hw=(1, 1), stream=None, comm=None,
-                 fold_cross=True, fold_tc=True):
+                 fold_cross=True, fold_tc=True, fold_band=True):
         from .dist import LocalComm, ShardPlan
         cfg = weights.cfg
         self.cfg, self.w = cfg, weights
@@ -195,6 +195,7 @@ class DeviceDenoiser:
             # At rows in the SEG_SOFTMAX tile order, so the logits GEMM's epilogue does the
             # per-head softmax (no fp32 logits round trip, no separate softmax pass)
             self.fold_tc = fold_tc and m % 8 == 0
+            self.fold_band = fold_band   # K loops of the fold GEMMs over the head bands only
             spt = 256 // self.J
             at_rows = (cfg.heads + spt - 1) // spt * 256 if self.fold_tc else HJ
             self.buf["xat"] = torch.zeros(cfg.layers, at_rows, m, dtype=bf, device=d)
@@ -312,14 +313,18 @@ class DeviceDenoiser:
             ops.gemm(B["cond_bf"], W.mats["layers.%d.cross.wkv" % i][0], B["ckv"][i], "bf16", stream=self.stream)
             if self.fold and self.fold_tc:
                 # At = (scale * blockdiag K) . Wq^T and Bt = Wo^T . (blockdiag V)^T: two tensor-core
-                # GEMMs over the zero-padded block-diagonal operands (40x the algebraic FLOPs,
-                # still ~2x faster than the CUDA-core fold)
+                # GEMMs over the zero-padded block-diagonal operands; each tile's K loop covers only
+                # its rows' head bands (kbd rows in the SEG_SOFTMAX tile order: 256 // J heads per
+                # 256-row tile; vbd rows head-major, J per head)
                 ops.xattn_blockdiag(B["ckv"][i], B["xkbd"], B["xvbd"], self.n_cond, cfg.heads, cfg.head_dim, self.J,
                                     self.scale, k_tiled=True, stream=self.stream)
                 fl = 2.0 * cfg.heads * self.J * cfg.head_dim * cfg.model_dim   # non-zero blocks only
-                ops.gemm(B["xkbd"], W.cross_wq_io(i), B["xat"][i], "bf16", stream=self.stream, algo_flops=fl)
-                ops.gemm(W.mats["layers.%d.cross.wo" % i][0], B["xvbd"], B["xbt"][i], "bf16", stream=self.stream,
+                band_k = (0, self.J, 256, 256 // self.J, cfg.head_dim) if self.fold_band else None
+                band_v = (1, self.J, 0, 0, cfg.head_dim) if self.fold_band else None
+                ops.gemm(B["xkbd"], W.cross_wq_io(i), B["xat"][i], "bf16", band=band_k, stream=self.stream,
                          algo_flops=fl)
+                ops.gemm(W.mats["layers.%d.cross.wo" % i][0], B["xvbd"], B["xbt"][i], "bf16", band=band_v,
+                         stream=self.stream, algo_flops=fl)
             elif self.fold:
                 p = "layers.%d." % i
                 ops.xattn_fold(B["ckv"][i], W.mats[p + "cross.wq"][0], W.mats[p + "cross.wo"][0], B["xat"][i],

@@ -70,12 +70,14 @@ class RopeTables:
 
 def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=0, row_offset=0,
          M=None, K=None, lda=None, a_chunks=1, a_chunk_stride=0, heads=0, head_dim=0,
-         heads_per_rank=0, rope=None, peers=None, stream=None, algo_flops=None):
+         heads_per_rank=0, rope=None, peers=None, band=None, stream=None, algo_flops=None):
     """out <- epilogue(a[M,K] @ w_t[N,K]^T). `a` may be a raw buffer when
     a_chunks > 1 (Ulysses gather: M, K, lda, a_chunk_stride explicit).
     peers: device addresses (ints) for the peer-store epilogues (qkv_rope: one
     receive block per head group; f32: replicated all-gather); `out` then only
-    fixes dtype/ldc."""
+    fixes dtype/ldc.
+    band: (side, rows, tile, per_tile, k) — the A (side 0) or B (side 1) operand is block
+    diagonal (ftb_epilogue.band_*); tiles skip the K blocks outside their rows' bands."""
     _need(a, torch.bfloat16, "A")
     _need(w_t, torch.bfloat16, "W^T")
     N, Kw = w_t.shape
@@ -98,6 +100,8 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
         _need(bias, torch.float32, "bias")
     epi = A.Epilogue(k, rows_per_group, row_offset, A.ptr(bias), A.ptr(group_vec), group_ld, A.ptr(out), ldc,
                      heads, head_dim, heads_per_rank, C.pointer(rope.struct) if rope is not None else None)
+    if band is not None:
+        epi.band_side, epi.band_rows, epi.band_tile, epi.band_per_tile, epi.band_k = (int(x) for x in band)
     if peers:
         if len(peers) > A.MAX_PEERS:
             raise ConfigError("at most %d peers" % A.MAX_PEERS)

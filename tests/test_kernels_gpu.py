@@ -420,3 +420,31 @@ def test_gemm_variants(ops, cuda, variant, M, N, K):
     assert rel(h, h0 + ref) < 1e-5
     refg = 0.5 * ref * (1 + torch.tanh(math.sqrt(2 / math.pi) * (ref + 0.044715 * ref ** 3)))
     assert rel(ob.float(), refg) < 5e-3
+
+
+@pytest.mark.parametrize("heads,hd,n_cond", [(40, 128, 37), (12, 128, 37), (7, 64, 9)])
+def test_gemm_block_diagonal_band(ops, cuda, heads, hd, n_cond):
+    """Fold GEMMs over the block-diagonal K / V operands with the K-band skip (each pair tile's
+    K loop covers only its rows' head bands) == the dense K loop bit for bit (the skipped
+    products are exact zeros), and == an fp32 reference of the block-diagonal product."""
+    m, J = heads * hd, (n_cond + 7) // 8 * 8
+    spt = 256 // J
+    g = torch.Generator().manual_seed(heads * hd)
+    kv = bf(torch.randn(n_cond, 2 * m, generator=g)).to(cuda)
+    wq = bf(torch.randn(m, m, generator=g) / math.sqrt(m)).to(cuda)
+    wo = bf(torch.randn(m, m, generator=g) / math.sqrt(m)).to(cuda)
+    at_rows = (heads + spt - 1) // spt * 256
+    kbd = torch.zeros(at_rows, m, dtype=torch.bfloat16, device=cuda)
+    vbd = torch.zeros(heads * J, m, dtype=torch.bfloat16, device=cuda)
+    ops.xattn_blockdiag(kv, kbd, vbd, n_cond, heads, hd, J, 0.125, k_tiled=True)
+    res = []
+    for band in (False, True):
+        at = torch.full((at_rows, m), float("nan"), dtype=torch.bfloat16, device=cuda)
+        bt = torch.full((m, heads * J), float("nan"), dtype=torch.bfloat16, device=cuda)
+        ops.gemm(kbd, wq, at, "bf16", band=(0, J, 256, spt, hd) if band else None)
+        ops.gemm(wo, vbd, bt, "bf16", band=(1, J, 0, 0, hd) if band else None)
+        res.append((at, bt))
+    torch.cuda.synchronize()
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+    assert rel(res[1][0].float(), kbd.float() @ wq.float().t()) < 5e-3
+    assert rel(res[1][1].float(), wo.float() @ vbd.float().t()) < 5e-3
