@@ -110,7 +110,8 @@ int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_
 /* Kernel variant for ftb_gemm_bf16: 0 auto (CTA pair when M,N >= 256), 1 single CTA, 2 CTA pair;
  * adding 4 selects the row-per-thread residual epilogue of the pair kernel, adding 8 drops its L2
  * prefetch of the residual rows, adding 16 keeps long-K residual GEMMs on one epilogue
- * warpgroup (A/B benchmarks). */
+ * warpgroup, adding 32 turns off the split-K tail wave of long-K residual GEMMs (the partial
+ * last round's tiles run as ordered K-slices on the idle CTA pairs) (A/B benchmarks). */
 int ftb_set_gemm_variant(int32_t variant);
 /* CTA-pair raster group (256-row m-blocks sharing one B sweep in L2): 0 auto (A panels of
  * the group ~40 MB, at least 8), else the given count (benchmarks). */
