@@ -448,3 +448,32 @@ def test_gemm_block_diagonal_band(ops, cuda, heads, hd, n_cond):
     assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
     assert rel(res[1][0].float(), kbd.float() @ wq.float().t()) < 5e-3
     assert rel(res[1][1].float(), wo.float() @ vbd.float().t()) < 5e-3
+
+
+def test_gemm_resid_split_tail_graph_replay(ops, cuda):
+    """The split-K tail's slice counters are re-armed by every launch, so a captured launch
+    replays to the same bits as eager launches (graph replays share the stream's counter block)."""
+    M, N, K = 10530, 5120, 8192
+    g = torch.Generator().manual_seed(11)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / math.sqrt(K)).to(cuda)
+    gate = torch.randn(28, N, generator=g).to(cuda)
+    h0 = torch.randn(M, N, generator=g).to(cuda)
+    rpg = (M + 27) // 28
+    h = h0.clone()
+    ops.gemm(a, w, h, "resid_f32", group_vec=gate, rows_per_group=rpg)
+    eager = h.clone()
+    s = torch.cuda.Stream(device=cuda)
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    hg = h0.clone()
+    with torch.cuda.stream(s):
+        ops.gemm(a, w, hg, "resid_f32", group_vec=gate, rows_per_group=rpg, stream=s)  # warm-up on s
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            ops.gemm(a, w, hg, "resid_f32", group_vec=gate, rows_per_group=rpg, stream=s)
+    for _ in range(3):
+        hg.copy_(h0)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(hg, eager)
