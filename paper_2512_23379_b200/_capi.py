@@ -46,6 +46,7 @@ _SIGS = {
     "ftb_set_conv_variant": ([i32], i32),
     "ftb_set_norm_variant": ([i32], i32),
     "ftb_set_gemm_group": ([i32], i32),
+    "ftb_set_attention_variant": ([i32], i32),
     "ftb_gemm_bf16": ([vp, i64, i32, i64, vp, i64, i32, i32, i32, C.POINTER(Epilogue), vp], i32),
     "ftb_norm_modulate": ([vp, i64, i32, i32, vp, vp, vp, vp, i64, i32, i64, f32, vp, i64, vp, vp, vp], i32),
     "ftb_attention": ([vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),
@@ -137,8 +138,9 @@ def stream_ptr(stream=None):
 
 
 # Kernel-variant overrides for same-box A/B runs of bench.py (benchmarking only; the defaults
-# are the product configuration): FTB_GEMM_VARIANT / FTB_CONV_VARIANT / FTB_NORM_VARIANT.
+# are the product configuration): FTB_GEMM_VARIANT / FTB_CONV_VARIANT / FTB_NORM_VARIANT /
+# FTB_ATTN_VARIANT.
 for _env, _fn in (("FTB_GEMM_VARIANT", "ftb_set_gemm_variant"), ("FTB_CONV_VARIANT", "ftb_set_conv_variant"),
-                  ("FTB_NORM_VARIANT", "ftb_set_norm_variant")):
+                  ("FTB_NORM_VARIANT", "ftb_set_norm_variant"), ("FTB_ATTN_VARIANT", "ftb_set_attention_variant")):
     if os.environ.get(_env):
         check(getattr(lib, _fn)(int(os.environ[_env])), _env)

@@ -15,6 +15,9 @@
 //      (cross-attention over conditioning tokens, ftlk-mode 9-token chunks).
 #include <math.h>
 
+#include <map>
+#include <mutex>
+
 #include "common.cuh"
 #include "ftb_internal.h"
 
@@ -33,6 +36,12 @@ struct AttnParams {
   int n_peers;
   long long peer_rows;
   __nv_bfloat16* o_peers[FTB_MAX_PEERS];
+  // fmha2 1-D grid: item = (head, 256-query block), n_qblk blocks per head. With ws != null
+  // the items from split_first on (the partial last round) run as two CTAs each, one per half
+  // of the key blocks, storing unnormalised fp32 O + (m, l) per row into ws for
+  // fmha2_combine_kernel.
+  int n_qblk, split_first;
+  float* ws;
 };
 
 #ifdef FTB_FMHA_TIMELINE
@@ -336,8 +345,15 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int warp = warp_id(), lane = lane_id();
-  const int qblk = blockIdx.x, head = blockIdx.y;
-  const int n_kv = (p.Lk + 127) / 128;
+  int item = blockIdx.x, part = -1;  // part >= 0: this CTA runs half of the key blocks
+  if (p.ws && item >= p.split_first) {
+    part = (item - p.split_first) & 1;
+    item = p.split_first + ((item - p.split_first) >> 1);
+  }
+  const int qblk = item % p.n_qblk, head = item / p.n_qblk;
+  const int n_kv_all = (p.Lk + 127) / 128;
+  const int j0 = part == 1 ? n_kv_all / 2 : 0;                 // first global key block
+  const int n_kv = part == 0 ? n_kv_all / 2 : n_kv_all - j0;  // key blocks of this CTA (loops count locally)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -379,7 +395,7 @@ __global__ void __launch_bounds__(384, 1)
         const CUtensorMap* tm = (i & 1) ? &tmV : &tmK;
         for (int b = 0; b < C::NBOX; ++b)
           tma_load_2d(smem + C::OFF_KV + slot * C::TILE + b * C::BOX, tm, &kv_full[slot], col0 + 64 * b,
-                      (i >> 1) * 128);
+                      (j0 + (i >> 1)) * 128);
       }
     }
   } else if (warp == 1) {
@@ -463,7 +479,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
       tmem_ld_wait();
       FTB_TL(t, j, 2);
-      const int valid = p.Lk - j * 128;
+      const int valid = p.Lk - (j0 + j) * 128;  // global key block
       if (valid < 128) {
 #pragma unroll
         for (int c = 0; c < 128; ++c)
@@ -566,6 +582,21 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const int grow = qblk * 256 + t * 128 + row;
     const float inv = 1.f / l;
+    if (p.ws && (int)blockIdx.x >= p.split_first) {  // half of the keys: unnormalised O, (m_ref, l) for the combine
+      float* ws = p.ws + (size_t)(blockIdx.x - p.split_first) * (256 * HD + 512);
+      float4* wrow = reinterpret_cast<float4*>(ws + (size_t)(t * 128 + row) * HD);
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        uint32_t o[32];
+        tmem_ld32(tO + c0, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          wrow[c0 / 4 + u] = make_float4(__uint_as_float(o[4 * u]), __uint_as_float(o[4 * u + 1]),
+                                         __uint_as_float(o[4 * u + 2]), __uint_as_float(o[4 * u + 3]));
+      }
+      reinterpret_cast<float2*>(ws + 256 * HD)[t * 128 + row] = make_float2(m_ref, l);
+    } else
 #pragma unroll 1
     for (int c0 = 0; c0 < HD; c0 += 32) {
       uint32_t o[32];
@@ -1011,8 +1042,79 @@ static int launch_fmha(const AttnParams& p, cudaStream_t s) {
   return check_launch("fmha_tc_kernel");
 }
 
+// Merge the two key halves of each split item: O = (O0 2^(m0-m) + O1 2^(m1-m)) / (l0 2^(m0-m) +
+// l1 2^(m1-m)), m = max(m0, m1) (m in the kernel's log2 units), stored like fmha2's epilogue.
 template <int HD>
-static int launch_fmha2(const AttnParams& p, cudaStream_t s, bool splitp = false) {
+__global__ void __launch_bounds__(256) fmha2_combine_kernel(const AttnParams p) {
+  const int s = blockIdx.x, r = threadIdx.x;
+  const int item = p.split_first + s;
+  const int qblk = item % p.n_qblk, head = item / p.n_qblk;
+  const long long grow = (long long)qblk * 256 + r;
+  if (grow >= p.Lq) return;
+  const float* w0 = p.ws + (size_t)(2 * s) * (256 * HD + 512);
+  const float* w1 = w0 + (256 * HD + 512);
+  const float2 a = reinterpret_cast<const float2*>(w0 + 256 * HD)[r];
+  const float2 b = reinterpret_cast<const float2*>(w1 + 256 * HD)[r];
+  const float m = fmaxf(a.x, b.x);
+  const float f0 = exp2f(a.x - m), f1 = exp2f(b.x - m);
+  const float inv = 1.f / (a.y * f0 + b.y * f1);
+  const float g0 = f0 * inv, g1 = f1 * inv;
+  const float4* o0 = reinterpret_cast<const float4*>(w0 + (size_t)r * HD);
+  const float4* o1 = reinterpret_cast<const float4*>(w1 + (size_t)r * HD);
+  uint4* dst = reinterpret_cast<uint4*>(attn_out_row(p, grow) + head * HD);
+#pragma unroll 4
+  for (int c = 0; c < HD / 8; ++c) {
+    const float4 x0 = o0[2 * c], x1 = o0[2 * c + 1], y0 = o1[2 * c], y1 = o1[2 * c + 1];
+    dst[c] = make_uint4(pack_bf16(x0.x * g0 + y0.x * g1, x0.y * g0 + y0.y * g1),
+                        pack_bf16(x0.z * g0 + y0.z * g1, x0.w * g0 + y0.w * g1),
+                        pack_bf16(x1.x * g0 + y1.x * g1, x1.y * g0 + y1.y * g1),
+                        pack_bf16(x1.z * g0 + y1.z * g1, x1.w * g0 + y1.w * g1));
+  }
+}
+
+static int g_fmha_kvsplit = 0;  // KV-split tail round (ftb_set_attention_variant: 0 on, 1 off); off until measured
+
+// fp32 workspace of the KV-split tail: one pool per device, allocated on the first launch made
+// outside stream capture, split into FMHA_WS_STREAMS slots of the largest tail (2 * SMs/2 split
+// CTAs at HD 128). A slot belongs to one stream (launches on one stream are ordered; concurrent
+// streams, e.g. emulated ranks, get their own), assigned on the stream's first launch even
+// during capture, so a graph captured on a fresh stream still takes the split path. No pool or
+// no free slot: the launch runs unsplit.
+constexpr int FMHA_WS_STREAMS = 8;
+static float* fmha_ws_for(cudaStream_t stream, size_t bytes) {
+  static std::mutex mu;
+  static std::map<int, std::pair<float*, size_t>> pool_of;  // device -> (base, slot bytes)
+  static std::map<std::pair<int, cudaStream_t>, int> slot_of;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto pl = pool_of.find(dev);
+  if (pl == pool_of.end()) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    const size_t slot = (size_t)sm_count() * (256 * 128 + 512) * sizeof(float);
+    float* base = nullptr;
+    if (cudaMalloc(&base, slot * FMHA_WS_STREAMS) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    pl = pool_of.emplace(dev, std::make_pair(base, slot)).first;
+  }
+  if (bytes > pl->second.second) return nullptr;
+  auto key = std::make_pair(dev, stream);
+  auto it = slot_of.find(key);
+  if (it == slot_of.end()) {
+    int used = 0;
+    for (auto& kv : slot_of) used += kv.first.first == dev;
+    if (used >= FMHA_WS_STREAMS) return nullptr;
+    it = slot_of.emplace(key, used).first;
+  }
+  return pl->second.first + (size_t)it->second * (pl->second.second / sizeof(float));
+}
+
+template <int HD>
+static int launch_fmha2(const AttnParams& p_in, cudaStream_t s, bool splitp = false) {
+  AttnParams p = p_in;
   using C = Fmha2Cfg<HD>;
   static bool configured = false;
   if (!configured) {
@@ -1033,12 +1135,28 @@ static int launch_fmha2(const AttnParams& p, cudaStream_t s, bool splitp = false
   if ((rc = mk(&tq, p.q, p.ldq, p.Lq))) return rc;
   if ((rc = mk(&tk, p.k, p.ldk, p.Lk))) return rc;
   if ((rc = mk(&tv, p.v, p.ldv, p.Lk))) return rc;
-  dim3 grid((p.Lq + 255) / 256, p.heads);
+  // 1-D grid of (head, query block) items, query block fastest (CTAs running together share
+  // K/V in L2). The R = items % SMs items of the partial last round run as two key halves each
+  // on otherwise idle SMs when 2R <= SMs (14B: 1680 items = 11.35 rounds -> 11.5; 1.3B: 3.4 -> 3.5)
+  p.n_qblk = (p.Lq + 255) / 256;
+  const int items = p.n_qblk * p.heads;
+  const int nsm = sm_count();
+  const int R = items % nsm;
+  p.ws = nullptr;
+  p.split_first = items;
+  if (g_fmha_kvsplit && items > nsm && R > 0 && 2 * R <= nsm && (p.Lk + 127) / 128 >= 4) {
+    p.ws = fmha_ws_for(s, (size_t)2 * R * (256 * HD + 512) * sizeof(float));
+    if (p.ws) p.split_first = items - R;
+  }
+  const int grid = p.ws ? items + R : items;
   if (splitp)
     fmha2_tc_kernel<HD, true><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
   else
     fmha2_tc_kernel<HD, false><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
-  return check_launch("fmha2_tc_kernel");
+  rc = check_launch("fmha2_tc_kernel");
+  if (rc || !p.ws) return rc;
+  fmha2_combine_kernel<HD><<<R, 256, 0, s>>>(p);
+  return check_launch("fmha2_combine_kernel");
 }
 
 template <int HDMAX>
@@ -1088,6 +1206,12 @@ static int attention_run(int32_t impl, AttnParams& p, void* stream) {
 static int default_impl(int Lq, int Lk, int head_dim) {
   if ((head_dim == 64 || head_dim == 128) && Lq >= 64) return Lk <= 128 ? 3 : 0;
   return 1;
+}
+
+extern "C" int ftb_set_attention_variant(int32_t v) {
+  if (v < 0 || v > 1) return set_error(FTB_EINVAL, "attention variant: 0 default, 1 = no KV-split tail round");
+  g_fmha_kvsplit = (v & 1) ? 0 : 1;
+  return FTB_OK;
 }
 
 #ifdef FTB_FMHA_TIMELINE

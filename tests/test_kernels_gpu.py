@@ -477,3 +477,43 @@ def test_gemm_resid_split_tail_graph_replay(ops, cuda):
         graph.replay()
         torch.cuda.synchronize()
         assert torch.equal(hg, eager)
+
+
+@pytest.mark.parametrize("Lq,Lk,heads,hd", [(4000, 4000, 10, 128), (4000, 3000, 10, 64), (10530, 10530, 12, 128)])
+def test_fmha_kv_split_tail(ops, cuda, Lq, Lk, heads, hd):
+    """Flash attention whose partial last round of (head, 256-query) items runs as two key
+    halves per item plus a combine kernel: every head matches the fp32 reference, the whole
+    items are bit-identical to the unsplit launch, and the split items differ from it only by
+    rounding (so the split really ran)."""
+    from paper_2512_23379_b200 import _capi as A
+    sms = torch.cuda.get_device_properties(cuda).multi_processor_count
+    n_qblk = (Lq + 255) // 256
+    items, R = n_qblk * heads, (n_qblk * heads) % sms
+    assert items > sms and 0 < 2 * R <= sms  # the shapes are chosen to take the split path
+    g = torch.Generator().manual_seed(Lq + Lk + hd)
+    q = bf(torch.randn(Lq, heads * hd, generator=g) * 2).to(cuda)
+    k = bf(torch.randn(Lk, heads * hd, generator=g) * 2).to(cuda)
+    v = bf(torch.randn(Lk, heads * hd, generator=g)).to(cuda)
+    scale = 1 / math.sqrt(hd)
+    outs = []
+    for variant in (0, 1):
+        o = torch.full((Lq, heads * hd), float("nan"), device=cuda, dtype=torch.bfloat16)
+        A.call("ftb_set_attention_variant", variant)
+        try:
+            ops.attention(q, k, v, o, heads, hd, Lq, Lk, scale, impl=0)
+        finally:
+            A.call("ftb_set_attention_variant", 0)
+        outs.append(o)
+    torch.cuda.synchronize()
+    split, whole = outs
+    first = items - R                      # first split item: head first // n_qblk
+    h0 = first // n_qblk
+    for h in sorted({0, h0, heads - 1}):
+        cols = slice(h * hd, (h + 1) * hd)
+        want = torch_attn(q[:, cols], k[:, cols], v[:, cols], 1, hd, scale)
+        assert rel(split[:, cols].float(), want) < 1e-2, h
+    r0 = (first % n_qblk) * 256
+    assert torch.equal(split[:, :h0 * hd], whole[:, :h0 * hd])
+    assert torch.equal(split[:r0, h0 * hd:(h0 + 1) * hd], whole[:r0, h0 * hd:(h0 + 1) * hd])
+    tail = (split[:, (heads - 1) * hd:].float() - whole[:, (heads - 1) * hd:].float())
+    assert 0 < float(tail.norm() / whole[:, (heads - 1) * hd:].float().norm()) < 5e-3
