@@ -116,7 +116,7 @@ int ftb_set_gemm_variant(int32_t variant);
 /* CTA-pair raster group (256-row m-blocks sharing one B sweep in L2): 0 auto (A panels of
  * the group ~40 MB, at least 8), else the given count (benchmarks). */
 int ftb_set_gemm_group(int32_t group_m);
-/* Flash-attention variant: 0 default (the partial last round of (head, 256-query) items runs
+/* Flash-attention variant: 0 (default) the partial last round of (head, 256-query) items runs
  * as two key halves per item on the idle SMs, merged by a combine kernel; per-stream fp32
  * workspace, grown outside stream capture), 1 = every item whole (A/B benchmarks). */
 int ftb_set_attention_variant(int32_t variant);

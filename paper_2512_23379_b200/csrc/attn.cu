@@ -1072,7 +1072,7 @@ __global__ void __launch_bounds__(256) fmha2_combine_kernel(const AttnParams p) 
   }
 }
 
-static int g_fmha_kvsplit = 0;  // KV-split tail round (ftb_set_attention_variant: 0 on, 1 off); off until measured
+static int g_fmha_kvsplit = 1;  // KV-split tail round (ftb_set_attention_variant: 0 on, 1 off)
 
 // fp32 workspace of the KV-split tail: one pool per device, allocated on the first launch made
 // outside stream capture, split into FMHA_WS_STREAMS slots of the largest tail (2 * SMs/2 split
