@@ -18,7 +18,8 @@ def dims_of(base, mult):
 
 def conv3d(x, w, b):
     """x [T_in, H, W, Cin]; w (Cout, Cin, kt, kh, kw); stride 1, spatial zero pad k//2,
-    no time pad (caller supplies causal frames). Returns [T_in-kt+1, H, W, Cout]."""
+    no time pad (caller supplies causal frames). Returns [T_in-kt+1, H, W, Cout].
+    Direct sum over the taps, one float64 BLAS product (pixels, Cin) x (Cin, Cout) per tap."""
     cout, cin, kt, kh, kw = w.shape
     T_in, H, W, _ = x.shape
     ph, pw = kh // 2, kw // 2
@@ -29,7 +30,8 @@ def conv3d(x, w, b):
     for dt in range(kt):
         for dy in range(kh):
             for dx in range(kw):
-                out += np.einsum("thwc,oc->thwo", xp[dt:dt + T, dy:dy + H, dx:dx + W], w[:, :, dt, dy, dx])
+                tap = xp[dt:dt + T, dy:dy + H, dx:dx + W].reshape(-1, cin)
+                out += (tap @ w[:, :, dt, dy, dx].T).reshape(out.shape)
     return out + b
 
 

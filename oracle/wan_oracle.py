@@ -64,17 +64,56 @@ def unpatchify(tok, lc, d, h, w, ph, pw):
     return x.reshape(lc, d, h, w)
 
 
+def _head_attention(q, k, v, scale):
+    s = (q @ k.T) * scale
+    s -= s.max(axis=-1, keepdims=True)
+    np.exp(s, out=s)
+    s /= s.sum(axis=-1, keepdims=True)
+    return s @ v
+
+
 def attention(q, k, v, scale):
-    """q (Lq, H, hd), k/v (Lk, H, hd) -> (Lq, H*hd). One head at a time through BLAS
-    (an [H, Lq, Lk] score tensor is 35 GB at the 14B streaming shape)."""
-    o = np.empty((q.shape[0], q.shape[1], v.shape[2]))
-    for h in range(q.shape[1]):
-        s = (q[:, h] @ k[:, h].T) * scale
-        s -= s.max(axis=-1, keepdims=True)
-        np.exp(s, out=s)
-        s /= s.sum(axis=-1, keepdims=True)
-        o[:, h] = s @ v[:, h]
+    """q (Lq, H, hd), k/v (Lk, H, hd) -> (Lq, H*hd). Softmax with max subtraction per head
+    (backends/reference.py:84-89). One head at a time (an [H, Lq, Lk] score tensor is 35 GB at
+    the 14B streaming shape); long sequences run the heads on a thread pool with single-threaded
+    BLAS in each worker (NumPy's elementwise softmax is single-threaded, so this is ~8x faster
+    than multithreaded BLAS one head after another; the arithmetic per head is unchanged)."""
+    H = q.shape[1]
+    o = np.empty((q.shape[0], H, v.shape[2]))
+    if q.shape[0] * k.shape[0] < (1 << 22) or H == 1:
+        for h in range(H):
+            o[:, h] = _head_attention(q[:, h], k[:, h], v[:, h], scale)
+        return o.reshape(q.shape[0], -1)
+    import concurrent.futures as cf
+    import os
+
+    from threadpoolctl import threadpool_limits
+    workers = max(1, min(H, os.cpu_count() or 1, 16))
+
+    def one(h):
+        o[:, h] = _head_attention(np.ascontiguousarray(q[:, h]), np.ascontiguousarray(k[:, h]),
+                                  np.ascontiguousarray(v[:, h]), scale)
+    with threadpool_limits(limits=1, user_api="blas"), cf.ThreadPoolExecutor(workers) as ex:
+        list(ex.map(one, range(H)))
     return o.reshape(q.shape[0], -1)
+
+
+def _rows_parallel(fn, x):
+    """fn applied to row blocks of x on a thread pool (NumPy ufuncs release the GIL; the
+    arithmetic per element is fn's). Used for the elementwise GELU over (L, ff) at 14B width."""
+    import concurrent.futures as cf
+    import os
+    n = max(1, min(16, os.cpu_count() or 1))
+    if x.shape[0] < 4096 or n == 1:
+        return fn(x)
+    out = np.empty_like(x)
+    edges = np.linspace(0, x.shape[0], n + 1).astype(int)
+
+    def one(i):
+        out[edges[i]:edges[i + 1]] = fn(x[edges[i]:edges[i + 1]])
+    with cf.ThreadPoolExecutor(n) as ex:
+        list(ex.map(one, range(n)))
+    return out
 
 
 def silu(x):
@@ -133,7 +172,7 @@ def denoise(P, cfg, motion, z, reference, audio, frame_t):
         h = h + attention(cq, ck, cv, scale) @ P[p + "cross.wo"]
         xn, _, _ = layernorm(h, np.ones(m), np.zeros(m))
         u = xn * (1.0 + mt[:, 4]) + mt[:, 3]
-        f = dense(gelu(dense(u, P[p + "ffn.w1"], P[p + "ffn.b1"])), P[p + "ffn.w2"], P[p + "ffn.b2"])
+        f = dense(_rows_parallel(gelu, dense(u, P[p + "ffn.w1"], P[p + "ffn.b1"])), P[p + "ffn.w2"], P[p + "ffn.b2"])
         h = h + mt[:, 5] * f
     fm = P["final.mod"][None] + temb[:, None, :]  # (L_c, 2, m)
     ft = fm[frame_of]

@@ -19,6 +19,25 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+_PARITY = []
+
+
+@pytest.fixture
+def record_parity(request):
+    """record_parity(name, value): parity figures printed in the terminal summary (so the
+    driver's `pytest -q` log carries the measured relative L2 of the scale tests)."""
+    def rec(name, value):
+        _PARITY.append((request.node.nodeid.split("::")[-1], name, float(value)))
+    return rec
+
+
+def pytest_terminal_summary(terminalreporter):
+    if _PARITY:
+        terminalreporter.write_line("parity figures (relative L2 unless stated):")
+        for test, name, v in _PARITY:
+            terminalreporter.write_line("  %-58s %-26s %.3e" % (test, name, v))
+
+
 @pytest.fixture(scope="session")
 def golden():
     with np.load(GOLDEN, allow_pickle=False) as z:

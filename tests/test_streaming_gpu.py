@@ -40,16 +40,16 @@ def test_generate_teacher_forced_per_chunk(golden, cuda, setup):
     assert np.allclose(motions[0], np.repeat(golden["r_reference_latent"][None], 2, 0), atol=1e-6)
 
 
-def test_generate_free_running_drift(golden, cuda, setup):
+def test_generate_free_running_drift(golden, cuda, setup, record_parity):
     from paper_2512_23379_b200.config import StreamConfig
     from paper_2512_23379_b200.streaming import generate
     cfg, store, codec = setup
     tg, _, frames = generate(store, cfg, codec, golden["r_reference_latent"], golden["r_signal"], 35,
                              cfg=StreamConfig(seed=int(golden["r_seed"])))
     drift = [rel(tg[7 * c:7 * c + 7], golden["r_targets"][7 * c:7 * c + 7]) for c in range(5)]
-    print("free-running per-chunk rel-L2:", ["%.2e" % d for d in drift])
-    assert drift[0] < BUDGET
-    assert max(drift) < 5 * BUDGET
+    for c, d in enumerate(drift):
+        record_parity("free-running chunk %d" % c, d)
+    assert max(drift) < BUDGET   # the north-star budget holds across the whole 5-chunk rollout
 
 
 def _run_session(store, cfg, codec, golden, n=35, push_in=(35,)):
