@@ -476,7 +476,7 @@ def main():
                 "components_ms": comp,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk}
-        ovr = {k: os.environ[k] for k in ("FTB_GEMM_VARIANT", "FTB_CONV_VARIANT", "FTB_NORM_VARIANT", "FTB_ATTN_VARIANT")
+        ovr = {k: os.environ[k] for k in ("FTB_GEMM_VARIANT", "FTB_GEMM_GROUP", "FTB_CONV_VARIANT", "FTB_ATTN_NO_SPLIT")
                if os.environ.get(k)}
         if ovr:   # A/B run with non-default kernel variants: say so in the line
             line["config"]["kernel_overrides"] = ovr

@@ -97,7 +97,22 @@ typedef struct ftb_epilogue {
    * rows' bands only (the skipped products are exact zeros; the folded cross-attention's
    * At = blockdiag(K) . Wq^T and Bt = Wo^T . blockdiag(V)^T). */
   int32_t band_side, band_rows, band_tile, band_per_tile, band_k;
+  /* Kernel selection of this call (0 = the product defaults; A/B benchmarks and tests set it):
+   * bits 0-1: 0 auto (CTA pair when M, N >= 256), 1 single CTA, 2 CTA pair; +4 row-per-thread
+   * residual epilogue of the pair kernel (instead of the smem-staged one); +8 no L2 prefetch of
+   * the residual rows; +16 long-K residual GEMMs on one epilogue warpgroup. */
+  int32_t variant;
+  /* CTA-pair raster group (256-row m-blocks sharing one B sweep in L2): 0 auto (A panels of the
+   * group ~40 MB, at least 8). */
+  int32_t raster_group;
+  /* Split-K tail wave of long-K residual GEMMs (K >= 8192): the partial last round's tiles run
+   * as ordered K-slices on the idle CTA pairs, serialised through FTB_TAIL_COUNTER_WORDS u32
+   * counters in device memory OWNED BY THE CALLER (zero-initialised once; every launch leaves
+   * them zero). Launches sharing one counter buffer must be stream-ordered (one buffer per
+   * stream of launches, e.g. per DeviceDenoiser). NULL: the tail runs unsplit. */
+  uint32_t* tail_counters;
 } ftb_epilogue;
+#define FTB_TAIL_COUNTER_WORDS 2048
 
 /* C[M,N] = A[M,K] . B[N,K]^T (bf16 in, fp32 accumulate, tcgen05 + TMEM, TMA-fed).
  * A is read as a_chunks K-slices of width K/a_chunks: element (r,k) at
@@ -106,20 +121,6 @@ typedef struct ftb_epilogue {
 int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_stride,
                   const void* B, int64_t ldb, int32_t M, int32_t N, int32_t K,
                   const ftb_epilogue* epi, void* stream);
-
-/* Kernel variant for ftb_gemm_bf16: 0 auto (CTA pair when M,N >= 256), 1 single CTA, 2 CTA pair;
- * adding 4 selects the row-per-thread residual epilogue of the pair kernel, adding 8 drops its L2
- * prefetch of the residual rows, adding 16 keeps long-K residual GEMMs on one epilogue
- * warpgroup, adding 32 turns off the split-K tail wave of long-K residual GEMMs (the partial
- * last round's tiles run as ordered K-slices on the idle CTA pairs) (A/B benchmarks). */
-int ftb_set_gemm_variant(int32_t variant);
-/* CTA-pair raster group (256-row m-blocks sharing one B sweep in L2): 0 auto (A panels of
- * the group ~40 MB, at least 8), else the given count (benchmarks). */
-int ftb_set_gemm_group(int32_t group_m);
-/* Flash-attention variant: 0 (default) the partial last round of (head, 256-query) items runs
- * as two key halves per item on the idle SMs, merged by a combine kernel; per-stream fp32
- * workspace, grown outside stream capture), 1 = every item whole (A/B benchmarks). */
-int ftb_set_attention_variant(int32_t variant);
 
 /* ---------------------------------------------------------------- norms */
 /* y = ((x - mean) * rstd) * (gamma?gamma:1) * (scale?1+scale[g]:1) + (beta?beta:0) + (shift?shift[g]:0)
@@ -131,28 +132,32 @@ int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t N,
                       int32_t rows_per_group, int64_t row_offset, float eps,
                       void* y, int64_t ldy, float* mean_out, float* rstd_out, void* stream);
 
-/* Norm kernel variant (benchmarks): 0 auto (register-resident vector kernel when the row
- * fits: 128 threads per row up to 2048 columns, else 256), 1 generic three-pass kernel,
- * 3 vector kernel with 256 threads at every width, 4 with 128 threads up to 5120 columns. */
-int ftb_set_norm_variant(int32_t variant);
-
 /* ---------------------------------------------------------------- attention */
 /* o[r, h*hd + d] = softmax_j(q_r . k_j * scale) v_j  per head h (bidirectional, no mask
- * beyond Lk). Row r of q at q + r*ldq + h*head_dim (bf16); same for k, v, o. */
+ * beyond Lk). Row r of q at q + r*ldq + h*head_dim (bf16); same for k, v, o.
+ * workspace: optional fp32 device scratch OWNED BY THE CALLER, workspace_bytes >=
+ * ftb_attention_workspace_bytes(Lq, Lk, heads, head_dim) (0 when no split applies): the flash
+ * kernel then runs the partial last round of (head, 256-query) items as two key halves on the
+ * idle SMs plus a combine kernel. NULL or too small: every item runs whole (same results up to
+ * fp32 rounding of the merge). Launches sharing one workspace must be stream-ordered. */
 int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                   void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
-                  float scale, void* stream);
-/* Explicit kernel selection (tests / benchmarks): 0 = tcgen05 flash kernel
- * (head_dim 64|128), 1 = short-KV CUDA-core kernel (Lk <= 1024). */
+                  float scale, void* workspace, size_t workspace_bytes, void* stream);
+/* Bytes of the KV-split workspace for this shape on the current device (0: no split). */
+size_t ftb_attention_workspace_bytes(int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim);
+/* Explicit kernel selection (tests / benchmarks): 0 = tcgen05 flash kernel (head_dim 64|128),
+ * 1 = CUDA-core kernel (any head_dim <= 128), 3 = short-KV tcgen05 kernel (Lk <= 128). */
 int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk,
                        const void* v, int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk,
-                       int32_t heads, int32_t head_dim, float scale, void* stream);
+                       int32_t heads, int32_t head_dim, float scale, void* workspace, size_t workspace_bytes,
+                       void* stream);
 
 /* Ulysses all-to-all #2 fused into the epilogue: output row r is stored at row r % peer_rows
  * of o_peers[r / peer_rows] (device pointers, peer-mapped; host array of n_peers entries). */
 int ftb_attention_scatter(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                           void* const* o_peers, int32_t n_peers, int64_t peer_rows, int64_t ldo, int32_t Lq,
-                          int32_t Lk, int32_t heads, int32_t head_dim, float scale, void* stream);
+                          int32_t Lk, int32_t heads, int32_t head_dim, float scale, void* workspace,
+                          size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- peer memory (multi-GPU) */
 /* IPC-exportable zeroed device allocation / free. */
@@ -172,16 +177,8 @@ int ftb_copy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 int ftb_peer_barrier(uint32_t* const* flags, uint32_t* epoch, int32_t rank, int32_t world, double timeout_s,
                      void* stream);
 
-/* Folded cross-attention (wan mode; the cond K/V are fixed for a chunk):
- * kv [n_cond][2m] bf16 (K | V, row stride ldkv), wqT / woT the W^T [m][ld] of the cross
- * query / output projections. Writes at [heads*J][m] = scale * K_h . Wq_h^T and
- * bt [m][heads*J] = Wo_h^T . V_h^T (j >= n_cond zero), J % 8 == 0, n_cond <= J <= 48.
- * Per step: S = U . at^T (f32), ftb_xattn_softmax, h += P . bt^T (residual GEMM).
- * Replaces net.py:259-261 (cross MHA + its residual) for the wan composition. */
-int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim, int32_t J,
-                   const void* wqT, int64_t ldwq, const void* woT, int64_t ldwo, int32_t m, float scale, void* at,
-                   void* bt, void* stream);
-/* Block-diagonal operands for folding the cross-attention projections on the tensor cores
+/* Folded cross-attention (wan mode; the cond K/V are fixed for a chunk).
+ * Block-diagonal operands for folding the cross-attention projections on the tensor cores
  * (net.py:259-261 composed with the chunk's fixed cond K/V): kbd[(h,j)][h*hd+d] = scale*K[j][h*hd+d],
  * vbd[(h,j)][h*hd+d] = V[j][h*hd+d], kv = [n_cond][K | V] bf16. Only the diagonal blocks are
  * written (caller zero-fills kbd / vbd once). Then At = kbd . Wq^T and Bt = Wo^T . vbd^T are two
@@ -189,9 +186,6 @@ int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, 
  * (h % k_tile_segs) * J + j: the FTB_EPI_SEG_SOFTMAX column order for the logits GEMM. */
 int ftb_xattn_blockdiag(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim, int32_t J,
                         float scale, void* kbd, void* vbd, int64_t ld, int32_t k_tile_segs, void* stream);
-/* P[r][h*J + j] = softmax_j<n_cond(S[r][h*J + j]) (bf16, padded columns 0), per head segment. */
-int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond, void* p,
-                      int64_t ldp, void* stream);
 
 /* ---------------------------------------------------------------- elementwise */
 int ftb_gelu_bf16(const void* x, void* y, int64_t n, void* stream);
@@ -227,7 +221,10 @@ int ftb_add_bcast_f32(const float* a, int64_t F, int64_t n, const float* b, int6
  * zero padding KH/2, KW/2; output frame t reads input frames t0+t .. t0+t+KT-1 (the
  * caller keeps the causal cache frames in front). mode 0: out bf16 [T_out][H][W][out_ld]
  * = acc + bias (+ resid[pix*resid_ld + n]); mode 1: time split, channel block j of
- * Cout/2 goes to output frame 2t+j; mode 2: uint8 RGB = clamp(rint((acc+bias+1)*127.5)). */
+ * Cout/2 goes to output frame 2t+j; mode 2: uint8 RGB = clamp(rint((acc+bias+1)*127.5)).
+ * Bits 8-10 of mode select the kernel of this call (0 auto; tests / A/B benchmarks): 1 per-tap
+ * boxes, 2 dx reuse (one haloed TMA box per (dt,dy) feeds the 3 dx taps) on CTA pairs, 3 dx reuse
+ * on single CTAs, 4 CTA pairs with one 128-pixel M-subtile per CTA (auto uses two at Cout 96). */
 int ftb_conv3d_bf16(const void* in, int32_t T_in, int32_t H, int32_t W, int32_t Cin,
                     const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0,
                     const float* bias, const void* resid, int64_t resid_ld,
@@ -255,10 +252,6 @@ int ftb_conv3d_norm_bf16(const void* in, const void* halo_top, const void* halo_
                          int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW,
                          int32_t t0, const float* bias, const void* resid, int64_t resid_ld, void* out,
                          int64_t out_ld, int32_t T_out, int32_t mode, const ftb_conv_norm* norm, void* stream);
-/* Conv kernel variant: 0 auto, 1 per-tap boxes, 2 dx reuse (one haloed TMA box per (dt,dy) feeds
- * the 3 dx taps) on CTA pairs, 3 dx reuse on single CTAs, 4 CTA pairs with one 128-pixel M-subtile
- * per CTA (auto uses two at Cout 96). */
-int ftb_set_conv_variant(int32_t variant);
 /* y = [silu](x / max(||x||_2, eps) * sqrt(C) * gamma) per pixel, channel-last bf16. */
 int ftb_rmsnorm_silu_bf16(const void* x, int64_t n_pix, int32_t C, const float* gamma, float eps,
                           int32_t silu, void* y, void* stream);

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FTB_LIB") or os.path.join(HERE, "_lib", "libftb2.so")   # FTB_LIB: A/B builds
 
 FTB_OK, FTB_EINVAL, FTB_ECUDA, FTB_ENCCL, FTB_ENONFINITE = 0, 1, 2, 3, 4
-MAX_PEERS, IPC_HANDLE_BYTES = 8, 64
+MAX_PEERS, IPC_HANDLE_BYTES, TAIL_COUNTER_WORDS = 8, 64, 2048
 EPI_BF16, EPI_GELU_BF16, EPI_F32, EPI_RESID_F32, EPI_ROWADD_F32, EPI_QKV_ROPE, EPI_SEG_SOFTMAX = range(7)
 
 vp, i32, i64, f32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint64
@@ -31,7 +31,8 @@ class Epilogue(C.Structure):
                 ("group_vec", vp), ("group_ld", i64), ("out", vp), ("ldc", i64),
                 ("heads", i32), ("head_dim", i32), ("heads_per_rank", i32), ("rope", C.POINTER(Rope3D)),
                 ("n_peers", i32), ("peer_out", vp * MAX_PEERS),
-                ("band_side", i32), ("band_rows", i32), ("band_tile", i32), ("band_per_tile", i32), ("band_k", i32)]
+                ("band_side", i32), ("band_rows", i32), ("band_tile", i32), ("band_per_tile", i32), ("band_k", i32),
+                ("variant", i32), ("raster_group", i32), ("tail_counters", vp)]
 
 
 class ConvNorm(C.Structure):
@@ -42,17 +43,14 @@ _SIGS = {
     "ftb_version": ([], i32),
     "ftb_last_error": ([], C.c_char_p),
     "ftb_device_sm_count": ([i32], i32),
-    "ftb_set_gemm_variant": ([i32], i32),
-    "ftb_set_conv_variant": ([i32], i32),
-    "ftb_set_norm_variant": ([i32], i32),
-    "ftb_set_gemm_group": ([i32], i32),
-    "ftb_set_attention_variant": ([i32], i32),
     "ftb_gemm_bf16": ([vp, i64, i32, i64, vp, i64, i32, i32, i32, C.POINTER(Epilogue), vp], i32),
     "ftb_norm_modulate": ([vp, i64, i32, i32, vp, vp, vp, vp, i64, i32, i64, f32, vp, i64, vp, vp, vp], i32),
-    "ftb_attention": ([vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),
-    "ftb_attention_impl": ([i32, vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp], i32),
+    "ftb_attention": ([vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp, C.c_size_t, vp], i32),
+    "ftb_attention_workspace_bytes": ([i32, i32, i32, i32], C.c_size_t),
+    "ftb_attention_impl": ([i32, vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp, C.c_size_t, vp],
+                           i32),
     "ftb_attention_scatter": ([vp, i64, vp, i64, vp, i64, C.POINTER(vp), i32, i64, i64, i32, i32, i32, i32, f32,
-                               vp], i32),
+                               vp, C.c_size_t, vp], i32),
     "ftb_sym_alloc": ([C.c_size_t, C.POINTER(vp)], i32),
     "ftb_sym_free": ([vp], i32),
     "ftb_ipc_export": ([vp, C.c_char_p], i32),
@@ -60,8 +58,6 @@ _SIGS = {
     "ftb_ipc_close": ([vp], i32),
     "ftb_peer_barrier": ([C.POINTER(vp), vp, i32, i32, C.c_double, vp], i32),
     "ftb_copy_d2d": ([vp, vp, C.c_size_t, vp], i32),
-    "ftb_xattn_fold": ([vp, i64, i32, i32, i32, i32, vp, i64, vp, i64, i32, f32, vp, vp, vp], i32),
-    "ftb_xattn_softmax": ([vp, i64, i32, i32, i32, i32, vp, i64, vp], i32),
     "ftb_xattn_blockdiag": ([vp, i64, i32, i32, i32, i32, f32, vp, vp, i64, i32, vp], i32),
     "ftb_gelu_bf16": ([vp, vp, i64, vp], i32),
     "ftb_silu_f32_to_bf16": ([vp, vp, i64, vp], i32),
@@ -138,9 +134,10 @@ def stream_ptr(stream=None):
 
 
 # Kernel-variant overrides for same-box A/B runs of bench.py (benchmarking only; the defaults
-# are the product configuration): FTB_GEMM_VARIANT / FTB_CONV_VARIANT / FTB_NORM_VARIANT /
-# FTB_ATTN_VARIANT.
-for _env, _fn in (("FTB_GEMM_VARIANT", "ftb_set_gemm_variant"), ("FTB_CONV_VARIANT", "ftb_set_conv_variant"),
-                  ("FTB_NORM_VARIANT", "ftb_set_norm_variant"), ("FTB_ATTN_VARIANT", "ftb_set_attention_variant")):
-    if os.environ.get(_env):
-        check(getattr(lib, _fn)(int(os.environ[_env])), _env)
+# are the product configuration). They are passed PER CALL by ops.py (the library keeps no
+# variant state): FTB_GEMM_VARIANT (ftb_epilogue.variant), FTB_GEMM_GROUP (raster_group),
+# FTB_CONV_VARIANT (conv mode bits 8-10), FTB_ATTN_NO_SPLIT=1 (no KV-split workspace).
+GEMM_VARIANT = int(os.environ.get("FTB_GEMM_VARIANT", "0"))
+GEMM_GROUP = int(os.environ.get("FTB_GEMM_GROUP", "0"))
+CONV_VARIANT = int(os.environ.get("FTB_CONV_VARIANT", "0"))
+ATTN_SPLIT = os.environ.get("FTB_ATTN_NO_SPLIT", "0") != "1"

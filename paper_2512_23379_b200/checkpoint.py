@@ -134,39 +134,52 @@ def load(path):
 
 def load_device_weights(path, device="cuda"):
     """Stream a checkpoint into bf16 device weights (model.DeviceWeights) one
-    tensor at a time. Returns (DeviceWeights, role, NetConfig)."""
+    tensor at a time. Returns (DeviceWeights, role, NetConfig). A malformed file
+    raises ConfigError (the mapping is closed first)."""
+    with open(path, "rb") as f:
+        mm = mmap.mmap(f.fileno(), 0, access=mmap.ACCESS_READ)
+    failure = None
+    try:
+        return _device_weights_from(mm, path, device)
+    except BaseException as e:  # noqa: BLE001
+        # the loader's frames (kept alive by the traceback) still export views of the mapping,
+        # and mm.close() would raise BufferError over the real error: drop them first
+        e.__traceback__ = None
+        failure = e
+    finally:
+        mm.close()
+    raise failure
+
+
+def _device_weights_from(mm, path, device):
     import torch
 
     from .model import DeviceWeights, round8
-    with open(path, "rb") as f:
-        mm = mmap.mmap(f.fileno(), 0, access=mmap.ACCESS_READ)
+    view = memoryview(mm)
+    # first pass: trailer + shape validation without materialising data
+    gen = _entries(view, path)
+    shapes = []
+    while True:
         try:
-            view = memoryview(mm)
-            # first pass: trailer + shape validation without materialising data
-            gen = _entries(view, path)
-            shapes = []
-            while True:
-                try:
-                    name, arr = next(gen)
-                except StopIteration as stop:
-                    meta = stop.value
-                    break
-                shapes.append((name, arr.shape))
-                del arr
-            role, net = _check(shapes, meta)
-            w = DeviceWeights(net, device)
-            gen = _entries(view, path)
-            for name, arr in gen:
-                if arr.ndim == 2 and not name.endswith(".mod"):
-                    K, N = arr.shape
-                    wt = torch.zeros(N, round8(K), dtype=torch.bfloat16, device=w.device)
-                    wt[:, :K] = torch.from_numpy(np.array(arr.T)).to(w.device).to(torch.bfloat16)
-                    w.mats[name] = (wt, K)
-                else:
-                    w.vecs[name] = torch.from_numpy(np.array(arr)).to(torch.float32).to(w.device)
-                del arr
-            w._fuse()
-            del view, gen
-        finally:
-            mm.close()
+            name, arr = next(gen)
+        except StopIteration as stop:
+            meta = stop.value
+            break
+        shapes.append((name, arr.shape))
+        del arr
+    role, net = _check(shapes, meta)
+    w = DeviceWeights(net, device)
+    gen = _entries(view, path)
+    for name, arr in gen:
+        if arr.ndim == 2 and not name.endswith(".mod"):
+            K, N = arr.shape
+            wt = torch.zeros(N, round8(K), dtype=torch.bfloat16, device=w.device)
+            wt[:, :K] = torch.from_numpy(np.array(arr.T)).to(w.device).to(torch.bfloat16)
+            w.mats[name] = (wt, K)
+        else:
+            w.vecs[name] = torch.from_numpy(np.array(arr)).to(torch.float32).to(w.device)
+        del arr
+    w._fuse()
+    del gen
+    view.release()
     return w, role, net

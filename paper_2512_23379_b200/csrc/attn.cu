@@ -2,21 +2,13 @@
 // beyond the key length). Restates the reference's mha_forward core
 // (backends/reference.py:77-92; Cython row loop _fast.pyx:162-209).
 //
-//  (0) fmha_tc_kernel  — tcgen05 flash attention for long sequences, head_dim 64|128.
-//      One CTA = one head x 128 query rows. Warp roles:
-//        w0 TMA producer (Q once, K/V 128-key blocks, 2-stage ring)
-//        w1 MMA issuer: S_j = Q K_j^T -> TMEM (double-buffered, S_{j+1} overlaps
-//           softmax_j), O += P_j V_j -> TMEM (V consumed MN-major)
-//        w2 TMEM allocator
-//        w4-7 softmax: one thread per query row, tcgen05.ld of S, exp2 online
-//           softmax with lazy (threshold 2^8) rescaling of O in TMEM, P -> smem bf16
-//           (128B-swizzled K-major, the A operand of the PV MMA), final O / l.
+//  (0) fmha2_tc_kernel — tcgen05 flash attention for long sequences, head_dim 64|128
+//      (two 128-query tiles per CTA, P in TMEM; see the kernel's comment).
+//  (3) xattn_tc_kernel  — short-KV tcgen05 kernel (Lk <= 128, one exact key block).
 //  (1) attn_small_kernel — CUDA-core online-softmax kernel for short key sets
 //      (cross-attention over conditioning tokens, ftlk-mode 9-token chunks).
 #include <math.h>
 
-#include <map>
-#include <mutex>
 
 #include "common.cuh"
 #include "ftb_internal.h"
@@ -66,233 +58,6 @@ __device__ __forceinline__ __nv_bfloat16* attn_out_row(const AttnParams& p, long
   return p.o + row * p.ldo;
 }
 
-// ============================================================ tcgen05 flash kernel
-template <int HD>
-struct FmhaCfg {
-  static constexpr int BQ = 128, BKV = 128;
-  static constexpr int BOX = 128 * 64 * 2;              // one 128-row x 64-col bf16 box (16 KB)
-  static constexpr int NBOX = HD / 64;
-  static constexpr int Q_BYTES = NBOX * BOX;
-  static constexpr int KV_BYTES = NBOX * BOX;           // 128 keys x HD
-  static constexpr int P_BYTES = 2 * BOX;               // 128 rows x 128 keys
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;
-  static constexpr int OFF_P = OFF_V + 2 * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_P + P_BYTES;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int TMEM_COLS = 512;                 // S0 | S1 | O
-  static constexpr int TM_O = 256;
-};
-
-template <int HD>
-__global__ void __launch_bounds__(256, 1)
-    fmha_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  using C = FmhaCfg<HD>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [2]
-  uint64_t* v_full = bars + 3;    // [2]
-  uint64_t* kv_empty = bars + 5;  // [2]
-  uint64_t* s_full = bars + 7;    // [2]
-  uint64_t* s_empty = bars + 9;   // [2]
-  uint64_t* p_full = bars + 11;
-  uint64_t* o_done = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-
-  const int warp = warp_id(), lane = lane_id();
-  const int qblk = blockIdx.x, head = blockIdx.y;
-  const int n_kv = (p.Lk + C::BKV - 1) / C::BKV;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmQ);
-    tma_prefetch(&tmK);
-    tma_prefetch(&tmV);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], 4);
-    }
-    mbar_init(p_full, 4);
-    mbar_init(o_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      const int col0 = head * HD;
-      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-      for (int b = 0; b < C::NBOX; ++b) tma_load_2d(smem + C::OFF_Q + b * C::BOX, &tmQ, q_full, col0 + 64 * b, qblk * C::BQ);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[st], C::KV_BYTES);
-        for (int b = 0; b < C::NBOX; ++b)
-          tma_load_2d(smem + C::OFF_K + st * C::KV_BYTES + b * C::BOX, &tmK, &k_full[st], col0 + 64 * b, j * C::BKV);
-        mbar_arrive_expect_tx(&v_full[st], C::KV_BYTES);
-        for (int b = 0; b < C::NBOX; ++b)
-          tma_load_2d(smem + C::OFF_V + st * C::KV_BYTES + b * C::BOX, &tmV, &v_full[st], col0 + 64 * b, j * C::BKV);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);  // B = V, MN-major
-      const uint32_t sq = smem_u32(smem + C::OFF_Q);
-      const uint32_t sp = smem_u32(smem + C::OFF_P);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        const uint32_t sk = smem_u32(smem + C::OFF_K + st * C::KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::BOX + (kk & 3) * 32;
-          mma_bf16_ss(tmem + st * 128, sdesc_sw128(sq + off, 16, 1024), sdesc_sw128(sk + off, 16, 1024), idesc_s,
-                      kk > 0);
-        }
-        mma_commit(&s_full[st]);
-      };
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_s(0);
-      for (int j = 0; j < n_kv; ++j) {
-        if (j + 1 < n_kv) {
-          const int st = (j + 1) & 1;
-          mbar_wait(&k_full[st], ((j + 1) >> 1) & 1);
-          if (j + 1 >= 2) mbar_wait(&s_empty[st], (((j + 1) >> 1) - 1) & 1);
-          tc_fence_after();
-          issue_s(j + 1);
-        }
-        mbar_wait(p_full, j & 1);
-        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sv = smem_u32(smem + C::OFF_V + (j & 1) * C::KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk) {
-          const uint64_t ad = sdesc_sw128(sp + (kk >> 2) * C::BOX + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(sv + kk * 16 * 128, C::BOX, 1024);
-          mma_bf16_ss(tmem + C::TM_O, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(o_done);
-        mma_commit(&kv_empty[j & 1]);
-      }
-    }
-  } else if (warp >= 4) {
-    const int qw = warp & 3;
-    const int row = qw * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(qw * 32) << 16;
-    uint8_t* prow = smem + C::OFF_P + row * 128;
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[128];
-      tmem_ld32(tmem + lane_off + st * 128 + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
-      tmem_ld32(tmem + lane_off + st * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-      tmem_ld32(tmem + lane_off + st * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(sr + 64));
-      tmem_ld32(tmem + lane_off + st * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(sr + 96));
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[st]);
-      const int valid = p.Lk - j * 128;  // keys [valid, 128) are padding
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        float s = __uint_as_float(sr[c]) * p.scale_log2;
-        s = (c < valid) ? s : -INFINITY;
-        sr[c] = __float_as_uint(s);
-        mx = fmaxf(mx, s);
-      }
-      float m_use = m_ref;
-      bool rescale = false;
-      if (j == 0) {
-        m_use = mx;
-      } else if (mx > m_ref + 8.f) {
-        m_use = mx;
-        rescale = true;
-      }
-      float rs = 0.f;
-      if (j > 0) mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} done: P buffer free, O stable
-      tc_fence_after();
-#pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {  // 16 chunks of 8 keys (16 B)
-        float e[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          e[t] = ex2(__uint_as_float(sr[ch * 8 + t]) - m_use);
-          rs += e[t];
-        }
-        uint4 w;
-        w.x = pack_bf16(e[0], e[1]);
-        w.y = pack_bf16(e[2], e[3]);
-        w.z = pack_bf16(e[4], e[5]);
-        w.w = pack_bf16(e[6], e[7]);
-        const int atom = ch >> 3, c16 = ch & 7;
-        *reinterpret_cast<uint4*>(prow + atom * C::BOX + ((c16 ^ (row & 7)) << 4)) = w;
-      }
-      if (__any_sync(0xffffffffu, rescale)) {
-        const float f = rescale ? ex2(m_ref - m_use) : 1.f;
-        l *= f;
-#pragma unroll 1
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_off + C::TM_O + c0, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * f);
-          tmem_st32(tmem + lane_off + C::TM_O + c0, o);
-        }
-        tmem_st_wait();
-      }
-      l += rs;
-      m_ref = m_use;
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-    }
-    mbar_wait(o_done, (n_kv - 1) & 1);
-    tc_fence_after();
-    const int grow = qblk * 128 + row;
-    const float inv = 1.f / l;
-#pragma unroll 1
-    for (int c0 = 0; c0 < HD; c0 += 32) {
-      uint32_t o[32];
-      tmem_ld32(tmem + lane_off + C::TM_O + c0, o);
-      tmem_ld_wait();
-      if (grow < p.Lq) {
-        uint4* dst = reinterpret_cast<uint4*>(attn_out_row(p, grow) + head * HD + c0);
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(o[8 * qq + 0]) * inv, __uint_as_float(o[8 * qq + 1]) * inv);
-          w.y = pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv);
-          w.z = pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv);
-          w.w = pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv);
-          dst[qq] = w;
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem);
-}
-
 // ============================================================ tcgen05 flash kernel v2 (2 Q tiles / CTA)
 // One CTA = one head x 256 queries as two 128-row tiles. The MMA warp interleaves the
 // tiles — PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) — so the tensor core works on one tile
@@ -324,9 +89,9 @@ struct Fmha2Cfg {
 
 // TMEM map (512 columns): S_t fp32 at [128t, 128t+128) with P_t (bf16 pairs) aliased onto
 // its first 64 columns; O_t fp32 at [256 + 128t, 256 + 128t + HD).
-// SPLITP: the softmax hands P over in two 64-key halves so PV of the first half overlaps
-// the exponentials of the second (shortens the S -> softmax -> PV -> S chain).
-template <int HD, bool SPLITP>
+// The softmax hands P over in two 64-key halves so PV of the first half overlaps the
+// exponentials of the second (shortens the S -> softmax -> PV -> S chain).
+template <int HD>
 __global__ void __launch_bounds__(384, 1)
     fmha2_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
@@ -341,7 +106,7 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* s_full = bars + 1 + 2 * NS; // [2] per tile
   uint64_t* p_full = s_full + 2;        // [2]
   uint64_t* o_done = s_full + 4;        // [2]
-  uint64_t* p_lo = s_full + 6;          // [2] first P half written (SPLITP)
+  uint64_t* p_lo = s_full + 6;          // [2] first P half written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int warp = warp_id(), lane = lane_id();
@@ -424,14 +189,12 @@ __global__ void __launch_bounds__(384, 1)
         }
       };
       auto issue_pv = [&](int t, int j) {
-        if (SPLITP) {
-          mbar_wait(&p_lo[t], j & 1);
-          tc_fence_after();
-          issue_pv_part(t, j, 0, 4);
-        }
+        mbar_wait(&p_lo[t], j & 1);
+        tc_fence_after();
+        issue_pv_part(t, j, 0, 4);
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
-        issue_pv_part(t, j, SPLITP ? 4 : 0, 8);
+        issue_pv_part(t, j, 4, 8);
         mma_commit_elect(&o_done[t]);
       };
       mbar_wait(q_full, 0);
@@ -541,39 +304,26 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
       };
-      if (SPLITP) {
-        FTB_TL(t, j, 3);
-        exp_chunks(0, 8);
-        FTB_TL(t, j, 4);
-        // PV_t(j-1) is complete here: the MMA warp committed s_full_t(j) after issuing PV_t(j-1),
-        // and a commit tracks every earlier tcgen05 op of the thread, so O_t is stable and the
-        // P region free without waiting on o_done
-        FTB_TL(t, j, 5);
-        tc_fence_after();
-        rescale_o();
-        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_lo[t]);
-        exp_chunks(8, 16);
-        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-        tmem_st_wait();
-        FTB_TL(t, j, 6);
-        l += rs2.x + rs2.y;
-        m_ref = m_use;
-      } else {
-        exp_chunks(0, 16);
-        const float rs = rs2.x + rs2.y;
-        if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);  // PV_t(j-1) done: O_t stable
-        tc_fence_after();
-        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
-        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-        rescale_o();
-        tmem_st_wait();
-        l += rs;
-        m_ref = m_use;
-      }
+      FTB_TL(t, j, 3);
+      exp_chunks(0, 8);
+      FTB_TL(t, j, 4);
+      // PV_t(j-1) is complete here: the MMA warp committed s_full_t(j) after issuing PV_t(j-1),
+      // and a commit tracks every earlier tcgen05 op of the thread, so O_t is stable and the
+      // P region free without waiting on o_done
+      FTB_TL(t, j, 5);
+      tc_fence_after();
+      rescale_o();
+      tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_lo[t]);
+      exp_chunks(8, 16);
+      tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+      tmem_st_wait();
+      FTB_TL(t, j, 6);
+      l += rs2.x + rs2.y;
+      m_ref = m_use;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
@@ -1017,31 +767,6 @@ __global__ void __launch_bounds__(128) attn_small_kernel(const AttnParams p) {
   }
 }
 
-template <int HD>
-static int launch_fmha(const AttnParams& p, cudaStream_t s) {
-  using C = FmhaCfg<HD>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fmha_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e, "fmha smem attribute");
-    configured = true;
-  }
-  CUtensorMap tq, tk, tv;
-  auto mk = [&](CUtensorMap* m, const void* ptr, long long ld, int rows) {
-    uint64_t dims[2] = {(uint64_t)ld, (uint64_t)rows};
-    uint64_t strides[1] = {(uint64_t)ld * 2};
-    uint32_t box[2] = {64, 128};
-    return make_tmap_bf16(m, ptr, 2, dims, strides, box);
-  };
-  int rc;
-  if ((rc = mk(&tq, p.q, p.ldq, p.Lq))) return rc;
-  if ((rc = mk(&tk, p.k, p.ldk, p.Lk))) return rc;
-  if ((rc = mk(&tv, p.v, p.ldv, p.Lk))) return rc;
-  dim3 grid((p.Lq + 127) / 128, p.heads);
-  fmha_tc_kernel<HD><<<grid, 256, C::SMEM, s>>>(tq, tk, tv, p);
-  return check_launch("fmha_tc_kernel");
-}
-
 // Merge the two key halves of each split item: O = (O0 2^(m0-m) + O1 2^(m1-m)) / (l0 2^(m0-m) +
 // l1 2^(m1-m)), m = max(m0, m1) (m in the kernel's log2 units), stored like fmha2's epilogue.
 template <int HD>
@@ -1072,55 +797,25 @@ __global__ void __launch_bounds__(256) fmha2_combine_kernel(const AttnParams p) 
   }
 }
 
-static int g_fmha_kvsplit = 1;  // KV-split tail round (ftb_set_attention_variant: 0 on, 1 off)
-
-// fp32 workspace of the KV-split tail: one pool per device, allocated on the first launch made
-// outside stream capture, split into FMHA_WS_STREAMS slots of the largest tail (2 * SMs/2 split
-// CTAs at HD 128). A slot belongs to one stream (launches on one stream are ordered; concurrent
-// streams, e.g. emulated ranks, get their own), assigned on the stream's first launch even
-// during capture, so a graph captured on a fresh stream still takes the split path. No pool or
-// no free slot: the launch runs unsplit.
-constexpr int FMHA_WS_STREAMS = 8;
-static float* fmha_ws_for(cudaStream_t stream, size_t bytes) {
-  static std::mutex mu;
-  static std::map<int, std::pair<float*, size_t>> pool_of;  // device -> (base, slot bytes)
-  static std::map<std::pair<int, cudaStream_t>, int> slot_of;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  auto pl = pool_of.find(dev);
-  if (pl == pool_of.end()) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-    const size_t slot = (size_t)sm_count() * (256 * 128 + 512) * sizeof(float);
-    float* base = nullptr;
-    if (cudaMalloc(&base, slot * FMHA_WS_STREAMS) != cudaSuccess) {
-      cudaGetLastError();
-      return nullptr;
-    }
-    pl = pool_of.emplace(dev, std::make_pair(base, slot)).first;
-  }
-  if (bytes > pl->second.second) return nullptr;
-  auto key = std::make_pair(dev, stream);
-  auto it = slot_of.find(key);
-  if (it == slot_of.end()) {
-    int used = 0;
-    for (auto& kv : slot_of) used += kv.first.first == dev;
-    if (used >= FMHA_WS_STREAMS) return nullptr;
-    it = slot_of.emplace(key, used).first;
-  }
-  return pl->second.first + (size_t)it->second * (pl->second.second / sizeof(float));
+// KV-split tail round: the R = items % SMs items of the partial last round run as two key halves
+// each on otherwise idle SMs when 2R <= SMs (14B: 1680 items = 11.35 rounds -> 11.5; 1.3B: 3.4 ->
+// 3.5). Returns R (0: no split) for this device's SM count.
+static int fmha2_split_items(int Lq, int Lk, int heads) {
+  const int items = ((Lq + 255) / 256) * heads;
+  const int nsm = sm_count();
+  const int R = items % nsm;
+  return (items > nsm && R > 0 && 2 * R <= nsm && (Lk + 127) / 128 >= 4) ? R : 0;
 }
 
+static size_t fmha2_ws_bytes(int R, int hd) { return (size_t)2 * R * (256 * hd + 512) * sizeof(float); }
+
 template <int HD>
-static int launch_fmha2(const AttnParams& p_in, cudaStream_t s, bool splitp = false) {
+static int launch_fmha2(const AttnParams& p_in, cudaStream_t s, float* ws, size_t ws_bytes) {
   AttnParams p = p_in;
   using C = Fmha2Cfg<HD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaSuccess;
-    for (auto fn : {fmha2_tc_kernel<HD, false>, fmha2_tc_kernel<HD, true>})
-      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(fmha2_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "fmha2 smem attribute");
     configured = true;
   }
@@ -1136,23 +831,18 @@ static int launch_fmha2(const AttnParams& p_in, cudaStream_t s, bool splitp = fa
   if ((rc = mk(&tk, p.k, p.ldk, p.Lk))) return rc;
   if ((rc = mk(&tv, p.v, p.ldv, p.Lk))) return rc;
   // 1-D grid of (head, query block) items, query block fastest (CTAs running together share
-  // K/V in L2). The R = items % SMs items of the partial last round run as two key halves each
-  // on otherwise idle SMs when 2R <= SMs (14B: 1680 items = 11.35 rounds -> 11.5; 1.3B: 3.4 -> 3.5)
+  // K/V in L2); the partial last round splits over the keys when the caller's workspace holds it
   p.n_qblk = (p.Lq + 255) / 256;
   const int items = p.n_qblk * p.heads;
-  const int nsm = sm_count();
-  const int R = items % nsm;
+  const int R = fmha2_split_items(p.Lq, p.Lk, p.heads);
   p.ws = nullptr;
   p.split_first = items;
-  if (g_fmha_kvsplit && items > nsm && R > 0 && 2 * R <= nsm && (p.Lk + 127) / 128 >= 4) {
-    p.ws = fmha_ws_for(s, (size_t)2 * R * (256 * HD + 512) * sizeof(float));
-    if (p.ws) p.split_first = items - R;
+  if (R && ws && ws_bytes >= fmha2_ws_bytes(R, HD)) {
+    p.ws = ws;
+    p.split_first = items - R;
   }
   const int grid = p.ws ? items + R : items;
-  if (splitp)
-    fmha2_tc_kernel<HD, true><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
-  else
-    fmha2_tc_kernel<HD, false><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
+  fmha2_tc_kernel<HD><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
   rc = check_launch("fmha2_tc_kernel");
   if (rc || !p.ws) return rc;
   fmha2_combine_kernel<HD><<<R, 256, 0, s>>>(p);
@@ -1170,7 +860,7 @@ static int launch_small(const AttnParams& p, cudaStream_t s) {
 
 using namespace ftb;
 
-static int attention_run(int32_t impl, AttnParams& p, void* stream) {
+static int attention_run(int32_t impl, AttnParams& p, float* ws, size_t ws_bytes, void* stream) {
   const long long ldq = p.ldq, ldk = p.ldk, ldv = p.ldv, ldo = p.ldo;
   const int head_dim = p.hd;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1181,21 +871,13 @@ static int attention_run(int32_t impl, AttnParams& p, void* stream) {
     if (head_dim == 64) return launch_xattn<64>(p, s);
     return set_error(FTB_EINVAL, "xattn: head_dim must be 64 or 128");
   }
-  if (impl == 5) {  // A/B reference: P handed over in one piece
-    if (head_dim == 128) return launch_fmha2<128>(p, s, false);
-    if (head_dim == 64) return launch_fmha2<64>(p, s, false);
-  }
-  if (impl == 0 || impl == 2) {
+  if (impl == 0) {  // flash kernel: 2 Q tiles per CTA, two softmax warpgroups
     if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
-    if (impl == 0) {  // 2 Q tiles per CTA, two softmax warpgroups, P handed over in two halves
-      if (head_dim == 128) return launch_fmha2<128>(p, s, true);
-      if (head_dim == 64) return launch_fmha2<64>(p, s, true);
-    } else {          // v1: 1 Q tile per CTA
-      if (head_dim == 128) return launch_fmha<128>(p, s);
-      if (head_dim == 64) return launch_fmha<64>(p, s);
-    }
+    if (head_dim == 128) return launch_fmha2<128>(p, s, ws, ws_bytes);
+    if (head_dim == 64) return launch_fmha2<64>(p, s, ws, ws_bytes);
     return set_error(FTB_EINVAL, "fmha: head_dim must be 64 or 128");
   }
+  if (impl != 1) return set_error(FTB_EINVAL, "attention: impl must be 0 (flash), 1 (CUDA-core) or 3 (short KV)");
   if (head_dim <= 16) return launch_small<16>(p, s);
   if (head_dim <= 32) return launch_small<32>(p, s);
   if (head_dim <= 64) return launch_small<64>(p, s);
@@ -1208,10 +890,10 @@ static int default_impl(int Lq, int Lk, int head_dim) {
   return 1;
 }
 
-extern "C" int ftb_set_attention_variant(int32_t v) {
-  if (v < 0 || v > 1) return set_error(FTB_EINVAL, "attention variant: 0 default, 1 = no KV-split tail round");
-  g_fmha_kvsplit = (v & 1) ? 0 : 1;
-  return FTB_OK;
+extern "C" size_t ftb_attention_workspace_bytes(int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim) {
+  if (Lq <= 0 || Lk <= 0 || heads <= 0 || default_impl(Lq, Lk, head_dim) != 0) return 0;
+  const int R = fmha2_split_items(Lq, Lk, heads);
+  return R ? fmha2_ws_bytes(R, head_dim) : 0;
 }
 
 #ifdef FTB_FMHA_TIMELINE
@@ -1222,7 +904,8 @@ extern "C" int ftb_debug_fmha_timeline(long long* out) {
 
 extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                                   int64_t ldv, void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads,
-                                  int32_t head_dim, float scale, void* stream) {
+                                  int32_t head_dim, float scale, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
   if (!q || !k || !v || !o || Lq < 0 || Lk <= 0 || heads <= 0 || head_dim <= 0)
     return set_error(FTB_EINVAL, "attention: bad arguments");
   if (Lq == 0) return FTB_OK;
@@ -1240,13 +923,13 @@ extern "C" int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, cons
   p.heads = heads;
   p.hd = head_dim;
   p.scale_log2 = scale * 1.4426950408889634f;
-  return attention_run(impl, p, stream);
+  return attention_run(impl, p, (float*)workspace, workspace_bytes, stream);
 }
 
 extern "C" int ftb_attention_scatter(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                                      int64_t ldv, void* const* o_peers, int32_t n_peers, int64_t peer_rows,
                                      int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
-                                     float scale, void* stream) {
+                                     float scale, void* workspace, size_t workspace_bytes, void* stream) {
   if (!q || !k || !v || !o_peers || n_peers < 1 || n_peers > FTB_MAX_PEERS || peer_rows <= 0 || Lq < 0 || Lk <= 0 ||
       heads <= 0 || head_dim <= 0)
     return set_error(FTB_EINVAL, "attention_scatter: bad arguments");
@@ -1271,11 +954,12 @@ extern "C" int ftb_attention_scatter(const void* q, int64_t ldq, const void* k, 
   p.n_peers = n_peers;
   p.peer_rows = peer_rows;
   for (int i = 0; i < n_peers; ++i) p.o_peers[i] = (__nv_bfloat16*)o_peers[i];
-  return attention_run(default_impl(Lq, Lk, head_dim), p, stream);
+  return attention_run(default_impl(Lq, Lk, head_dim), p, (float*)workspace, workspace_bytes, stream);
 }
 
 extern "C" int ftb_attention(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
                              void* o, int64_t ldo, int32_t Lq, int32_t Lk, int32_t heads, int32_t head_dim,
-                             float scale, void* stream) {
-  return ftb_attention_impl(default_impl(Lq, Lk, head_dim), q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim, scale, stream);
+                             float scale, void* workspace, size_t workspace_bytes, void* stream) {
+  return ftb_attention_impl(default_impl(Lq, Lk, head_dim), q, ldq, k, ldk, v, ldv, o, ldo, Lq, Lk, heads, head_dim,
+                            scale, workspace, workspace_bytes, stream);
 }

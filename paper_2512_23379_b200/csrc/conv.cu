@@ -1105,15 +1105,6 @@ static int launch_conv_dxr_vert(const void* in, int T_in, const void* w_t, const
 
 using namespace ftb;
 
-static int g_conv_variant = 0;  // 0 auto, 1 per-tap kernel, 2 dx reuse on CTA pairs, 3 dx reuse single-CTA,
-                                // 4 CTA pairs with one M-subtile per CTA
-extern "C" int ftb_set_conv_variant(int32_t v) {
-  if (v < 0 || v > 4)
-    return set_error(FTB_EINVAL, "conv variant must be 0 (auto), 1 (per-tap), 2 (dx reuse, CTA pair), 3 (dx reuse, 1 CTA) or 4 (pair, one subtile)");
-  g_conv_variant = v;
-  return FTB_OK;
-}
-
 static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in, int32_t H,
                        int32_t W, int32_t Cin, const void* w_t,
                                int32_t Cout, int32_t KT, int32_t KH, int32_t KW, int32_t t0, const float* bias,
@@ -1129,6 +1120,10 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
     if (!nrm->write_main && resid) return set_error(FTB_EINVAL, "conv3d: fused norm without main output takes no residual");
   }
   const int out_f32 = (mode >> 4) & 1, resid_f32 = (mode >> 5) & 1;
+  // kernel variant of this call (bits 8-10, 0 = auto): 1 per-tap kernel, 2 dx reuse on CTA pairs,
+  // 3 dx reuse single-CTA, 4 CTA pairs with one M-subtile per CTA (A/B benchmarks, tests)
+  const int variant = (mode >> 8) & 7;
+  if (variant > 4) return set_error(FTB_EINVAL, "conv3d: variant (mode bits 8-10) must be 0..4");
   mode &= 15;
   if (Cin % 8) return set_error(FTB_EINVAL, "conv3d: Cin must be a multiple of 8");
   if ((KH != 1 && KH != 3) || (KW != 1 && KW != 3) || KT < 1 || KT > 3)
@@ -1170,16 +1165,16 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
   }
   if (p.halo && (!halo_bot || KH != 3 || KW != 3 || Cin % 32))
     return set_error(FTB_EINVAL, "conv3d: halo rows need a 3x3 kernel, both halo buffers and Cin % 32 == 0");
-  if ((g_conv_variant != 1 || p.halo) && KH == 3 && KW == 3 && Cin % 32 == 0) {
+  if ((variant != 1 || p.halo) && KH == 3 && KW == 3 && Cin % 32 == 0) {
     cudaStream_t s0 = reinterpret_cast<cudaStream_t>(stream);
     const void *ht = halo_top, *hb = halo_bot;
     // CTA pairs halve each SM's weight traffic (auto for Cout 96 / 192: the smem-bound levels)
     // (Cout 96 / multiples of 192: the smem- and L2-feed-bound levels); variant 4 = pair
     // without the two-subtile weight sharing at Cout 96 (A/B)
-    const bool pair = (g_conv_variant == 2 || g_conv_variant == 4 || g_conv_variant == 0) &&
+    const bool pair = (variant == 2 || variant == 4 || variant == 0) &&
                       (Cout == 96 || Cout % 192 == 0) && !(norm && Cout > 192);
     if (pair) {
-      const bool msub = g_conv_variant != 4;
+      const bool msub = variant != 4;
       if (Cin % 64 == 0) {
         p.kb_per_tap = Cin / 64;
         if (Cout == 96)
@@ -1188,7 +1183,7 @@ static int conv3d_impl(const void* in, const void* halo_top, const void* halo_bo
         return launch_conv_dxr_pair<192, 64>(in, T_in, w_t, p, s0, ht, hb);
       }
       p.kb_per_tap = Cin / 32;
-      if (Cout == 96 && g_conv_variant != 2)   // vertical row reuse (variant 2 keeps two x-subtiles)
+      if (Cout == 96 && variant != 2)   // vertical row reuse (variant 2 keeps two x-subtiles)
         return msub ? launch_conv_dxr_vert<96, 32>(in, T_in, w_t, p, s0, ht, hb)
                     : launch_conv_dxr_pair<96, 32>(in, T_in, w_t, p, s0, ht, hb);
       if (Cout == 96)

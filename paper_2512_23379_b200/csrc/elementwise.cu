@@ -281,12 +281,6 @@ static inline int grid_for(long long n, int threads) {
 using namespace ftb;
 #define S(stream) reinterpret_cast<cudaStream_t>(stream)
 
-static int g_norm_variant = 0;
-extern "C" int ftb_set_norm_variant(int32_t v) {
-  g_norm_variant = v;
-  return FTB_OK;
-}
-
 extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t N, const float* gamma,
                                  const float* beta, const float* scale, const float* shift, int64_t mod_ld,
                                  int32_t rows_per_group, int64_t row_offset, float eps, void* y, int64_t ldy,
@@ -298,8 +292,8 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
   const bool vec = (N % 4 == 0) && N <= 4 * 256 * 8 && (ldx % 4 == 0) && (ldy % 4 == 0) && (!scale || mod_ld % 4 == 0) &&
                    al16(x) && (reinterpret_cast<uintptr_t>(y) & 7) == 0 && (!gamma || al16(gamma)) &&
                    (!beta || al16(beta)) && (!scale || al16(scale)) && (!shift || al16(shift)) && N >= 512;
-  const bool narrow = N <= 4 * 128 * 4 || g_norm_variant == 4;   // variant 4: 128-thread rows at any width (A/B)
-  if (vec && g_norm_variant != 1 && g_norm_variant != 3 && narrow && N <= 4 * 128 * 10 && (N / 4) % 128 == 0) {
+  const bool narrow = N <= 4 * 128 * 4;
+  if (vec && narrow && (N / 4) % 128 == 0) {
     // narrow rows (1.3B: m = 1536): 128 threads x 3 float4, every lane busy, twice the rows
     // resident per SM (at 256 threads half the lanes idled in the second float4)
     const int nv = N / 4 / 128;
@@ -311,12 +305,10 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
       FTB_NORM_VEC128(2);
     else if (nv <= 3)
       FTB_NORM_VEC128(3);
-    else if (nv <= 4)
-      FTB_NORM_VEC128(4);
     else
-      FTB_NORM_VEC128(10);
+      FTB_NORM_VEC128(4);
 #undef FTB_NORM_VEC128
-  } else if (vec && g_norm_variant != 1) {
+  } else if (vec) {
     const int nv = (N / 4 + 255) / 256;   // float4 per thread at 256 threads
 #define FTB_NORM_VEC(V)                                                                                             \
   norm_modulate_vec_kernel<V, 256, true><<<M, 256, 0, S(stream)>>>(x, ldx, N, gamma, beta, scale, shift, mod_ld, \
@@ -426,205 +418,8 @@ extern "C" int ftb_add_bcast_f32(const float* a, int64_t F, int64_t n, const flo
 //   S_h = (U·Wq_h)·K_h^T·s = U·(s·Wq_h·K_h^T)        At[(h,j)][k] = s·Σ_d K[j][h,d]·Wq^T[(h,d)][k]
 //   out = Σ_h P_h·(V_h·Wo_h) = P·Bt^T                  Bt[n][(h,j)] = Σ_d Wo^T[n][(h,d)]·V[j][h,d]
 // turning the two m×m projections per token into two m×(H·J) GEMMs (J = roundup(n_cond, 8)).
+// At and Bt are two tensor-core GEMMs over the block-diagonal operands built here.
 namespace ftb {
-
-// Block-cooperative staging of a bf16 [rows][cols] global tile (row stride ld elements) into
-// fp32 smem dst[r * dld + c]; rows in [rows, pad_rows) and columns >= cols are zero-filled.
-// 16-byte loads (cols % 8 == 0, 16-byte aligned rows), 8 in flight per thread.
-__device__ __forceinline__ void stage_bf16_rows(float* dst, int dld, const __nv_bfloat16* src, long long ld, int rows,
-                                                int cols, int pad_rows = -1) {
-  const int c8 = (cols + 7) >> 3;
-  const int total = (pad_rows > rows ? pad_rows : rows) * c8;
-  for (int base = 0; base < total; base += 8 * blockDim.x) {
-    uint4 buf[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + u * blockDim.x + threadIdx.x;
-      const int r = i / c8, c = (i - r * c8) * 8;
-      buf[u] = (i < total && r < rows && c < cols) ? __ldg(reinterpret_cast<const uint4*>(src + (long long)r * ld + c))
-                                                  : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + u * blockDim.x + threadIdx.x;
-      if (i >= total) break;
-      const int r = i / c8, c = (i - r * c8) * 8;
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&buf[u]);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h2[e]);
-        dst[r * dld + c + 2 * e] = f.x;
-        dst[r * dld + c + 2 * e + 1] = f.y;
-      }
-    }
-  }
-}
-
-// As stage_bf16_rows but stores transposed: dst[c * dld + r]. Consecutive threads take
-// consecutive rows, so the transposed smem stores hit consecutive banks.
-__device__ __forceinline__ void stage_bf16_rows_t(float* dst, int dld, const __nv_bfloat16* src, long long ld, int rows,
-                                                  int cols) {
-  const int c8 = (cols + 7) >> 3;
-  const int total = 128 * c8;   // always stage 128 rows (zero beyond `rows`)
-  for (int base = 0; base < total; base += 8 * blockDim.x) {
-    uint4 buf[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + u * blockDim.x + threadIdx.x;
-      const int r = i & 127, c = (i >> 7) * 8;
-      buf[u] = (i < total && r < rows) ? __ldg(reinterpret_cast<const uint4*>(src + (long long)r * ld + c))
-                                       : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = base + u * blockDim.x + threadIdx.x;
-      if (i >= total) break;
-      const int r = i & 127, c = (i >> 7) * 8;
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&buf[u]);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h2[e]);
-        dst[(c + 2 * e) * dld + r] = f.x;
-        dst[(c + 2 * e + 1) * dld + r] = f.y;
-      }
-    }
-  }
-}
-
-// At[(h,j)][k]: block = (head h, 128 columns k0..k0+127). Wq^T rows (h,d) x those columns and
-// K_h are staged as fp32 in smem; thread (k, jg) accumulates 24 j's over the hd reduction.
-__global__ void __launch_bounds__(256) xattn_fold_at_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv,
-                                                            int n_cond, int hd, int J, const __nv_bfloat16* __restrict__ wqT,
-                                                            long long ldw, int m, float scale,
-                                                            __nv_bfloat16* __restrict__ at) {
-  extern __shared__ float sm[];
-  float* wsh = sm;              // [hd][128]
-  float* ksh = sm + hd * 128;   // [48][hd]
-  const int h = blockIdx.y, k0 = blockIdx.x * 128;
-  // staging: 16-byte loads, all issued before any use (the loops are latency-bound otherwise)
-  stage_bf16_rows(wsh, 128, wqT + (long long)(h * hd) * ldw + k0, ldw, hd, min(128, m - k0));
-  stage_bf16_rows(ksh, hd, kv + h * hd, ldkv, n_cond, hd, 48);
-  __syncthreads();
-  // register tile: 4 columns (one float4 of wsh) x 6 j's per thread; j-group warp-uniform
-  const int kq = threadIdx.x & 31, jq = threadIdx.x >> 5;
-  float acc[6][4];
-#pragma unroll
-  for (int q = 0; q < 6; ++q)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[q][e] = 0.f;
-  for (int d = 0; d < hd; ++d) {
-    const float4 w = *reinterpret_cast<const float4*>(wsh + d * 128 + 4 * kq);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const float kk = ksh[(jq * 6 + q) * hd + d];
-      acc[q][0] = fmaf(kk, w.x, acc[q][0]);
-      acc[q][1] = fmaf(kk, w.y, acc[q][1]);
-      acc[q][2] = fmaf(kk, w.z, acc[q][2]);
-      acc[q][3] = fmaf(kk, w.w, acc[q][3]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    const int j = jq * 6 + q;
-    if (j >= J) continue;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = k0 + 4 * kq + e;
-      if (k < m) at[(long long)(h * J + j) * m + k] = __float2bfloat16_rn(j < n_cond ? acc[q][e] * scale : 0.f);
-    }
-  }
-}
-
-// Bt[n][(h,j)]: block = (head h, 128 rows n0..n0+127). Wo^T[n][(h,d)] is staged transposed
-// ([d][n], padded) so both the coalesced global read and the compute reads are conflict-free;
-// the [128][J] output tile goes out through smem as contiguous row segments.
-__global__ void __launch_bounds__(256) xattn_fold_bt_kernel(const __nv_bfloat16* __restrict__ kv, long long ldkv,
-                                                            int n_cond, int hd, int J, const __nv_bfloat16* __restrict__ woT,
-                                                            long long ldw, int m, int heads,
-                                                            __nv_bfloat16* __restrict__ bt) {
-  extern __shared__ float sm[];
-  float* wsh = sm;                        // [hd][132] (rows 16-byte aligned for float4 reads)
-  float* vsh = sm + hd * 132;             // [48][hd]
-  float* osh = vsh + 48 * hd;             // [128][48]
-  const int h = blockIdx.y, n0 = blockIdx.x * 128;
-  const int voff = heads * hd;            // V follows K in the kv rows
-  stage_bf16_rows_t(wsh, 132, woT + (long long)n0 * ldw + h * hd, ldw, min(128, m - n0), hd);
-  stage_bf16_rows(vsh, hd, kv + voff + h * hd, ldkv, n_cond, hd, 48);
-  __syncthreads();
-  // register tile: 4 rows (float4 of the transposed wsh) x 6 j's per thread; j-group warp-uniform
-  const int nq = threadIdx.x & 31, jq = threadIdx.x >> 5;
-  float acc[6][4];
-#pragma unroll
-  for (int q = 0; q < 6; ++q)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[q][e] = 0.f;
-  for (int d = 0; d < hd; ++d) {
-    const float4 w = *reinterpret_cast<const float4*>(wsh + d * 132 + 4 * nq);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      const float vv = vsh[(jq * 6 + q) * hd + d];
-      acc[q][0] = fmaf(w.x, vv, acc[q][0]);
-      acc[q][1] = fmaf(w.y, vv, acc[q][1]);
-      acc[q][2] = fmaf(w.z, vv, acc[q][2]);
-      acc[q][3] = fmaf(w.w, vv, acc[q][3]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 6; ++q)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) osh[(4 * nq + e) * 48 + jq * 6 + q] = acc[q][e];
-  __syncthreads();
-  // 8 threads per row, each a 16-byte run of the row's J (<= 48) outputs
-  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x) {
-    const int rr = i >> 3, j0 = (i & 7) * 8;
-    if (j0 >= J || n0 + rr >= m) continue;
-    uint4 w;
-    uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int j = j0 + 2 * e;
-      wp[e] = pack_bf16(j < n_cond ? osh[rr * 48 + j] : 0.f, j + 1 < n_cond ? osh[rr * 48 + j + 1] : 0.f);
-    }
-    *reinterpret_cast<uint4*>(bt + (long long)(n0 + rr) * (heads * J) + h * J + j0) = w;
-  }
-}
-
-// P = softmax over each head's J-column segment of S (first n_cond valid, rest -> 0), bf16.
-// Thread = (row, head); J % 8 == 0 so the segment moves as float4 / uint4.
-template <int JC>
-__global__ void xattn_softmax_kernel(const float* __restrict__ s, long long lds, int rows, int heads, int n_cond,
-                                     __nv_bfloat16* __restrict__ p, long long ldp) {
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= (long long)rows * heads) return;
-  const long long r = idx / heads;
-  const int h = (int)(idx - r * heads);
-  const float4* sr = reinterpret_cast<const float4*>(s + r * lds + h * JC);
-  float v[JC];
-#pragma unroll
-  for (int q = 0; q < JC / 4; ++q) {
-    const float4 f = __ldcs(sr + q);
-    v[4 * q] = f.x;
-    v[4 * q + 1] = f.y;
-    v[4 * q + 2] = f.z;
-    v[4 * q + 3] = f.w;
-  }
-  float mx = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < JC; ++j)
-    if (j < n_cond) mx = fmaxf(mx, v[j]);
-  float sum = 0.f;
-#pragma unroll
-  for (int j = 0; j < JC; ++j) {
-    v[j] = j < n_cond ? __expf(v[j] - mx) : 0.f;
-    sum += v[j];
-  }
-  const float inv = 1.f / sum;
-  uint4* pr = reinterpret_cast<uint4*>(p + r * ldp + h * JC);
-#pragma unroll
-  for (int q = 0; q < JC / 8; ++q)
-    pr[q] = make_uint4(pack_bf16(v[8 * q] * inv, v[8 * q + 1] * inv), pack_bf16(v[8 * q + 2] * inv, v[8 * q + 3] * inv),
-                       pack_bf16(v[8 * q + 4] * inv, v[8 * q + 5] * inv), pack_bf16(v[8 * q + 6] * inv, v[8 * q + 7] * inv));
-}
 
 // Block-diagonal operands of the tensor-core fold: kbd[(h,j)][h*hd + d] = scale * K[j][h*hd + d],
 // vbd[(h,j)][h*hd + d] = V[j][h*hd + d] for j < n_cond (kv = [n_cond][K | V]). Only the diagonal
@@ -659,31 +454,6 @@ __global__ void xattn_blockdiag_kernel(const __nv_bfloat16* __restrict__ kv, lon
 
 }  // namespace ftb
 
-extern "C" int ftb_xattn_fold(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim,
-                              int32_t J, const void* wqT, int64_t ldwq, const void* woT, int64_t ldwo, int32_t m,
-                              float scale, void* at, void* bt, void* stream) {
-  if (!kv || !wqT || !woT || !at || !bt || n_cond <= 0 || J < n_cond || J > 48 || heads * head_dim != m ||
-      head_dim > 128 || (J % 8) || (head_dim % 8) || (m % 8) || (ldkv % 8) || (ldwq % 8) || (ldwo % 8))
-    return set_error(FTB_EINVAL, "xattn_fold: bad arguments (n_cond <= J <= 48, J, head_dim, m, ld % 8 == 0)");
-  const size_t sm_at = ((size_t)head_dim * 128 + 48 * head_dim) * 4;
-  const size_t sm_bt = ((size_t)head_dim * 132 + 48 * head_dim + 128 * 48) * 4;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(xattn_fold_at_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(xattn_fold_bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    configured = true;
-  }
-  xattn_fold_at_kernel<<<dim3((m + 127) / 128, heads), 256, sm_at, S(stream)>>>(
-      (const __nv_bfloat16*)kv, ldkv, n_cond, head_dim, J, (const __nv_bfloat16*)wqT, ldwq, m, scale,
-      (__nv_bfloat16*)at);
-  int rc = check_launch("xattn_fold_at_kernel");
-  if (rc) return rc;
-  xattn_fold_bt_kernel<<<dim3((m + 127) / 128, heads), 256, sm_bt, S(stream)>>>(
-      (const __nv_bfloat16*)kv, ldkv, n_cond, head_dim, J, (const __nv_bfloat16*)woT, ldwo, m, heads,
-      (__nv_bfloat16*)bt);
-  return check_launch("xattn_fold_bt_kernel");
-}
-
 extern "C" int ftb_xattn_blockdiag(const void* kv, int64_t ldkv, int32_t n_cond, int32_t heads, int32_t head_dim,
                                    int32_t J, float scale, void* kbd, void* vbd, int64_t ld, int32_t k_tile_segs,
                                    void* stream) {
@@ -696,23 +466,4 @@ extern "C" int ftb_xattn_blockdiag(const void* kv, int64_t ldkv, int32_t n_cond,
                                                                      head_dim, J, scale, (__nv_bfloat16*)kbd,
                                                                      (__nv_bfloat16*)vbd, ld, k_tile_segs);
   return check_launch("xattn_blockdiag_kernel");
-}
-
-extern "C" int ftb_xattn_softmax(const float* s, int64_t lds, int32_t rows, int32_t heads, int32_t J, int32_t n_cond,
-                                 void* p, int64_t ldp, void* stream) {
-  if (!s || !p || rows < 0 || heads <= 0 || n_cond <= 0 || J < n_cond || (lds % 4) || (ldp % 8))
-    return set_error(FTB_EINVAL, "xattn_softmax: bad arguments");
-  if (rows == 0) return FTB_OK;
-  const long long n = (long long)rows * heads;
-  const unsigned grid = (unsigned)((n + 255) / 256);
-  switch (J) {
-    case 8: xattn_softmax_kernel<8><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
-    case 16: xattn_softmax_kernel<16><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
-    case 24: xattn_softmax_kernel<24><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
-    case 32: xattn_softmax_kernel<32><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
-    case 40: xattn_softmax_kernel<40><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
-    case 48: xattn_softmax_kernel<48><<<grid, 256, 0, S(stream)>>>(s, lds, rows, heads, n_cond, (__nv_bfloat16*)p, ldp); break;
-    default: return set_error(FTB_EINVAL, "xattn_softmax: J must be a multiple of 8 <= 48");
-  }
-  return check_launch("xattn_softmax_kernel");
 }

@@ -14,8 +14,6 @@
 // Replaces the reference's dense_forward (backends/reference.py:17-18) and the
 // adds/activations that follow it in net.py:230-274.
 #include <algorithm>
-#include <map>
-#include <mutex>
 
 #include "common.cuh"
 #include "ftb_internal.h"
@@ -841,61 +839,8 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
 
 using namespace ftb;
 
-static int g_gemm_variant = 0;  // 0 auto, 1 single-CTA, 2 CTA pair
-static int g_gemm_staged = 1;   // pair kernel residual epilogue through smem (flag 4 turns it off)
-static int g_gemm_prefetch = 1; // ... with an L2 prefetch of the h rows (flag 8 turns it off)
-static int g_gemm_tail = 1;  // split-K tail wave for staged residual pair GEMMs (flag 32 turns it off)
-static int g_gemm_epg2_resid = 1;  // residual GEMMs: two epilogue warpgroups at every K (flag 16: K <= 2048 only)
-
-extern "C" int ftb_set_gemm_variant(int32_t v) {
-  if ((v & 3) > 2 || v < 0 || v > 62)
-    return set_error(FTB_EINVAL, "gemm variant must be 0 (auto), 1 (single CTA) or 2 (CTA pair), plus 4 = row-per-thread "
-                                 "residual epilogue, 8 = no h prefetch, 16 = one epilogue warpgroup for long-K residual "
-                                 "GEMMs, 32 = no split-K tail wave");
-  g_gemm_variant = v & 3;
-  g_gemm_staged = (v & 4) ? 0 : 1;
-  g_gemm_prefetch = (v & 8) ? 0 : 1;
-  g_gemm_epg2_resid = (v & 16) ? 0 : 1;
-  g_gemm_tail = (v & 32) ? 0 : 1;
-  return FTB_OK;
-}
-
-// Slice counters of the split tail: one block of FTB_TAIL_SLOTS x 16 words per stream (launches
-// on one stream are ordered, so they can share a block; concurrent streams, e.g. emulated
-// ranks, must not). Statically zeroed; every launch leaves its counters at zero.
-constexpr int FTB_TAIL_SLOTS = 128;  // >= n_clusters (74 on B200)
-constexpr int FTB_TAIL_STREAMS = 64;
-__device__ unsigned g_tail_flags[FTB_TAIL_STREAMS * FTB_TAIL_SLOTS * 16];
-
-static unsigned* tail_flags_for(cudaStream_t stream) {
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, int> slot_of;
-  static std::map<int, unsigned*> base_of;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  auto b = base_of.find(dev);
-  if (b == base_of.end()) {
-    void* ptr = nullptr;
-    if (cudaGetSymbolAddress(&ptr, g_tail_flags) != cudaSuccess) return nullptr;
-    b = base_of.emplace(dev, static_cast<unsigned*>(ptr)).first;
-  }
-  auto key = std::make_pair(dev, stream);
-  auto it = slot_of.find(key);
-  if (it == slot_of.end()) {
-    int used = 0;
-    for (auto& kv : slot_of) used += kv.first.first == dev;
-    if (used >= FTB_TAIL_STREAMS) return nullptr;  // caller runs the tail unsplit
-    it = slot_of.emplace(key, used).first;
-  }
-  return b->second + (size_t)it->second * FTB_TAIL_SLOTS * 16;
-}
-
-static int g_gemm_group = 0;
-extern "C" int ftb_set_gemm_group(int32_t g) {
-  g_gemm_group = g;
-  return FTB_OK;
-}
+// Split-K tail counters: FTB_TAIL_COUNTER_WORDS = FTB_TAIL_SLOTS x 16 words per caller buffer.
+constexpr int FTB_TAIL_SLOTS = FTB_TAIL_COUNTER_WORDS / 16;  // >= n_clusters (74 on B200)
 
 extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64_t a_chunk_stride, const void* B,
                              int64_t ldb, int32_t M, int32_t N, int32_t K, const ftb_epilogue* epi, void* stream) {
@@ -929,12 +874,18 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
     for (int i = 0; i < epi->n_peers; ++i)
       if (!epi->peer_out[i]) return set_error(FTB_EINVAL, "gemm: null peer pointer");
   }
+  // kernel selection of this call (ftb_epilogue.variant; 0 = product defaults)
+  const int variant = epi->variant;
+  if (variant < 0 || (variant & 3) == 3 || variant > 31)
+    return set_error(FTB_EINVAL, "gemm: variant must be 0/1/2 (auto / single CTA / CTA pair) + 4 (row-per-thread "
+                                 "residual epilogue) + 8 (no h prefetch) + 16 (one epilogue warpgroup at long K)");
+  if (epi->raster_group < 0) return set_error(FTB_EINVAL, "gemm: raster_group must be >= 0");
   GemmParams p{};
   p.n_peers = epi->n_peers;
-  p.staged = g_gemm_staged;
+  p.staged = (variant & 4) ? 0 : 1;
   // short K only: there the h rows must stream at DRAM rate behind a short mainloop; at long K
   // the prefetched rows just displace A/B panels from L2 (measured -3..-4 % at K >= 5120)
-  p.prefetch = g_gemm_prefetch && K <= 2048;
+  p.prefetch = !(variant & 8) && K <= 2048;
   for (int i = 0; i < epi->n_peers; ++i) p.peers[i] = epi->peer_out[i];
   p.M = M;
   p.N = N;
@@ -964,7 +915,7 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   }
   if (epi->rope) p.rope = *epi->rope;
 
-  const bool pair = g_gemm_variant == 2 || (g_gemm_variant == 0 && M >= 256 && N >= 256);
+  const bool pair = (variant & 3) == 2 || ((variant & 3) == 0 && M >= 256 && N >= 256);
   int BN = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
   // few m-blocks (cond-token K/V projections, M = 37): narrower tiles until the grid covers
   // the SMs, so the weight stream is spread over every SM's load path
@@ -976,7 +927,7 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
     // the B panel streams past once per group
     const long long panel = 256LL * K * 2;
     int gmax = (int)(40LL * 1024 * 1024 / (panel > 0 ? panel : 1));
-    if (g_gemm_group > 0) gmax = g_gemm_group;
+    if (epi->raster_group > 0) gmax = epi->raster_group;
     p.group_m = gmax < 8 ? 8 : gmax;
   }
   CUtensorMap ta, tb;
@@ -999,14 +950,14 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   // short K: the per-tile mainloop is shorter than one epilogue warpgroup's drain -> two groups
   // (+ residual GEMMs at any K: the column-split fp32 epilogue drains h in half the time; FFN2
   // K=13824 1232-1281 -> 1408 TFLOP/s, chunk GEMM time -4.5 ms; bf16 epilogues lose at long K)
-  const bool epg2 = K <= 2048 || (g_gemm_epg2_resid && epi->kind == FTB_EPI_RESID_F32);
+  const bool epg2 = K <= 2048 || (!(variant & 16) && epi->kind == FTB_EPI_RESID_F32);
   if (pair) {
     auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     const bool staged = p.staged && (p.kind == FTB_EPI_RESID_F32 || (p.kind == FTB_EPI_F32 && !p.n_peers)) &&
                         N % 32 == 0 && !(p.ldc & 3) && al16(p.out) &&
                         (!p.group_vec || (!(p.group_ld & 3) && al16(p.group_vec))) && (!p.bias || al16(p.bias));
     p.tail_split = 1;
-    if (staged && g_gemm_tail && p.kind == FTB_EPI_RESID_F32 && p.band_k <= 0) {
+    if (staged && epi->tail_counters && p.kind == FTB_EPI_RESID_F32 && p.band_k <= 0) {
       // partial last wave of R < n_clusters / 2 tiles: run them as K-slices on the idle pairs
       // (FFN2 / O-proj at M = 10530, N = 5120: 840 tiles = 11.35 waves of 74 pairs -> 11.5)
       const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
@@ -1019,8 +970,8 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
       int sp = (R && num_kb >= 128) ? std::min(4, n_clusters / R) : 1;
       while (sp > 1 && num_kb / sp < 8) --sp;
       if (sp > 1 && n_clusters <= FTB_TAIL_SLOTS) {
-        p.tail_flags = tail_flags_for(s);
-        if (p.tail_flags) p.tail_split = sp;
+        p.tail_flags = epi->tail_counters;
+        p.tail_split = sp;
       }
     }
     if (staged) return epg2 ? launch_gemm_pair<2, true>(ta, tb, p, s) : launch_gemm_pair<1, true>(ta, tb, p, s);

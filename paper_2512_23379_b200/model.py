@@ -141,7 +141,7 @@ class DeviceDenoiser:
     (dist.py): this rank owns tokens [start, start + Ls) of the padded chunk."""
 
     def __init__(self, weights: DeviceWeights, chunk_len, motion_len, latent_hw=(1, 1), stream=None, comm=None,
-                 fold_cross=True, fold_tc=True, fold_band=True):
+                 fold_cross=True, fold_band=True):
         from .dist import LocalComm, ShardPlan
         cfg = weights.cfg
         self.cfg, self.w = cfg, weights
@@ -186,26 +186,27 @@ class DeviceDenoiser:
             "e0": torch.empty(F, 6 * m, dtype=f32, device=d),
         }
         # folded cross-attention (wan): the projections fold through the chunk's fixed K/V
-        # (ops.xattn_fold) -> two m x (H*J) GEMMs per layer instead of two m x m ones
-        self.fold = cfg.mode == "wan" and self.n_cond <= 48 and fold_cross
+        # -> two m x (H*J) GEMMs per layer instead of two m x m ones. The fold runs on the
+        # tensor cores over block-diagonal K / V operands (zero off the diagonal); At rows are in
+        # the SEG_SOFTMAX tile order, so the logits GEMM's epilogue does the per-head softmax (no
+        # fp32 logits round trip, no separate softmax pass)
+        self.fold = cfg.mode == "wan" and self.n_cond <= 48 and fold_cross and m % 8 == 0
         if self.fold:
             self.J = round8(self.n_cond)
             HJ = cfg.heads * self.J
-            # tensor-core fold (default): block-diagonal K / V operands, zero off the diagonal;
-            # At rows in the SEG_SOFTMAX tile order, so the logits GEMM's epilogue does the
-            # per-head softmax (no fp32 logits round trip, no separate softmax pass)
-            self.fold_tc = fold_tc and m % 8 == 0
             self.fold_band = fold_band   # K loops of the fold GEMMs over the head bands only
             spt = 256 // self.J
-            at_rows = (cfg.heads + spt - 1) // spt * 256 if self.fold_tc else HJ
+            at_rows = (cfg.heads + spt - 1) // spt * 256
             self.buf["xat"] = torch.zeros(cfg.layers, at_rows, m, dtype=bf, device=d)
             self.buf["xbt"] = torch.empty(cfg.layers, m, HJ, dtype=bf, device=d)
-            if not self.fold_tc:
-                self.buf["xs"] = torch.empty(Ls, HJ, dtype=f32, device=d)
             self.buf["xp"] = torch.empty(Ls, HJ, dtype=bf, device=d)
-            if self.fold_tc:
-                self.buf["xkbd"] = torch.zeros(at_rows, m, dtype=bf, device=d)
-                self.buf["xvbd"] = torch.zeros(HJ, m, dtype=bf, device=d)
+            self.buf["xkbd"] = torch.zeros(at_rows, m, dtype=bf, device=d)
+            self.buf["xvbd"] = torch.zeros(HJ, m, dtype=bf, device=d)
+        # caller-owned kernel scratch (the library keeps none): the flash kernel's KV-split
+        # workspace and the split-K tail counters of the long-K residual GEMMs; every launch of
+        # this denoiser is ordered on its stream, so one copy each serves all of them
+        self.attn_ws = ops.attention_workspace(Lp, Lp, self.hpr, cfg.head_dim, d) if self.L > 128 else None
+        self.buf["tail_ctr"] = torch.zeros(ops.A.TAIL_COUNTER_WORDS, dtype=torch.int32, device=d)
         self.peer = g > 1 and getattr(self.comm, "peer", False)
         if self.peer:
             # symmetric receive buffers: the producers' epilogues store into them over NVLink
@@ -311,7 +312,7 @@ class DeviceDenoiser:
         ops.cast_f32_bf16(B["cond"], B["cond_bf"], stream=self.stream)
         for i in range(cfg.layers):
             ops.gemm(B["cond_bf"], W.mats["layers.%d.cross.wkv" % i][0], B["ckv"][i], "bf16", stream=self.stream)
-            if self.fold and self.fold_tc:
+            if self.fold:
                 # At = (scale * blockdiag K) . Wq^T and Bt = Wo^T . (blockdiag V)^T: two tensor-core
                 # GEMMs over the zero-padded block-diagonal operands; each tile's K loop covers only
                 # its rows' head bands (kbd rows in the SEG_SOFTMAX tile order: 256 // J heads per
@@ -325,11 +326,6 @@ class DeviceDenoiser:
                          algo_flops=fl)
                 ops.gemm(W.mats["layers.%d.cross.wo" % i][0], B["xvbd"], B["xbt"][i], "bf16", band=band_v,
                          stream=self.stream, algo_flops=fl)
-            elif self.fold:
-                p = "layers.%d." % i
-                ops.xattn_fold(B["ckv"][i], W.mats[p + "cross.wq"][0], W.mats[p + "cross.wo"][0], B["xat"][i],
-                               B["xbt"][i], self.n_cond, cfg.heads, cfg.head_dim, self.J, self.scale,
-                               stream=self.stream)
 
     def prepare_cond(self, signal, reference):
         """cond = [sig tokens + frame pos ; ref token] and per-layer cross K|V
@@ -378,17 +374,18 @@ class DeviceDenoiser:
                 rq = B["qkv_recv"]
                 self.comm.barrier(s)
                 ops.attention_scatter(rq[:, 0:hw], rq[:, hw:2 * hw], rq[:, 2 * hw:], hpr, hd, pl.L_pad, L,
-                                      self.scale, self._ao_peers, Ls, hw, stream=s)
+                                      self.scale, self._ao_peers, Ls, hw, workspace=self.attn_ws, stream=s)
                 self.comm.barrier(s)
                 o_in = dict(a=B["ao_recv"], M=Ls, K=m, lda=hw, a_chunks=g, a_chunk_stride=Ls * hw)
             elif g == 1:
-                ops.attention(qkv[:, 0:m], qkv[:, m:2 * m], qkv[:, 2 * m:], ao, H_, hd, L, L, self.scale, stream=s)
+                ops.attention(qkv[:, 0:m], qkv[:, m:2 * m], qkv[:, 2 * m:], ao, H_, hd, L, L, self.scale,
+                              workspace=self.attn_ws, stream=s)
                 o_in = dict(a=ao)
             else:
                 rq, af = B["qkv_recv"], B["attn_full"]
                 self.comm.all_to_all(rq, qkv, stream=s)                       # heads <- sequence
                 ops.attention(rq[:, 0:hw], rq[:, hw:2 * hw], rq[:, 2 * hw:], af, hpr, hd, pl.L_pad, L, self.scale,
-                              stream=s)
+                              workspace=self.attn_ws, stream=s)
                 self.comm.all_to_all(ao, af, stream=s)                        # sequence <- heads
                 o_in = dict(a=ao, M=Ls, K=m, lda=hw, a_chunks=g, a_chunk_stride=Ls * hw)
             if wan:
@@ -397,12 +394,8 @@ class DeviceDenoiser:
             else:
                 ops.gemm(o_in.pop("a"), W.mats[p + "self.wo"][0], h, "resid_f32", stream=s, **o_in)
             ops.norm_modulate(h, u, gamma=W.vecs[p + "ln2.g"], beta=W.vecs[p + "ln2.b"], stream=s)
-            if self.fold:   # S = U.At^T (f32) -> per-head softmax -> h += P.Bt^T
-                if self.fold_tc:   # logits GEMM with the per-head softmax in its epilogue
-                    ops.xattn_logits_softmax(u, B["xat"][i], B["xp"], H_, self.J, self.n_cond, stream=s)
-                else:
-                    ops.gemm(u, B["xat"][i], B["xs"], "f32", stream=s)
-                    ops.xattn_softmax(B["xs"], B["xp"], H_, self.J, self.n_cond, stream=s)
+            if self.fold:   # P = softmax_seg(U.At^T) (logits GEMM, softmax in its epilogue); h += P.Bt^T
+                ops.xattn_logits_softmax(u, B["xat"][i], B["xp"], H_, self.J, self.n_cond, stream=s)
                 ops.gemm(B["xp"], B["xbt"][i], h, "resid_f32", stream=s)
             else:
                 ops.gemm(u, W.mats[p + "cross.wq"][0], qkv[:, 0:m], "bf16", stream=s)
@@ -415,11 +408,13 @@ class DeviceDenoiser:
             else:
                 ops.norm_modulate(h, u, gamma=W.vecs[p + "ln3.g"], beta=W.vecs[p + "ln3.b"], stream=s)
             ops.gemm(u, W.mats[p + "ffn.w1"][0], ffb, "gelu_bf16", bias=W.vecs[p + "ffn.b1"], stream=s)
+            tail = B["tail_ctr"]
             if wan:
                 ops.gemm(ffb, W.mats[p + "ffn.w2"][0], h, "resid_f32", bias=W.vecs[p + "ffn.b2"],
-                         group_vec=md[:, 5 * m:6 * m], rows_per_group=T, row_offset=s0, stream=s)
+                         group_vec=md[:, 5 * m:6 * m], rows_per_group=T, row_offset=s0, stream=s, tail_counters=tail)
             else:
-                ops.gemm(ffb, W.mats[p + "ffn.w2"][0], h, "resid_f32", bias=W.vecs[p + "ffn.b2"], stream=s)
+                ops.gemm(ffb, W.mats[p + "ffn.w2"][0], h, "resid_f32", bias=W.vecs[p + "ffn.b2"], stream=s,
+                         tail_counters=tail)
         if wan:
             fm = fv["final"]
             ops.norm_modulate(h, u, shift=fm[:, 0:m], scale=fm[:, m:2 * m], rows_per_group=T, row_offset=s0, stream=s)

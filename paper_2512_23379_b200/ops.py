@@ -70,14 +70,18 @@ class RopeTables:
 
 def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=0, row_offset=0,
          M=None, K=None, lda=None, a_chunks=1, a_chunk_stride=0, heads=0, head_dim=0,
-         heads_per_rank=0, rope=None, peers=None, band=None, stream=None, algo_flops=None):
+         heads_per_rank=0, rope=None, peers=None, band=None, stream=None, algo_flops=None, variant=None,
+         tail_counters=None):
     """out <- epilogue(a[M,K] @ w_t[N,K]^T). `a` may be a raw buffer when
     a_chunks > 1 (Ulysses gather: M, K, lda, a_chunk_stride explicit).
     peers: device addresses (ints) for the peer-store epilogues (qkv_rope: one
     receive block per head group; f32: replicated all-gather); `out` then only
     fixes dtype/ldc.
     band: (side, rows, tile, per_tile, k) — the A (side 0) or B (side 1) operand is block
-    diagonal (ftb_epilogue.band_*); tiles skip the K blocks outside their rows' bands."""
+    diagonal (ftb_epilogue.band_*); tiles skip the K blocks outside their rows' bands.
+    variant: kernel selection of this call (ftb_epilogue.variant; None = FTB_GEMM_VARIANT or 0).
+    tail_counters: caller-owned int32 [TAIL_COUNTER_WORDS] zeroed buffer enabling the split-K
+    tail wave of long-K residual GEMMs (one buffer per stream of launches)."""
     _need(a, torch.bfloat16, "A")
     _need(w_t, torch.bfloat16, "W^T")
     N, Kw = w_t.shape
@@ -102,6 +106,12 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
                      heads, head_dim, heads_per_rank, C.pointer(rope.struct) if rope is not None else None)
     if band is not None:
         epi.band_side, epi.band_rows, epi.band_tile, epi.band_per_tile, epi.band_k = (int(x) for x in band)
+    epi.variant = A.GEMM_VARIANT if variant is None else int(variant)
+    epi.raster_group = A.GEMM_GROUP
+    if tail_counters is not None:
+        if tail_counters.dtype != torch.int32 or tail_counters.numel() < A.TAIL_COUNTER_WORDS:
+            raise ConfigError("tail_counters must be int32 with >= %d words" % A.TAIL_COUNTER_WORDS)
+        epi.tail_counters = tail_counters.data_ptr()
     if peers:
         if len(peers) > A.MAX_PEERS:
             raise ConfigError("at most %d peers" % A.MAX_PEERS)
@@ -135,22 +145,44 @@ def norm_modulate(x, out, *, gamma=None, beta=None, scale=None, shift=None, rows
     return out
 
 
-def attention(q, k, v, out, heads, head_dim, Lq, Lk, scale, *, impl=None, stream=None):
+def attention_workspace_bytes(Lq, Lk, heads, head_dim):
+    """fp32 workspace bytes of the flash kernel's KV-split tail round for this shape (0: none)."""
+    return int(A.lib.ftb_attention_workspace_bytes(int(Lq), int(Lk), int(heads), int(head_dim)))
+
+
+def attention_workspace(Lq, Lk, heads, head_dim, device):
+    """Caller-owned KV-split workspace (None when the shape has no split round or
+    FTB_ATTN_NO_SPLIT=1); pass it to every attention call of that shape on one stream."""
+    nb = attention_workspace_bytes(Lq, Lk, heads, head_dim) if A.ATTN_SPLIT else 0
+    return torch.empty(nb // 4, dtype=torch.float32, device=device) if nb else None
+
+
+def _ws(workspace):
+    if workspace is None:
+        return None, 0
+    _need(workspace, torch.float32, "workspace")
+    return A.ptr(workspace), workspace.numel() * 4
+
+
+def attention(q, k, v, out, heads, head_dim, Lq, Lk, scale, *, impl=None, workspace=None, stream=None):
     """q/k/v/out are 2-d views (rows, ld) whose head h lives at columns
-    [h*head_dim, (h+1)*head_dim)."""
+    [h*head_dim, (h+1)*head_dim). workspace: attention_workspace() of this shape (optional)."""
     for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
         _need(t, torch.bfloat16, nm)
     args = (A.ptr(q), _ld(q), A.ptr(k), _ld(k), A.ptr(v), _ld(v), A.ptr(out), _ld(out),
-            Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))
+            Lq, Lk, heads, head_dim, float(scale), *_ws(workspace), A.stream_ptr(stream))
     if impl is None:   # the library's dispatch (ftb_attention): short-KV tcgen05 kernel when Lk <= 128
         impl = (3 if Lk <= 128 else 0) if (head_dim in (64, 128) and Lq >= 64) else 1
-    kind = {0: "fmha", 2: "fmha", 3: "xattn"}.get(impl, "attn_small")
+    kind = {0: "fmha", 3: "xattn"}.get(impl, "attn_small")
     with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
         A.call("ftb_attention_impl", int(impl), *args)
+    if impl == 0 and workspace is not None:
+        A.LAUNCHES[0] += 1   # + fmha2_combine_kernel of the KV-split tail round
     return out
 
 
-def attention_scatter(q, k, v, heads, head_dim, Lq, Lk, scale, o_peers, peer_rows, ldo, *, stream=None):
+def attention_scatter(q, k, v, heads, head_dim, Lq, Lk, scale, o_peers, peer_rows, ldo, *, workspace=None,
+                      stream=None):
     """attention() whose output row r lands in row r % peer_rows of the buffer at
     device address o_peers[r // peer_rows] (Ulysses all-to-all #2 in the epilogue)."""
     for t, nm in ((q, "q"), (k, "k"), (v, "v")):
@@ -161,7 +193,10 @@ def attention_scatter(q, k, v, heads, head_dim, Lq, Lk, scale, o_peers, peer_row
     kind = "fmha" if Lk > 128 else "xattn"
     with _Prof(kind, 4.0 * Lq * Lk * heads * head_dim, 2.0 * heads * head_dim * (2 * Lq + 2 * Lk), stream):
         A.call("ftb_attention_scatter", A.ptr(q), _ld(q), A.ptr(k), _ld(k), A.ptr(v), _ld(v), arr, len(o_peers),
-               int(peer_rows), int(ldo), Lq, Lk, heads, head_dim, float(scale), A.stream_ptr(stream))
+               int(peer_rows), int(ldo), Lq, Lk, heads, head_dim, float(scale), *_ws(workspace),
+               A.stream_ptr(stream))
+    if Lk > 128 and workspace is not None:
+        A.LAUNCHES[0] += 1   # + fmha2_combine_kernel
 
 
 def peer_barrier(flag_ptrs, epoch, rank, world, timeout_s=30.0, *, stream=None):
@@ -233,17 +268,6 @@ def add_bcast(a, b, out, stream=None):
     return out
 
 
-def xattn_fold(kv, wq_t, wo_t, at, bt, n_cond, heads, head_dim, J, scale, *, stream=None):
-    """Fold the cross-attention projections through the chunk's fixed K/V (elementwise.cu):
-    at [heads*J][m] = scale * K_h . Wq_h^T,  bt [m][heads*J] = Wo_h^T . V_h^T (padded j -> 0)."""
-    for t, nm in ((kv, "kv"), (wq_t, "wq_t"), (wo_t, "wo_t"), (at, "at"), (bt, "bt")):
-        _need(t, torch.bfloat16, nm)
-    m = heads * head_dim
-    with _Prof("xattn_fold", 4.0 * n_cond * m * m, 0.0, stream):
-        A.call("ftb_xattn_fold", A.ptr(kv), _ld(kv), n_cond, heads, head_dim, J, A.ptr(wq_t), _ld(wq_t), A.ptr(wo_t),
-               _ld(wo_t), m, float(scale), A.ptr(at), A.ptr(bt), A.stream_ptr(stream))
-
-
 def xattn_blockdiag(kv, kbd, vbd, n_cond, heads, head_dim, J, scale, *, k_tiled=False, stream=None):
     """Diagonal blocks of the tensor-core fold operands (elementwise.cu): kbd[(h,j)][h*hd+d] =
     scale * K[j][h*hd+d], vbd likewise from V; the rest of kbd / vbd must already be zero.
@@ -279,12 +303,3 @@ def tiled_seg_rows(heads, J):
     h = torch.arange(heads).repeat_interleave(J)
     j = torch.arange(J).repeat(heads)
     return (h // spt) * 256 + (h % spt) * J + j
-
-
-def xattn_softmax(s, p, heads, J, n_cond, *, stream=None):
-    """Per-head softmax over J-column segments of s (f32) -> p (bf16), padded columns 0."""
-    _need(s, torch.float32, "s")
-    _need(p, torch.bfloat16, "p")
-    rows = s.shape[0]
-    with _Prof("xattn", 0.0, float(rows) * heads * J * 6, stream):
-        A.call("ftb_xattn_softmax", A.ptr(s), _ld(s), rows, heads, J, n_cond, A.ptr(p), _ld(p), A.stream_ptr(stream))

@@ -319,6 +319,7 @@ class DeviceVAEDecoder:
             halos = self._exchange_halos(L, inp, T_in, Cin)
         tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%d %d->%d k%d%d%d" % (
             T_out, H, W, Cin, cw.cout, kt, kh, kw)
+        mode = mode | (A.CONV_VARIANT << 8)   # kernel selection of this call (0 = auto; A/B runs)
         with ops._Prof(tag, 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
             if norm is not None:
                 gamma, nout, write_main = norm

@@ -1,19 +1,17 @@
-"""Norm + AdaLN variants at the 14B / 1.3B row shapes: time (CUDA events) and bit-equality.
-usage: python scripts/norm_bench.py [variants, default 0,1]"""
+"""Norm + AdaLN at the 14B / 1.3B row shapes: time (CUDA events) and achieved GB/s.
+usage: python scripts/norm_bench.py [--diag]"""
 import sys
 
 import torch
 
 sys.path.insert(0, ".")
-from paper_2512_23379_b200 import _capi as A  # noqa: E402
 from paper_2512_23379_b200 import ops  # noqa: E402
 from scripts.gemm_shapes import timeit  # noqa: E402
 
 
 def main():
     dev = torch.device("cuda")
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    variants = [int(v) for v in args[0].split(",")] if args else [0, 1]
+    variants = [0]
     L = 10530
     for m in (5120, 1536):
         h = torch.randn(L, m, device=dev) * 3 + 0.5
@@ -23,7 +21,6 @@ def main():
         b = torch.randn(m, device=dev)
         ref = None
         for var in variants:
-            A.call("ftb_set_norm_variant", var)
             u = torch.empty(L, m, device=dev, dtype=torch.bfloat16)
             cases = [("adaln", dict(shift=mod[:, :m], scale=mod[:, m:], rows_per_group=1170)),
                      ("affine", dict(gamma=g, beta=b))]
@@ -47,7 +44,6 @@ def main():
                     else:
                         same = "bit-equal" if torch.equal(ref, u) else "DIFF max %.3g" % (ref.float() - u.float()).abs().max()
                 print("m=%d var=%d %-6s %.1f us %.0f GB/s %s" % (m, var, tag, t * 1e3, byt / t / 1e6, same), flush=True)
-    A.call("ftb_set_norm_variant", 0)
 
 
 if __name__ == "__main__":

@@ -19,7 +19,7 @@ def main(which):
         out = torch.empty(L, 3 * m, device=dev, dtype=torch.bfloat16)
         groups = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0]
         for g in groups:
-            A.call("ftb_set_gemm_group", g)
+            A.GEMM_GROUP = g   # raster group of these calls (ftb_epilogue.raster_group)
             for _ in range(3):
                 ops.gemm(a, w, out, "bf16")
     if which in ("oproj", "ffn2", "xpb", "all"):
@@ -40,11 +40,8 @@ def main(which):
         h = torch.randn(L, m, device=dev)
         u = torch.empty(L, m, device=dev, dtype=torch.bfloat16)
         mod = torch.randn(10, 2 * m, device=dev)
-        variants = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0]
-        for var in variants:
-            A.call("ftb_set_norm_variant", var)
-            for _ in range(3):
-                ops.norm_modulate(h, u, shift=mod[:, :m], scale=mod[:, m:], rows_per_group=1170)
+        for _ in range(3):
+            ops.norm_modulate(h, u, shift=mod[:, :m], scale=mod[:, m:], rows_per_group=1170)
     if which in ("fmha", "all"):
         q = torch.randn(L, H * hd, device=dev).to(torch.bfloat16)
         o = torch.empty_like(q)

@@ -15,7 +15,7 @@ def main():
     from paper_2512_23379_b200 import _capi as A
     variants = [int(v) for v in sys.argv[1].split(",")] if len(sys.argv) > 1 else [0]
     for var, mode in [(v, "all") for v in variants] * 2:
-        A.call("ftb_set_conv_variant", var)
+        A.CONV_VARIANT = var   # conv mode bits 8-10 of every call (vae._conv)
         dec = DeviceVAEDecoder(VAEConfig(z_dim=16), dev, params=None, seed=201, rgb8=True, fuse_norm=mode)
         for _ in range(2):
             dec.decode_device_tensor(z, s)

@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "ftb2.h")
 
 def declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(ftb_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(ftb_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_header():
@@ -45,7 +45,7 @@ def test_error_mapping_without_gpu():
     from paper_2512_23379_b200.errors import ConfigError
     # argument validation happens before any device work
     with pytest.raises(ConfigError):
-        _capi.call("ftb_attention_impl", 0, None, 0, None, 0, None, 0, None, 0, 1, 1, 1, 64, 1.0, None)
+        _capi.call("ftb_attention_impl", 0, None, 0, None, 0, None, 0, None, 0, 1, 1, 1, 64, 1.0, None, 0, None)
 
 
 def test_struct_layouts_match_header(tmp_path):

@@ -62,3 +62,14 @@ def test_streaming_device_loader(cuda):
     wt, K = w.mats["in.w"]
     assert K == 9 and torch.equal(wt[:, :K].cpu(), torch.from_numpy(store.params["in.w"].T.copy()).to(torch.bfloat16))
     assert np.allclose(w.vecs["final.g"].cpu().numpy(), store.params["final.g"])
+
+
+@pytest.mark.parametrize("cut", [10, 300, 2000])
+def test_device_loader_truncated_raises_config_error(tmp_path, cut):
+    """A malformed file reaches the caller as ConfigError, not as the BufferError of closing a
+    still-exported mapping (the failure happens in validation, before any device copy)."""
+    blob = open(GOLD, "rb").read()
+    p = tmp_path / "trunc.ftlk"
+    p.write_bytes(blob[:-cut])
+    with pytest.raises(ConfigError):
+        CK.load_device_weights(p, device="cpu")

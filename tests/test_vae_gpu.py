@@ -38,7 +38,6 @@ CONV_CASES = [  # T_out, H, W, Cin, Cout, k
 @pytest.mark.parametrize("T,H,W,Cin,Cout,k", CONV_CASES)
 def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k, variant):
     from paper_2512_23379_b200 import _capi as A
-    A.call("ftb_set_conv_variant", variant)
     r = np.random.default_rng(T * 100 + W)
     kt = k[0]
     x = bfr(r.standard_normal((T + kt - 1, H, W, Cin)))
@@ -52,8 +51,7 @@ def test_conv3d_implicit_gemm(cuda, T, H, W, Cin, Cout, k, variant):
     rd = torch.as_tensor(resid).to(torch.bfloat16).to(cuda)
     out = torch.empty(T, H, W, Cout, dtype=torch.bfloat16, device=cuda)
     A.call("ftb_conv3d_bf16", A.ptr(xd), T + kt - 1, H, W, Cin, A.ptr(wt), Cout, *k, 0, A.ptr(bd), A.ptr(rd),
-           Cout, A.ptr(out), Cout, T, 0, A.stream_ptr())
-    A.call("ftb_set_conv_variant", 0)
+           Cout, A.ptr(out), Cout, T, variant << 8, A.stream_ptr())   # mode 0, kernel variant in bits 8-10
     assert rel(out.float().cpu().numpy(), want) < 8e-3
 
 
@@ -77,12 +75,8 @@ def test_conv3d_halo_rows_match_full_image(cuda, variant, H, r0, r1, C):
     wt = torch.as_tensor(np.transpose(w, (0, 2, 3, 4, 1)).reshape(C, -1)).to(torch.bfloat16).to(cuda).contiguous()
     bd = torch.as_tensor(b, dtype=torch.float32).to(cuda)
     out = torch.empty(T, r1 - r0, W, C, dtype=torch.bfloat16, device=cuda)
-    A.call("ftb_set_conv_variant", variant)
-    try:
-        A.call("ftb_conv3d_halo_bf16", A.ptr(xd), A.ptr(top), A.ptr(bot), T + kt - 1, r1 - r0, W, C, A.ptr(wt), C,
-               3, 3, 3, 0, A.ptr(bd), None, 0, A.ptr(out), C, T, 0, A.stream_ptr())
-    finally:
-        A.call("ftb_set_conv_variant", 0)
+    A.call("ftb_conv3d_halo_bf16", A.ptr(xd), A.ptr(top), A.ptr(bot), T + kt - 1, r1 - r0, W, C, A.ptr(wt), C,
+           3, 3, 3, 0, A.ptr(bd), None, 0, A.ptr(out), C, T, variant << 8, A.stream_ptr())
     assert rel(out.float().cpu().numpy(), want) < 8e-3
 
 
