@@ -119,19 +119,95 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+REF_KERNELS = ("dense_forward", "dense_backward", "gelu_forward", "gelu_backward", "layernorm_forward",
+               "layernorm_backward", "mha_forward", "mha_backward")
+
+
+def reference_tiny_chunks(n_chunks, backend):
+    """C1: the reference itself (ftlk installed in baseline/_ref, the Cython extension built
+    there), `metrics.rollout_stream` over `NetGenerator` (4-step ladder, NetConfig(), random
+    init) unpaced, plus the orthogonal codec decode of every chunk's targets — the engine's
+    per-chunk work (streaming.py:283-356). The kernel table is rebound to `backend` the way the
+    reference's own benchmark does it (benchmarks/bench_backends.py:65-90). Returns per-chunk
+    seconds (list) or raises ImportError when the reference is not installed."""
+    refdir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(refdir, "ftlk")):
+        raise ImportError("reference not installed in baseline/_ref")
+    if refdir not in sys.path:
+        sys.path.insert(0, refdir)
+    import ftlk.backends as K
+    from ftlk.diffusion import SamplerPlan
+    from ftlk.metrics import NetGenerator, StreamContext, rollout_stream
+    from ftlk.net import Denoiser, NetConfig
+    from ftlk.world import Codec
+    impl = K.get_backend(backend)
+    saved = {n: getattr(K, n) for n in REF_KERNELS}
+    for n in REF_KERNELS:
+        setattr(K, n, getattr(impl, n))
+    try:
+        cfg = NetConfig()
+        store = Denoiser(cfg).init_params(200)
+        gen = NetGenerator(store, cfg, SamplerPlan())
+        r = np.random.default_rng(0)
+        codec = Codec(np.linalg.qr(r.standard_normal((cfg.latent_dim, cfg.latent_dim)))[0])
+        times = []
+        inner = gen.chunk
+
+        def timed(ctx, c, motion, sig, rng):
+            t0 = time.perf_counter()
+            ch = inner(ctx, c, motion, sig, rng)
+            codec.decode(ch.targets)
+            times.append(time.perf_counter() - t0)
+            return ch
+        gen.chunk = timed
+        ident = r.standard_normal(cfg.latent_dim)
+        ctx = StreamContext(0, 0, ident, r.uniform(-1, 1, 7 * n_chunks), ident, codec.encode(ident))
+        rollout_stream(gen, ctx, 7 * n_chunks)
+        return times
+    finally:
+        for n, fn in saved.items():
+            setattr(K, n, fn)
+
+
 def reference_arm(args):
-    """CPU reference path (the oracle port of the reference's NumPy fp64 path),
-    rank 0 only, each step a bounded layer sample extrapolated to one chunk."""
+    """CPU reference path, rank 0 only (other ranks exit without work).
+    tiny (C1): the reference itself, rollout_stream unpaced on both of its backends
+    (python = NumPy, cython = its compiled extension), median chunk over >= 200 chunks per step.
+    wan shapes: the oracle port of the reference's NumPy fp64 path, each step one layer on one
+    latent frame of tokens extrapolated to the chunk (infeasible in full on a host)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.cpu_baseline import extrapolated_chunk_seconds, make_layer
     from paper_2512_23379_b200 import config as C
     cfg = getattr(C, MODELS[args.model])
+    if args.model == "tiny":
+        per_step, det = [], {}
+        for i in range(args.warmup + args.steps):
+            t = reference_tiny_chunks(200, "cython")
+            if i >= args.warmup:
+                per_step.append(float(np.median(t)))
+        det["cython_chunk_ms_median"] = 1000.0 * float(np.median(per_step))
+        det["python_chunk_ms_median"] = 1000.0 * float(np.median(reference_tiny_chunks(200, "python")))
+        chunk_s = float(np.median(per_step))
+        fps = 7.0 / chunk_s
+        cb = {"value": fps, "unit": "FPS", "cores": 1, "kind": "reference",
+              "sample": "ftlk rollout_stream (NetGenerator, 4-step ladder) + Codec.decode, unpaced, cython "
+                        "backend, median chunk of 200 per step (python backend: %.2f ms/chunk)" %
+                        det["python_chunk_ms_median"]}
+        line = {"metric": "streaming FPS (tiny ftlk-shape DiT, 4-step chunk, 7 frames/chunk)", "value": fps,
+                "unit": "FPS", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": chunk_s * 1000.0, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_name(args), "model": args.model}, "cpu_baseline": cb,
+                "e2e": {"value": fps, "unit": "FPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "detail": det}
+        print(json.dumps(line), flush=True)
+        return
+    from oracle.cpu_baseline import extrapolated_chunk_seconds, make_layer
     H, W = C.BUCKETS[args.bucket]
     T = (H // 16) * (W // 16)
     L = 9 * T
-    L_s = max(16, T // 5)
+    L_s = T       # one latent frame of tokens
     P = make_layer(cfg.model_dim, cfg.ff_dim)
     times, det = [], None
     for i in range(args.warmup + args.steps):
@@ -142,10 +218,12 @@ def reference_arm(args):
     chunk_s = float(np.median(times))
     fps = 28.0 / chunk_s
     cb = {"value": fps, "unit": "FPS", "cores": os.cpu_count(), "kind": "port",
-          "sample": "one %s-width wan layer fwd (fp64 NumPy oracle) on %d of %d tokens, extrapolated "
-                    "linear x L/Ls + attention x (L/Ls)^2 to %d layers x 4 steps; DiT only" %
-                    (args.model, L_s, L, cfg.layers)}
-    line = {"metric": "streaming FPS (14B-shape DiT, 4-step chunk, 28 frames/chunk)", "value": fps, "unit": "FPS",
+          "sample": "one %s-width wan layer fwd (fp64 NumPy oracle) on one latent frame (%d of %d tokens), "
+                    "self-attention core timed on %d of %d heads; extrapolated linear x L/Ls + attention x "
+                    "(L/Ls)^2 to %d layers x 4 steps; DiT only" %
+                    (args.model, L_s, L, det["attn_heads_timed"], cfg.heads, cfg.layers)}
+    line = {"metric": "streaming FPS (%s-shape DiT, 4-step chunk, 28 frames/chunk)" % (
+                {"14b": "14B", "1.3b": "1.3B"}[args.model]), "value": fps, "unit": "FPS",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": chunk_s * 1000.0, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": {"workload": workload_name(args), "model": args.model},
@@ -195,6 +273,8 @@ def pick_comm(args, w, Lc, Lm, lat_hw, stream, dev):
 
 
 def workload_name(args):
+    if args.model == "tiny":   # C1: the reference's default NetConfig (9 tokens, no spatial grid)
+        return "stream_chunk_tiny_ftlk_Lc9_Lm2_4step"
     return "stream_chunk_%s_%s_Lc9_Lm2_4step" % (args.model, args.bucket)
 
 
@@ -263,7 +343,13 @@ def main():
     vae = None
     if cfg.mode == "wan" and not args.no_decode:   # N > 1: spatially split decode with halo exchange
         from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig
-        vae = DeviceVAEDecoder(VAEConfig(z_dim=cfg.latent_dim), dev, params=None, seed=201, rgb8=True, comm=comm)
+        # the decode has its own channel (barrier flags / process group): in the engine it runs on
+        # the decode stream concurrently with the denoise stream's Ulysses barriers
+        vae = DeviceVAEDecoder(VAEConfig(z_dim=cfg.latent_dim), dev, params=None, seed=201, rgb8=True,
+                               comm=comm.channel("vae") if comm is not None else None)
+    elif not args.no_decode:                       # ftlk (C1): the reference's orthogonal codec
+        from paper_2512_23379_b200.codec import Codec
+        vae = Codec(np.linalg.qr(np.random.default_rng(0).standard_normal((cfg.latent_dim, cfg.latent_dim)))[0])
 
     from paper_2512_23379_b200.streaming import DeviceStreamer
 
@@ -305,9 +391,9 @@ def main():
             dstream.wait_stream(stream)
         if mark:
             ev[2].record(dstream)
-        if vae is not None:
+        if vae is not None:   # N > 1: the decoded slabs are gathered into rank 0's frames
             with torch.cuda.stream(dstream):
-                vae.decode_device_tensor(x0, dstream)
+                vae.decode_device_tensor(x0, dstream, gather=True)
             if overlap:
                 freed[c & 1] = torch.cuda.Event()
                 freed[c & 1].record(dstream)
@@ -360,8 +446,9 @@ def main():
             if vae is not None:
                 # decoded uint8 frames -> pinned host slot c%2; the host waits for chunk c-1's
                 # frames (not chunk c's), so it enqueues chunk c+1 while chunk c runs
-                frames, ev = vae.decode_device_async(xo, stream, c & 1)
-                pending.append((frames, ev))
+                frames, ev = vae.decode_device_async(xo, stream, c & 1, gather=True)
+                if frames is not None:     # rank 0 receives the full frames
+                    pending.append((frames, ev))
                 if len(pending) > 1:
                     f, e = pending.pop(0)
                     e.synchronize()
@@ -398,7 +485,7 @@ def main():
     ds.d.buf["cond_in"].copy_(cond_all[nsteps - 1])
     ds._device_chunk()                      # eager: every launch bracketed by events
     if vae is not None:
-        vae.decode_device_tensor(ds.x0_static, stream)
+        vae.decode_device_tensor(ds.x0_static, stream, gather=True)
     torch.cuda.synchronize()
     prof = ops.PROFILER
     ops.PROFILER = None
@@ -452,12 +539,21 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.mode == "wan":
         from oracle.cpu_baseline import extrapolated_chunk_seconds
         T = d.T
-        chunk_s, det = extrapolated_chunk_seconds(cfg.model_dim, cfg.heads, cfg.ff_dim, cfg.layers, 4, d.L,
-                                                  max(16, T // 5))
+        chunk_s, det = extrapolated_chunk_seconds(cfg.model_dim, cfg.heads, cfg.ff_dim, cfg.layers, 4, d.L, T)
         cpu = {"value": frames_per_chunk / chunk_s, "unit": "FPS", "cores": os.cpu_count(), "kind": "port",
-               "sample": "one %s-width wan layer fwd (fp64 NumPy oracle) on %d of %d tokens, extrapolated to "
-                         "%d layers x 4 steps (DiT only)" % (args.model, det["L_sample"], d.L, cfg.layers),
+               "sample": "one %s-width wan layer fwd (fp64 NumPy oracle) on one latent frame (%d of %d tokens), "
+                         "self-attention core on %d of %d heads, extrapolated to %d layers x 4 steps (DiT only)" % (
+                             args.model, det["L_sample"], d.L, det["attn_heads_timed"], cfg.heads, cfg.layers),
                "chunk_seconds": chunk_s}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            t = reference_tiny_chunks(200, "cython")
+            chunk_s = float(np.median(t))
+            cpu = {"value": frames_per_chunk / chunk_s, "unit": "FPS", "cores": 1, "kind": "reference",
+                   "sample": "ftlk rollout_stream + Codec.decode (baseline/_ref, cython backend), median of 200 "
+                             "chunks", "chunk_seconds": chunk_s}
+        except ImportError as e:
+            cpu = {"value": None, "unit": "FPS", "cores": 0, "kind": "reference", "sample": "unavailable: %s" % e}
 
     if rank == 0:
         line = {"metric": "streaming FPS (%s-shape DiT, 4-step chunk, %d frames/chunk)" % (

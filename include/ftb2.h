@@ -170,6 +170,10 @@ int ftb_ipc_import(const uint8_t* handle, void** ptr);
 int ftb_ipc_close(void* ptr);
 /* Stream-ordered device-to-device copy (peer-mapped destinations: VAE halo rows). */
 int ftb_copy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+/* Stream-ordered strided device-to-device copy of `height` rows of `width` bytes (pitches in
+ * bytes): a VAE row slab [T][rows][W][3] into rank 0's peer-mapped full frames [T][H][W][3]. */
+int ftb_copy_d2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                    void* stream);
 /* Stream-ordered barrier over `world` ranks: flags[i] = rank i's [world] u32 flag words
  * (peer-mapped), epoch = this rank's device counter (incremented per call, so the barrier
  * is CUDA-graph capturable). Fences prior stores system-wide, signals every rank, then
@@ -200,6 +204,12 @@ int ftb_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream);
 int ftb_patchify_composite(const float* motion, const float* z, const float* reference,
                            int32_t Lm, int32_t Lc, int32_t D, int32_t H, int32_t W,
                            int32_t ph, int32_t pw, void* out, int64_t ldo, void* stream);
+
+/* Same token layout from an arbitrary stacked composite f32 [Lc][C][H][W] (C = 2D+1 channels
+ * z_noise | z_mask | z_cond as given: non-canonical masks / conditioning rows,
+ * diffusion.py:89-135 CompositeInput, consumed by net.py:223-238). */
+int ftb_patchify_stacked(const float* stacked, int32_t Lc, int32_t C, int32_t H, int32_t W, int32_t ph, int32_t pw,
+                         void* out, int64_t ldo, void* stream);
 
 /* x0 tokens f32 [Lc*T][ldx] (feature (c*ph+py)*pw+px) -> target frames.
  * x0_out [Lc-Lm][D][H][W] = x0 of frames >= Lm; if update:

@@ -58,12 +58,14 @@ _SIGS = {
     "ftb_ipc_close": ([vp], i32),
     "ftb_peer_barrier": ([C.POINTER(vp), vp, i32, i32, C.c_double, vp], i32),
     "ftb_copy_d2d": ([vp, vp, C.c_size_t, vp], i32),
+    "ftb_copy_d2d_2d": ([vp, C.c_size_t, vp, C.c_size_t, C.c_size_t, C.c_size_t, vp], i32),
     "ftb_xattn_blockdiag": ([vp, i64, i32, i32, i32, i32, f32, vp, vp, i64, i32, vp], i32),
     "ftb_gelu_bf16": ([vp, vp, i64, vp], i32),
     "ftb_silu_f32_to_bf16": ([vp, vp, i64, vp], i32),
     "ftb_cast_f32_bf16": ([vp, vp, i64, vp], i32),
     "ftb_cast_bf16_f32": ([vp, vp, i64, vp], i32),
     "ftb_patchify_composite": ([vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, i64, vp], i32),
+    "ftb_patchify_stacked": ([vp, i32, i32, i32, i32, i32, i32, vp, i64, vp], i32),
     "ftb_unpatch_ddim": ([vp, i64, i32, i32, i32, i32, i32, i32, i32, vp, vp, f32, f32, f32, f32, i32, vp], i32),
     "ftb_codec_decode": ([vp, vp, vp, i32, i32, vp], i32),
     "ftb_fill_normal_bf16": ([vp, i64, u64, f32, vp], i32),

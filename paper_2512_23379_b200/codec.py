@@ -43,25 +43,42 @@ class Codec:
             raise ConfigError("latent dimension does not match codec")
         return latents @ self.Q
 
-    def decode_device(self, latents_dev, stream):
-        """latents_dev: device fp32 (n, D[,1,1]) -> host float64 frames (n, D)."""
+    def _bufs(self, lat, slot=0):
         D = self.Q.shape[0]
-        lat = latents_dev.reshape(-1, D)
-        n = lat.shape[0]
-        dev = lat.device
+        n, dev = lat.shape[0], lat.device
         Qd = self._dev.get(dev)
         if Qd is None:
             Qd = torch.as_tensor(self.Q, dtype=torch.float32).to(dev)
             self._dev[dev] = Qd
-        key = (dev, n)
+        key = (dev, n, slot)
         bufs = self._pinned.get(key)
         if bufs is None:
             bufs = (torch.empty(n, D, dtype=torch.float32, device=dev),
                     torch.empty(n, D, dtype=torch.float32).pin_memory())
             self._pinned[key] = bufs
-        out, host = bufs
+        return Qd, bufs
+
+    def decode_device_tensor(self, latents_dev, stream=None, gather=False, slot=0):
+        """latents_dev: device fp32 (n, D[,1,1]) -> device fp32 frames (n, D) (replicated decode:
+        the codec is per frame, so `gather` has nothing to collect)."""
+        lat = latents_dev.reshape(-1, self.Q.shape[0])
+        Qd, (out, _) = self._bufs(lat, slot)
         ops.codec_decode(lat, Qd, out, stream=stream)
+        return out
+
+    def decode_device_async(self, latents_dev, stream, slot=0, gather=False):
+        """Decode + D2H into pinned buffer `slot`, enqueued on `stream`: (host tensor, event)."""
+        lat = latents_dev.reshape(-1, self.Q.shape[0])
+        _, (out, host) = self._bufs(lat, slot)
+        self.decode_device_tensor(latents_dev, stream, slot=slot)
         with torch.cuda.stream(stream):
             host.copy_(out, non_blocking=True)
-        stream.synchronize()
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        return host, ev
+
+    def decode_device(self, latents_dev, stream):
+        """latents_dev: device fp32 (n, D[,1,1]) -> host float64 frames (n, D)."""
+        host, ev = self.decode_device_async(latents_dev, stream)
+        ev.synchronize()
         return host.numpy().astype(np.float64)

@@ -170,6 +170,31 @@ __global__ void patchify_kernel(const float* __restrict__ motion, const float* _
   }
 }
 
+// Patchify of an arbitrary stacked composite [Lc][C][H][W] (the caller's own z_mask / z_cond
+// rows: any CompositeInput the reference's Denoiser.forward accepts, net.py:223-238).
+__global__ void patchify_stacked_kernel(const float* __restrict__ st, int Lc, int C, int H, int W, int ph, int pw,
+                                        __nv_bfloat16* __restrict__ out, long long ldo, long long total) {
+  const int gh = H / ph, gw = W / pw;
+  const long long tpf = (long long)gh * gw;
+  const int F = C * ph * pw;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long tok = i / ldo;
+    const int feat = (int)(i - tok * ldo);
+    float v = 0.f;
+    if (feat < F) {
+      const int f = (int)(tok / tpf);
+      const int rem = (int)(tok - f * tpf);
+      const int ty = rem / gw, tx = rem - (rem / gw) * gw;
+      const int c = feat / (ph * pw);
+      const int pr = feat - c * ph * pw;
+      const int py = pr / pw, px = pr - (pr / pw) * pw;
+      v = st[(((long long)f * C + c) * H + ty * ph + py) * W + tx * pw + px];
+    }
+    out[i] = __float2bfloat16_rn(v);
+  }
+}
+
 // x0 tokens -> target-frame latents; DDIM update of the sampler state
 // (diffusion.py:229-236): eps = (z - a_i x0)/s_i ; z = a_n x0 + s_n eps.
 __global__ void unpatch_ddim_kernel(const float* __restrict__ x0t, long long ldx, int Lm, int Lc, int D, int H,
@@ -344,6 +369,17 @@ extern "C" int ftb_patchify_composite(const float* motion, const float* z, const
   patchify_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(motion, z, reference, Lm, Lc, D, H, W, ph, pw,
                                                                (__nv_bfloat16*)out, ldo, total);
   return check_launch("patchify_kernel");
+}
+
+extern "C" int ftb_patchify_stacked(const float* stacked, int32_t Lc, int32_t C, int32_t H, int32_t W, int32_t ph,
+                                    int32_t pw, void* out, int64_t ldo, void* stream) {
+  if (!stacked || !out || Lc <= 0 || C <= 0 || ph <= 0 || pw <= 0 || H % ph || W % pw)
+    return set_error(FTB_EINVAL, "patchify_stacked: bad arguments");
+  if (ldo < (int64_t)C * ph * pw) return set_error(FTB_EINVAL, "patchify_stacked: ldo too small");
+  const long long total = (long long)Lc * (H / ph) * (W / pw) * ldo;
+  patchify_stacked_kernel<<<grid_for(total, 256), 256, 0, S(stream)>>>(stacked, Lc, C, H, W, ph, pw,
+                                                                      (__nv_bfloat16*)out, ldo, total);
+  return check_launch("patchify_stacked_kernel");
 }
 
 extern "C" int ftb_unpatch_ddim(const float* x0_tok, int64_t ldx, int32_t Lm, int32_t Lc, int32_t D, int32_t H,

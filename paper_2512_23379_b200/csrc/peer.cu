@@ -61,6 +61,15 @@ extern "C" int ftb_copy_d2d(void* dst, const void* src, size_t bytes, void* stre
   return e == cudaSuccess ? FTB_OK : set_cuda_error(e, "copy_d2d");
 }
 
+extern "C" int ftb_copy_d2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                               void* stream) {
+  if (!dst || !src || width > dpitch || width > spitch) return set_error(FTB_EINVAL, "copy_d2d_2d: bad arguments");
+  if (!width || !height) return FTB_OK;
+  cudaError_t e = cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToDevice,
+                                    reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FTB_OK : set_cuda_error(e, "copy_d2d_2d");
+}
+
 struct BarrierParams {
   uint32_t* flags[FTB_MAX_PEERS];  // rank i's flag words [world]; flags[i][r] = last epoch rank r signalled i
   uint32_t* epoch;                 // this rank's local epoch counter (device word)

@@ -29,6 +29,13 @@ Two transports:
     torch.distributed, device flag barrier); `ThreadPeerComm` runs g emulated ranks
     on one device (peer addresses are the other ranks' buffers, barrier on the host)
     so the fused layouts are tested without kernels that wait on one another.
+
+Channels. A communicator's exchanges are ordered on ONE stream (its barrier epoch / collective
+sequence). Work that runs concurrently on another stream or thread — the VAE decode on the
+engine's decode stream, the host-side input broadcast of the ingest thread — takes its own
+channel: `comm.channel(name)` (same transport, independent barrier flags and epoch, or its own
+process group) and `comm.host_channel(name)` (host objects: `host_broadcast`). Channels are
+created collectively (every rank, same order, from the main thread).
 """
 
 import threading
@@ -36,6 +43,14 @@ import threading
 import torch
 
 from .errors import ConfigError
+
+
+def slab_rows(h, world):
+    """Row slab sizes of a spatial split of h rows over `world` ranks (first h % world ranks
+    get one more row); the VAE decoder and the frame gather use the same partition."""
+    if h < world:
+        raise ConfigError("latent height %d cannot be split over %d ranks" % (h, world))
+    return [h // world + (1 if i < h % world else 0) for i in range(world)]
 
 
 class ShardPlan:
@@ -73,6 +88,18 @@ class LocalComm:
     def all_gather(self, out, inp, stream=None):
         out.copy_(inp)
 
+    def channel(self, name):
+        return self
+
+    def host_channel(self, name):
+        return self
+
+    def host_broadcast(self, obj, src=0):
+        return obj
+
+    def gather_rows(self, full_name, full, slab, sizes, stream=None):
+        full.copy_(slab)
+
 
 def _on(stream):
     import contextlib
@@ -100,6 +127,35 @@ class TorchComm:
         with _on(stream):
             self.dist.all_gather_into_tensor(out.reshape(-1), inp.reshape(-1), group=self.group)
 
+    def channel(self, name):
+        """Independent process group over the same ranks (collective: call on every rank)."""
+        return TorchComm(self.dist.new_group(ranks=list(range(self.world))))
+
+    def host_channel(self, name):
+        """gloo group for host objects (the ingest thread's per-chunk input broadcast)."""
+        return TorchComm(self.dist.new_group(ranks=list(range(self.world)), backend="gloo"))
+
+    def host_broadcast(self, obj, src=0):
+        lst = [obj]
+        self.dist.broadcast_object_list(lst, src=src, group=self.group)
+        return lst[0]
+
+    def gather_rows(self, full_name, full, slab, sizes, stream=None):
+        """Row slabs [T][rows_r][...] of every rank -> rank 0's full [T][sum(rows)][...]
+        (slabs padded to the largest; only rank 0's `full` is written)."""
+        mx = max(sizes)
+        T, rows = slab.shape[0], slab.shape[1]
+        with _on(stream):
+            pad = torch.zeros((T, mx) + tuple(slab.shape[2:]), dtype=slab.dtype, device=slab.device)
+            pad[:, :rows].copy_(slab)
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            self.dist.all_gather(parts, pad, group=self.group)
+            if self.rank == 0:
+                r0 = 0
+                for r, n in enumerate(sizes):
+                    full[:, r0:r0 + n].copy_(parts[r][:, :n])
+                    r0 += n
+
     def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
         """Spatial-split halo swap: my first row -> rank-1 (its bottom halo), my last
         row -> rank+1 (its top halo); global edges receive zeros."""
@@ -125,6 +181,17 @@ class _ThreadHub:
         self.world = world
         self.barrier = threading.Barrier(world)
         self.slots = [None] * world
+        self.sym = {}
+        self._subs = {}
+        self._lock = threading.Lock()
+
+    def sub(self, name):
+        """The hub of channel `name` (created by whichever rank asks first)."""
+        with self._lock:
+            h = self._subs.get(name)
+            if h is None:
+                h = self._subs[name] = _ThreadHub(self.world)
+            return h
 
 
 class ThreadComm:
@@ -168,6 +235,34 @@ class ThreadComm:
             for src in range(g):
                 ov[src].copy_(self.hub.slots[src].reshape(-1))
         self._exchange(out, inp, stream, pick)
+
+    def channel(self, name):
+        return ThreadComm(self.hub.sub(name), self.rank)
+
+    def host_channel(self, name):
+        return ThreadComm(self.hub.sub("host:" + name), self.rank)
+
+    def host_broadcast(self, obj, src=0):
+        if self.rank == src:
+            self.hub.slots[src] = obj
+        self.hub.barrier.wait()
+        out = self.hub.slots[src]
+        self.hub.barrier.wait()
+        return out
+
+    def gather_rows(self, full_name, full, slab, sizes, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        s.synchronize()
+        self.hub.slots[self.rank] = slab
+        self.hub.barrier.wait()
+        if self.rank == 0:
+            with torch.cuda.stream(s):
+                r0 = 0
+                for r, n in enumerate(sizes):
+                    full[:, r0:r0 + n].copy_(self.hub.slots[r])
+                    r0 += n
+            s.synchronize()
+        self.hub.barrier.wait()
 
     def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream()
@@ -262,9 +357,31 @@ class PeerComm:
                 recv_bot.zero_()
         self.barrier(s)
 
+    def gather_rows(self, full_name, full, slab, sizes, stream=None):
+        """Row slabs of every rank -> rank 0's symmetric buffer `full_name` ([T][H][...], H =
+        sum(sizes)): each rank stores its slab rows straight into rank 0's frames over NVLink
+        (one strided peer copy: T rows of rows*rowbytes), between two barriers (rank 0 has
+        consumed the previous frames / the stores are visible)."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        T, rows = slab.shape[0], slab.shape[1]
+        row_b = slab[0, 0].numel() * slab.element_size()
+        H = sum(sizes)
+        row0 = sum(sizes[:self.rank])
+        self.barrier(s)
+        _copy_2d_to_peer(self._addrs[full_name][0] + row0 * row_b, H * row_b, slab, rows * row_b, rows * row_b, T,
+                         s)
+        self.barrier(s)
+
     # collective fallbacks used outside the fused path (VAE halo, tests)
     def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
         raise NotImplementedError
+
+
+def _copy_2d_to_peer(dst_addr, dpitch, src, spitch, width, height, stream):
+    import ctypes as C
+    from . import _capi as A
+    A.call("ftb_copy_d2d_2d", C.c_void_p(int(dst_addr)), C.c_size_t(int(dpitch)), C.c_void_p(src.data_ptr()),
+           C.c_size_t(int(spitch)), C.c_size_t(int(width)), C.c_size_t(int(height)), A.stream_ptr(stream))
 
 
 def _copy_to_peer(dst_addr, src, nbytes, stream):
@@ -288,8 +405,13 @@ class ThreadPeerComm(PeerComm):
     @staticmethod
     def make(world):
         hub = _ThreadHub(world)
-        hub.sym = {}
         return [ThreadPeerComm(hub, r) for r in range(world)]
+
+    def channel(self, name):
+        return ThreadPeerComm(self.hub.sub(name), self.rank)
+
+    def host_channel(self, name):
+        return ThreadComm(self.hub.sub("host:" + name), self.rank)
 
     def sym(self, name, shape, dtype, device):
         t = torch.zeros(shape, dtype=dtype, device=device)
@@ -364,6 +486,16 @@ class IpcPeerComm(PeerComm):
 
     def neighbor_exchange(self, *a, **k):
         self._coll.neighbor_exchange(*a, **k)
+
+    def channel(self, name):
+        """Same ranks, own process group, own flag words and epoch counter (a barrier stream of
+        its own: the engine's decode stream runs the VAE halo barriers concurrently with the
+        DiT barriers on the denoise stream)."""
+        grp = self.dist.new_group(ranks=list(range(self.world)))
+        return IpcPeerComm(self.device, group=grp, timeout_s=self.timeout_s, barrier_mode=self.barrier_mode)
+
+    def host_channel(self, name):
+        return TorchComm(self.dist.new_group(ranks=list(range(self.world)), backend="gloo"))
 
     def close(self):
         from . import _capi as A

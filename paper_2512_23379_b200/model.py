@@ -335,11 +335,13 @@ class DeviceDenoiser:
         self.upload_cond()
 
     # ------------------------------------------------------------ one denoise step
-    def step(self, motion, z, reference, fv, x0_out=None, ddim=None):
+    def step(self, motion, z, reference, fv, x0_out=None, ddim=None, stacked=None):
         """One Denoiser.forward on device. motion [L_m, D, H, W], z [L_c-L_m, D, H, W],
         reference [D, H, W] (fp32 device). Writes x0 tokens to buf['x0tok'] (all L
         tokens on every rank); if x0_out is given, also unpatchifies the target frames
-        (and applies the DDIM update to z when ddim=(a_i, s_i, a_n, s_n))."""
+        (and applies the DDIM update to z when ddim=(a_i, s_i, a_n, s_n)).
+        stacked: an explicit composite [L_c][2D+1][H][W] (f32 device) instead of the canonical
+        one assembled from motion / z / reference (any z_mask / z_cond rows)."""
         cfg, B, W = self.cfg, self.buf, self.w
         m, H_, hd = cfg.model_dim, cfg.heads, cfg.head_dim
         L, T, s = self.L, self.T, self.stream
@@ -347,8 +349,11 @@ class DeviceDenoiser:
         s0, Ls, g, hpr = pl.start, pl.Ls, pl.world, self.hpr
         hw = hpr * hd
         D = cfg.latent_dim
-        ops.patchify(motion, z, reference, self.Lm, self.Lc, D, self.H, self.W, self.ph, self.pw, B["tok"][:L],
-                     stream=s)
+        if stacked is not None:
+            ops.patchify_stacked(stacked, self.ph, self.pw, B["tok"][:L], stream=s)
+        else:
+            ops.patchify(motion, z, reference, self.Lm, self.Lc, D, self.H, self.W, self.ph, self.pw, B["tok"][:L],
+                         stream=s)
         h = B["h"]
         tok = B["tok"][s0:s0 + Ls]
         wan = cfg.mode == "wan"

@@ -80,11 +80,14 @@ class ParamStore:
 
 
 class _DeviceRunner:
-    """Device weights of one ParamStore + per-geometry DeviceDenoiser cache."""
+    """Device weights of one ParamStore + per-geometry DeviceDenoiser cache. With a
+    communicator (dist.py) the denoisers run Ulysses sequence parallel over its ranks; every
+    rank holds the same runner (replicated weights and sampler state)."""
 
-    def __init__(self, cfg, store, device):
+    def __init__(self, cfg, store, device, comm=None):
         self.cfg = cfg
         self.device = torch.device(device)
+        self.comm = comm
         self.weights = DeviceWeights.from_host(cfg, store.params, self.device)
         self._geo = {}
         self.stream = None
@@ -93,7 +96,7 @@ class _DeviceRunner:
         key = (lc, lm, tuple(hw))
         d = self._geo.get(key)
         if d is None:
-            d = DeviceDenoiser(self.weights, lc, lm, hw, stream=self.stream)
+            d = DeviceDenoiser(self.weights, lc, lm, hw, stream=self.stream, comm=self.comm)
             self._geo[key] = d
         return d
 
@@ -111,19 +114,20 @@ class _DeviceRunner:
         lc, lm = comp.chunk_len, comp.motion_len
         if comp.latent_dim != cfg.latent_dim:
             raise ConfigError("composite latent dim %d != net latent dim %d" % (comp.latent_dim, cfg.latent_dim))
-        mask_ok = comp.z_mask[0] == 1.0 and not np.any(comp.z_mask[1:])
-        cond_ok = np.array_equal(comp.z_cond[0], comp.reference) and not np.any(comp.z_cond[1:])
-        if not (mask_ok and cond_ok):
-            raise ConfigError("composite must be canonical (z_mask=[1,0..], z_cond=[reference,0..]), "
-                              "as built by composite_from_state")
         d = self._geometry(comp.z_noise.shape, lc, lm)
         fshape = (d.cfg.latent_dim, d.H, d.W)
-        motion = self._dev(comp.z_noise[:lm], (lm,) + fshape) if lm else None
-        z = self._dev(comp.z_noise[lm:], (lc - lm,) + fshape)
-        ref = self._dev(comp.reference, fshape)
+        mask_ok = comp.z_mask[0] == 1.0 and not np.any(comp.z_mask[1:])
+        cond_ok = np.array_equal(comp.z_cond[0], comp.reference) and not np.any(comp.z_cond[1:])
         d.prepare_cond(comp.signal, comp.reference)
         fv = d.frame_vectors(comp.frame_t)
-        x0t = d.step(motion, z, ref, fv)
+        if mask_ok and cond_ok:   # Eq.1 assembled on device from motion / z / reference
+            motion = self._dev(comp.z_noise[:lm], (lm,) + fshape) if lm else None
+            z = self._dev(comp.z_noise[lm:], (lc - lm,) + fshape)
+            ref = self._dev(comp.reference, fshape)
+            x0t = d.step(motion, z, ref, fv)
+        else:                     # any other composite (own mask / conditioning rows): upload it whole
+            st = self._dev(comp.stacked(), (lc, 2 * d.cfg.latent_dim + 1, d.H, d.W))
+            x0t = d.step(None, None, None, fv, stacked=st)
         out = d.tokens_to_frames(x0t).to(torch.float64).cpu().numpy()
         return out.reshape(comp.z_noise.shape)
 
@@ -149,12 +153,12 @@ class _DeviceRunner:
 _RUNNERS = weakref.WeakKeyDictionary()
 
 
-def device_runner(cfg, store, device="cuda"):
+def device_runner(cfg, store, device="cuda", comm=None):
     per = _RUNNERS.setdefault(store, {})
-    key = (cfg, str(device))
+    key = (cfg, str(device), id(comm))
     r = per.get(key)
     if r is None:
-        r = _DeviceRunner(cfg, store, device)
+        r = _DeviceRunner(cfg, store, device, comm)
         per[key] = r
     return r
 
@@ -162,18 +166,19 @@ def device_runner(cfg, store, device="cuda"):
 class Denoiser:
     """Stateless evaluator over a ParamStore (net.py:209-375), device-backed."""
 
-    def __init__(self, cfg: NetConfig, device="cuda"):
+    def __init__(self, cfg: NetConfig, device="cuda", comm=None):
         self.cfg = cfg
         self.device = device
+        self.comm = comm   # optional Ulysses communicator (every rank calls with the same inputs)
 
     def init_params(self, seed: int) -> ParamStore:
         return ParamStore.init(self.cfg, seed)
 
     def forward(self, params_store: ParamStore, comp: CompositeInput) -> np.ndarray:
-        return device_runner(self.cfg, params_store, self.device).forward_host(comp)
+        return device_runner(self.cfg, params_store, self.device, self.comm).forward_host(comp)
 
     def as_denoise_fn(self, params_store: ParamStore):
-        runner = device_runner(self.cfg, params_store, self.device)
+        runner = device_runner(self.cfg, params_store, self.device, self.comm)
 
         def fn(comp: CompositeInput) -> np.ndarray:
             return runner.forward_host(comp)

@@ -211,6 +211,13 @@ def patchify(motion, z, reference, Lm, Lc, D, H, W, ph, pw, out, stream=None):
     return out
 
 
+def patchify_stacked(stacked, ph, pw, out, stream=None):
+    """stacked f32 device [Lc][C][H][W] -> bf16 patch tokens (any composite)."""
+    Lc, Cc, H, W = stacked.shape
+    A.call("ftb_patchify_stacked", A.ptr(stacked), Lc, Cc, H, W, ph, pw, A.ptr(out), _ld(out), A.stream_ptr(stream))
+    return out
+
+
 def unpatch_ddim(x0_tok, Lm, Lc, D, H, W, ph, pw, z, x0_out, coeffs=None, stream=None):
     if coeffs is None:
         a_i = s_i = a_n = s_n = 0.0

@@ -197,10 +197,10 @@ class DeviceVAEDecoder:
         if self._geo == key:
             return
         self._geo = key
+        from .dist import slab_rows
         g, r = self.comm.world, self.comm.rank
-        if h < g:
-            raise ConfigError("latent height %d cannot be split over %d ranks" % (h, g))
-        sizes = [h // g + (1 if i < h % g else 0) for i in range(g)]
+        sizes = slab_rows(h, g)
+        self.sizes = sizes
         self.row0, self.rows = sum(sizes[:r]), sizes[r]
         geo = [dict(T=T, H=self.rows, W=w, C=0)]
         ups = 1
@@ -247,6 +247,14 @@ class DeviceVAEDecoder:
         npx = last["T"] * last["H"] * last["W"]
         self.out_rgb = torch.empty(npx * 3, dtype=torch.uint8, device=self.dev)
         self.out_f = torch.empty(npx * 32, dtype=f32, device=self.dev)
+        self.frames_full = None
+        if self.split:   # rank 0 receives every slab of the decoded frames (engine output)
+            sf = last["H"] // self.rows
+            full = (last["T"], h * sf, last["W"], 3 if self.rgb8 else 32)
+            dt = torch.uint8 if self.rgb8 else f32
+            self.px_sizes = [n * sf for n in sizes]
+            self.frames_full = (self.comm.sym("vae_frames", full, dt, self.dev) if getattr(self.comm, "peer", False)
+                                else torch.empty(full, dtype=dt, device=self.dev))
         for cw in self.W.values():
             cw.cache = None
             cw.hcache = None
@@ -342,10 +350,19 @@ class DeviceVAEDecoder:
             A.call(fn, A.ptr(x), npix, C, A.ptr(g), 1e-12, 1, A.ptr(y), A.stream_ptr(stream))
 
     # ------------------------------------------------------------ decode
-    def decode_device_tensor(self, z, stream=None):
+    def decode_device_tensor(self, z, stream=None, gather=False):
         """z: device f32 [T, z_dim, h, w] -> device output (uint8 [T*tf, H, W, 3] if
         rgb8 else f32 [T*tf, H, W, 32] with channels 0..2 valid). With a split
-        communicator the output is this rank's row slab [T*tf, H_local, W, .]."""
+        communicator the output is this rank's row slab [T*tf, H_local, W, .]; with
+        gather=True every slab is collected into rank 0's full frames (returned on rank 0,
+        None on the other ranks)."""
+        out = self._decode(z, stream)
+        if not (gather and self.split):
+            return out
+        self.comm.gather_rows("vae_frames", self.frames_full, out, self.px_sizes, stream)
+        return self.frames_full if self.comm.rank == 0 else None
+
+    def _decode(self, z, stream=None):
         if z.dim() != 4 or z.shape[1] != self.cfg.z_dim:
             raise ConfigError("VAE input must be [T, z_dim, h, w]")
         T, _, h, w = z.shape
@@ -453,9 +470,13 @@ class DeviceVAEDecoder:
         return buf
 
     def decode_device(self, z, stream):
-        """Codec interface of the streaming engine: device latents -> host frames."""
+        """Codec interface of the streaming engine: device latents -> host frames. A split
+        decoder gathers the slabs to rank 0, which returns the full frames; other ranks None."""
         with torch.cuda.stream(stream):
-            out = self.decode_device_tensor(z.reshape(z.shape[0], self.cfg.z_dim, *z.shape[-2:]), stream)
+            out = self.decode_device_tensor(z.reshape(z.shape[0], self.cfg.z_dim, *z.shape[-2:]), stream,
+                                            gather=True)
+            if out is None:
+                return None
             key = tuple(out.shape) + (out.dtype,)
             host = self._host.get(key)
             if host is None:
@@ -465,12 +486,16 @@ class DeviceVAEDecoder:
         stream.synchronize()
         return host.numpy().copy() if host.dtype == torch.uint8 else host.float().numpy()
 
-    def decode_device_async(self, z, stream, slot=0):
+    def decode_device_async(self, z, stream, slot=0, gather=False):
         """decode_device without the host wait: decode + D2H into pinned buffer `slot` are
         enqueued on `stream`; returns (pinned host tensor, event recorded after the copy).
-        Two slots let chunk c's frames land while chunk c+1 is being enqueued."""
+        Two slots let chunk c's frames land while chunk c+1 is being enqueued. gather=True:
+        split decoders collect the frames on rank 0 (other ranks get (None, None))."""
         with torch.cuda.stream(stream):
-            out = self.decode_device_tensor(z.reshape(z.shape[0], self.cfg.z_dim, *z.shape[-2:]), stream)
+            out = self.decode_device_tensor(z.reshape(z.shape[0], self.cfg.z_dim, *z.shape[-2:]), stream,
+                                            gather=gather)
+            if out is None:
+                return None, None
             key = tuple(out.shape) + (out.dtype, int(slot))
             host = self._host.get(key)
             if host is None:
