@@ -180,6 +180,13 @@ int ftb_copy_d2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, si
  * waits for all; traps after timeout_s seconds instead of hanging. */
 int ftb_peer_barrier(uint32_t* const* flags, uint32_t* epoch, int32_t rank, int32_t world, double timeout_s,
                      void* stream);
+/* Protocol self-test of ftb_peer_barrier with `world` concurrent ranks on one device (one
+ * co-resident block per rank, cooperative launch): `rounds` x (payload store, barrier, check
+ * every rank's payload, barrier). Caller-zeroed buffers: flags [world][world], epochs [world],
+ * data [rounds][world]; errors[0] += mismatches. Used by the tests (one GPU emulates the ranks
+ * without separate launches that wait on one another). */
+int ftb_peer_barrier_selftest(int32_t world, int32_t rounds, uint32_t* flags, uint32_t* epochs, uint32_t* data,
+                              uint32_t* errors, double timeout_s, void* stream);
 
 /* Folded cross-attention (wan mode; the cond K/V are fixed for a chunk).
  * Block-diagonal operands for folding the cross-attention projections on the tensor cores

@@ -57,6 +57,7 @@ _SIGS = {
     "ftb_ipc_import": ([C.c_char_p, C.POINTER(vp)], i32),
     "ftb_ipc_close": ([vp], i32),
     "ftb_peer_barrier": ([C.POINTER(vp), vp, i32, i32, C.c_double, vp], i32),
+    "ftb_peer_barrier_selftest": ([i32, i32, vp, vp, vp, vp, C.c_double, vp], i32),
     "ftb_copy_d2d": ([vp, vp, C.c_size_t, vp], i32),
     "ftb_copy_d2d_2d": ([vp, C.c_size_t, vp, C.c_size_t, C.c_size_t, C.c_size_t, vp], i32),
     "ftb_xattn_blockdiag": ([vp, i64, i32, i32, i32, i32, f32, vp, vp, i64, i32, vp], i32),

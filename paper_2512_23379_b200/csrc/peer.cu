@@ -77,24 +77,24 @@ struct BarrierParams {
   unsigned long long timeout_ns;
 };
 
-__global__ void peer_barrier_kernel(const BarrierParams p) {
-  __shared__ uint32_t e_sh;
-  // make every store this rank issued before the barrier (previous kernels on the
-  // stream, peer-mapped or local) visible system-wide before signalling
+// The barrier protocol, executed by one warp for rank `rank`: fence this rank's prior stores
+// system-wide, bump the local epoch, release-store it into every rank's flag word for this
+// rank, then acquire-spin until every rank's word for us reaches the epoch (trap on timeout).
+__device__ __forceinline__ void barrier_warp(uint32_t* const* flags, uint32_t* epoch, int rank, int world,
+                                             unsigned long long timeout_ns) {
   __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t e = *p.epoch + 1;
-    *p.epoch = e;
-    e_sh = e;
+  __syncwarp();
+  uint32_t e = 0;
+  if (threadIdx.x % 32 == 0) {
+    e = *epoch + 1;
+    *epoch = e;
   }
-  __syncthreads();
-  const uint32_t e = e_sh;
-  const int i = threadIdx.x;
-  if (i < p.world) {
-    uint32_t* dst = p.flags[i] + p.rank;
+  e = __shfl_sync(0xffffffffu, e, 0);
+  const int i = threadIdx.x % 32;
+  if (i < world) {
+    uint32_t* dst = flags[i] + rank;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst), "r"(e) : "memory");
-    const uint32_t* mine = p.flags[p.rank] + i;
+    const uint32_t* mine = flags[rank] + i;
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
@@ -103,14 +103,66 @@ __global__ void peer_barrier_kernel(const BarrierParams p) {
       if ((int)(v - e) >= 0) break;
       unsigned long long t1;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      if (t1 - t0 > p.timeout_ns) {
-        printf("ftb_peer_barrier: rank %d timed out waiting for rank %d (epoch %u, saw %u)\n", p.rank, i, e, v);
+      if (t1 - t0 > timeout_ns) {
+        printf("ftb_peer_barrier: rank %d timed out waiting for rank %d (epoch %u, saw %u)\n", rank, i, e, v);
         __trap();
       }
       __nanosleep(64);
     }
   }
-  __syncthreads();
+  __syncwarp();
+}
+
+__global__ void peer_barrier_kernel(const BarrierParams p) {
+  barrier_warp(p.flags, p.epoch, p.rank, p.world, p.timeout_ns);
+}
+
+// Self-test of the protocol with truly concurrent ranks on ONE device: block b plays rank b
+// (cooperative launch: all blocks co-resident, so the ranks' spins cannot starve one another).
+// Per round every rank writes a payload word, passes the barrier, and checks every rank's
+// payload of that round (it must be visible after the barrier); mismatches are counted.
+struct SelftestParams {
+  uint32_t* flags[FTB_MAX_PEERS];
+  uint32_t* epochs;   // [world]
+  uint32_t* data;     // [rounds][world]
+  uint32_t* errors;   // [1]
+  int world, rounds;
+  unsigned long long timeout_ns;
+};
+
+__global__ void peer_barrier_selftest_kernel(const SelftestParams p) {
+  const int rank = blockIdx.x;
+  for (int r = 0; r < p.rounds; ++r) {
+    if (threadIdx.x == 0) p.data[(size_t)r * p.world + rank] = (uint32_t)(r * 131 + rank * 7 + 1);
+    barrier_warp(p.flags, p.epochs + rank, rank, p.world, p.timeout_ns);
+    const int i = threadIdx.x;
+    if (i < p.world) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.data + (size_t)r * p.world + i) : "memory");
+      if (v != (uint32_t)(r * 131 + i * 7 + 1)) atomicAdd(p.errors, 1u);
+    }
+    // second barrier: nobody overwrites round r+1's slot reuse before all checked round r
+    barrier_warp(p.flags, p.epochs + rank, rank, p.world, p.timeout_ns);
+  }
+}
+
+extern "C" int ftb_peer_barrier_selftest(int32_t world, int32_t rounds, uint32_t* flags, uint32_t* epochs,
+                                         uint32_t* data, uint32_t* errors, double timeout_s, void* stream) {
+  if (world < 1 || world > FTB_MAX_PEERS || rounds < 1 || !flags || !epochs || !data || !errors)
+    return set_error(FTB_EINVAL, "peer_barrier_selftest: bad arguments");
+  SelftestParams p{};
+  for (int i = 0; i < world; ++i) p.flags[i] = flags + (size_t)i * world;
+  p.epochs = epochs;
+  p.data = data;
+  p.errors = errors;
+  p.world = world;
+  p.rounds = rounds;
+  p.timeout_ns = (unsigned long long)((timeout_s > 0 ? timeout_s : 10.0) * 1e9);
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)peer_barrier_selftest_kernel, dim3(world), dim3(32), args, 0,
+                                              reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return set_cuda_error(e, "peer_barrier_selftest launch");
+  return check_launch("peer_barrier_selftest_kernel");
 }
 
 extern "C" int ftb_peer_barrier(uint32_t* const* flags, uint32_t* epoch, int32_t rank, int32_t world,

@@ -16,9 +16,18 @@ Geometry is the reference's, bit-exact (streaming.py:246-306):
 Execution: three host threads as in the reference, but the denoise stage
 runs the whole 4-step ladder on a dedicated CUDA stream (device-resident
 weights, motion cache and sampler state) and hands the chunk's target latents
-to the decode stage through a CUDA event; the decode stage decodes on its own
+to the decode stage through a CUDA event without waiting for them (the host
+enqueues chunk n+1 while chunk n runs); the decode stage decodes on its own
 stream (orthogonal codec or the causal VAE), copies frames to pinned host
 memory and emits them, so decoding chunk n overlaps denoising chunk n+1.
+
+Multi-GPU (north star "8xB200"): with `comm` (dist.py) every rank
+runs the same session. Rank 0 owns the input: its ingest thread broadcasts
+each ready chunk (index, driving window) to the other ranks over a host
+channel, so every rank draws the same noise and keeps the same (replicated)
+sampler state; the DiT step runs Ulysses sequence parallel over the ranks; a
+spatially split VAE (built on `comm.channel("vae")`) decodes one row slab per
+rank and gathers the frames into rank 0, which alone emits them.
 """
 
 import collections
@@ -33,7 +42,8 @@ import numpy as np
 import torch
 
 from .config import PACING_MODES, SamplerPlan, StreamConfig  # noqa: F401
-from .errors import ConfigError
+from . import ops
+from .errors import ConfigError, NumericError
 from .net import device_runner
 from .seeding import chunk_noise
 
@@ -88,6 +98,11 @@ class DeviceStreamer:
         self.x0_static = torch.empty((nt,) + self.fshape, dtype=torch.float32, device=self.dev)
         self.slots = [torch.empty((nt,) + self.fshape, dtype=torch.float32, device=self.dev) for _ in range(4)]
         self.slot = 0
+        # per-chunk non-finite count of the target latents (device, inside the captured chunk)
+        # and one pinned host copy per output slot, read by whoever waits for that chunk
+        self.nonfinite = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.nonfinite_host = [torch.zeros(1, dtype=torch.int32).pin_memory() for _ in range(4)]
+        self.last_slot = 0
         self._k = 0
         self._h2d_ev = [None, None]
         self.use_graph = use_graph and (self.d.comm.world == 1 or getattr(self.d.comm, "capturable", False))
@@ -107,6 +122,7 @@ class DeviceStreamer:
         nt, lm = cfg.stride, cfg.motion_len
         self.d.upload_cond()
         self.d.sample(self.motion, self.ref, self.z, cfg.sampler, self.x0_static)
+        ops.count_nonfinite(self.x0_static, self.nonfinite, stream=self.d.stream)
         if lm:
             if lm <= nt:
                 self.motion.copy_(self.x0_static[nt - lm:])
@@ -175,19 +191,36 @@ class DeviceStreamer:
             if self.use_graph and self._eager_runs == 1:
                 self._capture()
         x0 = self.slots[self.slot]
+        self.nonfinite_host[self.slot].copy_(self.nonfinite, non_blocking=True)
+        self.last_slot = self.slot
         self.slot = (self.slot + 1) % len(self.slots)
         x0.copy_(self.x0_static)
         return x0
+
+    def check_finite(self, c, slot):
+        """NumericError (reference errors.py:17-18) when chunk c's target latents held a NaN/Inf.
+        Call after the chunk's work is known complete (the caller has synchronised with it)."""
+        n = int(self.nonfinite_host[slot].item())
+        if n:
+            raise NumericError("chunk %d: %d non-finite target latents" % (c, n))
 
 
 class StreamSession:
     """One live stream; command it from a single controller thread."""
 
     def __init__(self, store, net_cfg, codec, reference_frame, cfg: StreamConfig, *, device="cuda",
-                 reference_latent=None, latent_hw=(1, 1)):
+                 reference_latent=None, latent_hw=(1, 1), comm=None):
         self.cfg = cfg
         self.codec = codec
-        runner = device_runner(net_cfg, store, device)
+        self._rank = comm.rank if comm is not None else 0
+        self._world = comm.world if comm is not None else 1
+        ccomm = getattr(codec, "comm", None)
+        if ccomm is not None and ccomm.world not in (1, self._world):
+            raise ConfigError("the decoder's communicator spans %d ranks, the session %d" % (ccomm.world,
+                                                                                          self._world))
+        # rank 0 broadcasts every ready chunk's window to the followers (collective: created here)
+        self._host = comm.host_channel("ingest") if self._world > 1 else None
+        runner = device_runner(net_cfg, store, device, comm)
         if reference_latent is None:
             reference_frame = np.asarray(reference_frame, dtype=np.float64)
             if net_cfg.mode == "ftlk" and reference_frame.shape != (net_cfg.latent_dim,):
@@ -219,7 +252,8 @@ class StreamSession:
         self._denoise_stream = torch.cuda.Stream(device=runner.device)
         self._decode_stream = torch.cuda.Stream(device=runner.device)
         self._workers = [
-            threading.Thread(target=self._ingest_loop, daemon=True, name="ftb-ingest"),
+            threading.Thread(target=self._ingest_loop if self._rank == 0 else self._follow_loop, daemon=True,
+                             name="ftb-ingest"),
             threading.Thread(target=self._denoise_loop, daemon=True, name="ftb-denoise"),
             threading.Thread(target=self._decode_loop, daemon=True, name="ftb-decode"),
         ]
@@ -228,6 +262,9 @@ class StreamSession:
 
     # ---------------------------------------------------------------- controller API
     def push_signal(self, samples) -> int:
+        if self._rank != 0:
+            raise ConfigError("rank %d follows rank 0's chunk schedule: push the driving signal on rank 0"
+                              % self._rank)
         if self._closed.is_set():
             raise ConfigError("session is closed")
         self._raise_pending_error()
@@ -320,11 +357,36 @@ class StreamSession:
                     keep_from = (c + 1) * cfg.stride - cfg.motion_len
                     self._pending = {j: v for j, v in self._pending.items() if j >= keep_from}
                     self._next_window += 1
+                    if self._host is not None:
+                        self._host.host_broadcast((c, window))     # followers run the same chunk
                     noise = chunk_noise(cfg.seed, c, (cfg.stride,) + self._reference.shape)
                     signal_ms += (time.perf_counter() - t1) * 1000.0
                     t_origin = time.perf_counter() - signal_ms / 1000.0
                     self._to_denoise.put((c, window, noise, signal_ms, t_origin))
                     signal_ms = 0.0
+        except Exception as exc:  # noqa: BLE001
+            self._fail(exc)
+        finally:
+            if self._host is not None:
+                try:
+                    self._host.host_broadcast(None)                # end of stream for the followers
+                except Exception as exc:  # noqa: BLE001
+                    self._fail(exc)
+            self._to_denoise.put(None)
+
+    def _follow_loop(self):
+        """Ranks > 0: the chunk schedule comes from rank 0 (same windows, same noise draw)."""
+        cfg = self.cfg
+        try:
+            while True:
+                item = self._host.host_broadcast(None)
+                if item is None:
+                    break
+                t0 = time.perf_counter()
+                c, window = item
+                self._next_window = c + 1
+                noise = chunk_noise(cfg.seed, c, (cfg.stride,) + self._reference.shape)
+                self._to_denoise.put((c, window, noise, (time.perf_counter() - t0) * 1000.0, t0))
         except Exception as exc:  # noqa: BLE001
             self._fail(exc)
         finally:
@@ -339,13 +401,15 @@ class StreamSession:
                     if item is None:
                         break
                     c, window, noise, signal_ms, t_ready = item
-                    t0 = time.perf_counter()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(self._denoise_stream)
                     x0 = self._ds.denoise_chunk(c, window, noise)
-                    ev = torch.cuda.Event()
+                    slot = self._ds.last_slot
+                    ev = torch.cuda.Event(enable_timing=True)
                     ev.record(self._denoise_stream)
-                    ev.synchronize()
-                    denoise_ms = (time.perf_counter() - t0) * 1000.0
-                    self._to_decode.put((c, x0, ev, signal_ms, denoise_ms, 0.0, t_ready))
+                    # no host wait: the decode stage waits on `ev`, this thread enqueues chunk c+1
+                    # (the 4-slot x0 ring and the 2-deep decode queue keep chunk c's slot alive)
+                    self._to_decode.put((c, x0, (e0, ev, slot), signal_ms, 0.0, t_ready))
         except Exception as exc:  # noqa: BLE001
             self._fail(exc)
         finally:
@@ -361,7 +425,7 @@ class StreamSession:
                     item = self._to_decode.get()
                     if item is None:
                         break
-                    c, x0, ev, signal_ms, denoise_ms, motion_ms, t_ready = item
+                    c, x0, (e0, ev, slot), signal_ms, motion_ms, t_ready = item
                     if cfg.pacing == "realtime":
                         now = time.perf_counter()
                         if next_due is None:
@@ -369,12 +433,20 @@ class StreamSession:
                         if next_due > now:
                             time.sleep(next_due - now)
                         next_due += chunk_period
-                    t0 = time.perf_counter()
                     self._decode_stream.wait_event(ev)
-                    frames = self.codec.decode_device(x0, self._decode_stream)
-                    decode_ms = (time.perf_counter() - t0) * 1000.0
-                    fpc = len(frames)
-                    emitted = [EmittedFrame(c * fpc + j, c, frames[j]) for j in range(fpc)]
+                    d0 = torch.cuda.Event(enable_timing=True)
+                    d0.record(self._decode_stream)
+                    frames = self.codec.decode_device(x0, self._decode_stream)   # waits for the frames
+                    d1 = torch.cuda.Event(enable_timing=True)
+                    d1.record(self._decode_stream)
+                    d1.synchronize()
+                    self._ds.check_finite(c, slot)
+                    denoise_ms = e0.elapsed_time(ev)
+                    decode_ms = d0.elapsed_time(d1)
+                    if self._rank != 0:
+                        frames = None      # rank 0 emits (a split decoder gathered the frames there)
+                    fpc = self.frames_per_chunk if frames is None else len(frames)
+                    emitted = [] if frames is None else [EmittedFrame(c * fpc + j, c, frames[j]) for j in range(fpc)]
                     t_emit = time.perf_counter()
                     total_ms = (t_emit - t_ready) * 1000.0
                     misc_ms = max(0.0, total_ms - signal_ms - denoise_ms - decode_ms - motion_ms)
@@ -385,8 +457,8 @@ class StreamSession:
                             self._cycle_ring[self._cycle_count % _RECENT] = (t_emit - self._last_emit_t) * 1000.0
                             self._cycle_count += 1
                         self._last_emit_t = t_emit
-                        self._frames_emitted += fpc
-                        self._chunks_emitted += 1
+                        self._frames_emitted += len(emitted)
+                        self._chunks_emitted += 1 if emitted else 0
                         self._last_generate_ms = denoise_ms + decode_ms
                         self._last_cycle = {"signal_ms": signal_ms, "denoise_ms": denoise_ms,
                                             "decode_ms": decode_ms, "motion_encode_ms": motion_ms,
@@ -403,13 +475,15 @@ def start_stream(store, net_cfg, codec, reference_frame, cfg: StreamConfig, **kw
 
 
 def generate(store, net_cfg, codec, reference_latent, signal, n_frames, *, cfg: StreamConfig = None,
-             device="cuda", latent_hw=(1, 1), decode=True, motion_override=None):
+             device="cuda", latent_hw=(1, 1), decode=True, motion_override=None, comm=None):
     """Synchronous chunked generation with the engine's exact geometry (the
     reference's `rollout_stream`, metrics.py:128-149). Returns
     (targets (n_frames_latent, ...), motions per chunk, decoded frames or None).
-    `motion_override[c]` teacher-forces chunk c's motion rows (parity tests)."""
+    `motion_override[c]` teacher-forces chunk c's motion rows (parity tests).
+    With `comm` every rank calls it with the same arguments (Ulysses DiT, replicated
+    sampler state); a split decoder returns the frames on rank 0 only."""
     cfg = cfg or StreamConfig()
-    runner = device_runner(net_cfg, store, device)
+    runner = device_runner(net_cfg, store, device, comm)
     ds = DeviceStreamer(runner, cfg, codec, reference_latent, latent_hw)
     stride = cfg.stride
     n_chunks = int(np.ceil(n_frames / stride))
@@ -426,8 +500,11 @@ def generate(store, net_cfg, codec, reference_latent, signal, n_frames, *, cfg: 
                        if cfg.motion_len else np.zeros((0,) + ds.ref_host.shape))
         x0 = ds.denoise_chunk(c, window)
         outs.append(x0.double().cpu().numpy().reshape((stride,) + ds.ref_host.shape))
+        ds.check_finite(c, ds.last_slot)
         if decode and codec is not None:
-            frames.append(codec.decode_device(x0, torch.cuda.current_stream()))
+            fr = codec.decode_device(x0, torch.cuda.current_stream())
+            if fr is not None:
+                frames.append(fr)
     targets = np.concatenate(outs, axis=0)[:n_frames]
     fr = np.concatenate(frames, axis=0) if frames else None
     return targets, motions, fr

@@ -105,3 +105,65 @@ def test_gloo_halo_exchange_world3():
     for p in ps:
         p.join(timeout=60)
     assert all(r[1] == "ok" for r in res), res
+
+
+def _engine_io_worker(rank, world, port, q):
+    """Host plumbing of the multi-rank engine: the ingest channel's chunk broadcast (rank 0 ->
+    followers, end-of-stream sentinel), a decode channel independent of the DiT group, and the
+    frame gather of row slabs into rank 0 (uneven slabs)."""
+    import torch.distributed as dist
+
+    from paper_2512_23379_b200.dist import TorchComm, slab_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        host = comm.host_channel("ingest")
+        vae = comm.channel("vae")
+        assert (host.world, host.rank, vae.world, vae.rank) == (world, rank, world, rank)
+        windows = [np.full((3, 2), 0.5 * c) for c in range(4)]
+        seen = []
+        for c in range(5):
+            item = host.host_broadcast((c, windows[c]) if c < 4 else None) if rank == 0 else host.host_broadcast(None)
+            if item is None:
+                break
+            seen.append(item)
+        assert [c for c, _ in seen] == [0, 1, 2, 3]
+        assert all(np.array_equal(w, windows[c]) for c, w in seen)
+        sizes = slab_rows(7, world)
+        r0 = sum(sizes[:rank])
+        slab = torch.arange(r0, r0 + sizes[rank], dtype=torch.float32).view(1, -1, 1, 1).expand(2, -1, 3, 2).clone()
+        full = torch.full((2, 7, 3, 2), -1.0)
+        vae.gather_rows("frames", full, slab, sizes)
+        if rank == 0:
+            want = torch.arange(7, dtype=torch.float32).view(1, 7, 1, 1).expand(2, 7, 3, 2)
+            assert torch.equal(full, want)
+        q.put((rank, "ok", 0))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_engine_host_plumbing(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30100 + world * 50 + os.getpid() % 40
+    ps = [ctx.Process(target=_engine_io_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res
+
+
+def test_slab_rows_partition():
+    from paper_2512_23379_b200.dist import slab_rows
+    assert slab_rows(52, 8) == [7, 7, 7, 7, 6, 6, 6, 6]
+    assert slab_rows(90, 8) == [12, 12, 11, 11, 11, 11, 11, 11]
+    assert sum(slab_rows(9, 8)) == 9
+    with pytest.raises(Exception):
+        slab_rows(5, 8)

@@ -184,3 +184,24 @@ def test_split_vae_matches_unsplit(cuda, world, transport):
         full = np.concatenate([sl for _, sl in slabs], axis=1)[..., :3]
         assert full.shape == want[i][..., :3].shape
         assert rel(full, want[i][..., :3]) < 2e-3, i
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_barrier_protocol_concurrent_ranks(cuda, world):
+    """The device barrier's protocol (release-store of the epoch into every rank's flag word,
+    acquire-spin on its own) with `world` truly concurrent ranks: one co-resident block per rank
+    in a cooperative launch (never separate launches that wait on one another on one GPU).
+    Every round's payload of every rank is visible after the barrier; the epochs advance once
+    per barrier."""
+    from paper_2512_23379_b200 import _capi as A
+    rounds = 2000
+    flags = torch.zeros(world * world, dtype=torch.int32, device=cuda)
+    epochs = torch.zeros(world, dtype=torch.int32, device=cuda)
+    data = torch.zeros(rounds * world, dtype=torch.int32, device=cuda)
+    errors = torch.zeros(1, dtype=torch.int32, device=cuda)
+    A.call("ftb_peer_barrier_selftest", world, rounds, A.ptr(flags), A.ptr(epochs), A.ptr(data), A.ptr(errors),
+           10.0, A.stream_ptr())
+    torch.cuda.synchronize()
+    assert int(errors.item()) == 0
+    assert torch.all(epochs == 2 * rounds)
+    assert torch.all(flags == 2 * rounds)

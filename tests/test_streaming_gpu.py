@@ -179,3 +179,24 @@ def test_wan_stream_with_vae_decoder(cuda):
     VPb = {k: (torch.as_tensor(v).to(torch.bfloat16).double().numpy() if k.endswith(".w") else v) for k, v in VP.items()}
     want = VO.VAEOracle(VPb, **vcfg).decode(tg[:4])
     assert rel(frf[..., :3], want) < BUDGET
+
+
+def test_nonfinite_chunk_raises_numeric_error(golden, cuda, setup):
+    """A NaN on the numeric path surfaces as the reference's NumericError (errors.py:17-18),
+    from generate() and from the live session (device count inside the captured chunk)."""
+    from paper_2512_23379_b200.config import StreamConfig
+    from paper_2512_23379_b200.errors import NumericError
+    from paper_2512_23379_b200.streaming import generate, start_stream
+    cfg, store, codec = setup
+    bad = store.clone()
+    bad.params["out.b"][3] = np.nan
+    with pytest.raises(NumericError):
+        generate(bad, cfg, codec, golden["r_reference_latent"], golden["r_signal"], 14,
+                 cfg=StreamConfig(seed=int(golden["r_seed"])))
+    sess = start_stream(bad, cfg, codec, golden["r_reference_frame"], StreamConfig(seed=int(golden["r_seed"])))
+    sess.push_signal((i, golden["r_signal"][i]) for i in range(14))
+    with pytest.raises(NumericError):
+        deadline = time.time() + 60
+        while time.time() < deadline:
+            sess.next_frames(wait=True, timeout=0.2)
+    sess.close()
