@@ -160,3 +160,25 @@ def test_wan_folded_cross_attention_matches_projections(cuda):
     ref = WO.denoise(store.bf16_rounded().params, ocfg, x["motion"], x["z"], x["ref"], x["audio"],
                      np.where(np.arange(Lc) < Lm, 0.0, 0.75))
     assert rel(outs[0], ref) < BUDGET
+
+
+def test_forward_accepts_any_composite(cuda):
+    """Denoiser.forward takes any CompositeInput, like the reference's (net.py:223-238): a
+    mask / conditioning layout other than composite_from_state's is patchified as given."""
+    from paper_2512_23379_b200.diffusion import composite_from_state
+    from paper_2512_23379_b200.net import Denoiser
+    cfg, store = _store("default")
+    r = np.random.default_rng(4)
+    comp = composite_from_state(r.standard_normal((2, 8)), r.standard_normal((7, 8)), r.standard_normal(8),
+                                r.uniform(-1, 1, 9), 0.5)
+    comp.z_mask[1] = 1.0                       # a second "given" frame
+    comp.z_cond[3] = r.standard_normal(8)      # conditioning on another row
+    out = Denoiser(cfg).forward(store, comp)
+    P = store.bf16_rounded().params
+    ref = FO.denoise(P, dict(model_dim=cfg.model_dim, layers=cfg.layers, heads=cfg.heads),
+                     {"stacked": comp.stacked(), "frame_t": comp.frame_t, "signal": comp.signal,
+                      "reference": comp.reference, "motion_len": comp.motion_len})
+    assert rel(out, ref) < 5e-3
+    canon = Denoiser(cfg).forward(store, composite_from_state(comp.z_noise[:2], comp.z_noise[2:], comp.reference,
+                                                              comp.signal, 0.5))
+    assert rel(out, canon) > 1e-3               # the extra mask / cond rows were really used
