@@ -101,6 +101,15 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except Exception:  # noqa: BLE001
             self.proc.kill()
+        note = None
+        if not self.lines:   # timed region shorter than the sampling period (tiny model): one
+            try:             # sample right after it, while the clocks are still at the load state
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                self.lines = [ln.strip() for ln in out.stdout.splitlines() if ln.strip()]
+                note = "timed region shorter than the 200 ms sampling period: one sample right after it"
+            except Exception:  # noqa: BLE001
+                pass
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -115,8 +124,11 @@ class ClockSampler:
             for nm, v in zip(names, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        res = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if note:
+            res["note"] = note
+        return res
 
 
 REF_KERNELS = ("dense_forward", "dense_backward", "gelu_forward", "gelu_backward", "layernorm_forward",

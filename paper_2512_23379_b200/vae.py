@@ -357,6 +357,7 @@ class DeviceVAEDecoder:
         gather=True every slab is collected into rank 0's full frames (returned on rank 0,
         None on the other ranks)."""
         out = self._decode(z, stream)
+        self.last_slab = out
         if not (gather and self.split):
             return out
         self.comm.gather_rows("vae_frames", self.frames_full, out, self.px_sizes, stream)

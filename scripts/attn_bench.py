@@ -48,13 +48,27 @@ def main():
             t = timeit(lambda: ops.attention(q, kv[:, :5120], kv[:, 5120:], o, 40, 128, L, 37, 0.088, impl=impl))
             print("cross14b impl=%d %.1f us  %.0f GB/s (Q read + O write)" % (impl, t * 1e3, 2 * q.numel() * 2 / t / 1e6),
                   flush=True)
-    for (H, hd, tag) in [(40, 128, "attn14b"), (12, 128, "attn1.3b")]:
+    import statistics
+    for (H, hd, tag) in [(40, 128, "attn14b"), (12, 128, "attn1.3b"), (5, 128, "attn14b_g8")]:
         q, k, v = (torch.randn(L, H * hd, device=dev).to(torch.bfloat16) for _ in range(3))
         o = torch.empty_like(q)
+        ws = ops.attention_workspace(L, L, H, hd, dev)
         fl = 4.0 * L * L * H * hd
-        for impl in [i for i in impls if i != 3]:
-            t = timeit(lambda: ops.attention(q, k, v, o, H, hd, L, L, 1 / math.sqrt(hd), impl=impl))
-            print("%s impl=%d %.3f ms %.0f TFLOP/s" % (tag, impl, t, fl / t / 1e9), flush=True)
+        qs, ks, vs = (x.view(1, L, H, hd).transpose(1, 2) for x in (q, k, v))
+        runs = {}
+        for _ in range(5):   # interleaved: same clocks / power state for every variant
+            for impl in [i for i in impls if i != 3]:
+                for w_, wn in ((None, ""), (ws, "+split")):
+                    if w_ is None and ws is not None and impl == 0 and len(impls) > 1:
+                        continue
+                    t = timeit(lambda: ops.attention(q, k, v, o, H, hd, L, L, 1 / math.sqrt(hd), impl=impl,
+                                                     workspace=w_))
+                    runs.setdefault("impl=%d%s" % (impl, wn), []).append(t)
+            t = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qs, ks, vs))
+            runs.setdefault("torch_sdpa", []).append(t)
+        for name, ts in runs.items():
+            t = statistics.median(ts)
+            print("%s %-16s %.3f ms %.0f TFLOP/s" % (tag, name, t, fl / t / 1e9), flush=True)
 
 
 if __name__ == "__main__":

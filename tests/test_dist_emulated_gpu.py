@@ -168,8 +168,11 @@ def test_split_vae_matches_unsplit(cuda, world, transport):
             for i, z in enumerate(zs):
                 with torch.cuda.stream(s):
                     zd = torch.as_tensor(z, dtype=torch.float32, device=cuda)
-                out = dec.decode_device(zd, s)
-                got[i][rk] = (dec.row0, out)
+                    full = dec.decode_device_tensor(zd, s, gather=True)  # frames gathered into rank 0
+                    full = None if full is None else full.clone()
+                    slab = dec.last_slab.clone()                         # this rank's row slab
+                s.synchronize()
+                got[i][rk] = (dec.row0, slab.cpu().numpy(), None if full is None else full.cpu().numpy())
         except Exception as e:  # noqa: BLE001
             errs.append(e)
             raise
@@ -181,9 +184,11 @@ def test_split_vae_matches_unsplit(cuda, world, transport):
     assert not errs, errs
     for i in range(2):
         slabs = sorted(got[i], key=lambda x: x[0])
-        full = np.concatenate([sl for _, sl in slabs], axis=1)[..., :3]
-        assert full.shape == want[i][..., :3].shape
-        assert rel(full, want[i][..., :3]) < 2e-3, i
+        cat = np.concatenate([sl for _, sl, _ in slabs], axis=1)
+        assert cat[..., :3].shape == want[i][..., :3].shape
+        assert rel(cat[..., :3], want[i][..., :3]) < 2e-3, i
+        gathered = [fg for _, _, fg in got[i] if fg is not None]
+        assert len(gathered) == 1 and np.array_equal(gathered[0], cat)   # rank 0 alone gets all slabs
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
