@@ -91,13 +91,8 @@ struct Fmha2Cfg {
 // its first 64 columns; O_t fp32 at [256 + 128t, 256 + 128t + HD).
 // The softmax hands P over in two 64-key halves so PV of the first half overlaps the
 // exponentials of the second (shortens the S -> softmax -> PV -> S chain).
-// SW = softmax warps per tile. SW = 4: one thread per row (tcgen05.ld 32x32b, 128 keys per
-// thread per block). SW = 8: two warps per TMEM lane quadrant, each owning 16 rows through
-// tcgen05.ld 16x256b, so four threads share a row (32 keys each per block) and the row max /
-// sum reduce with two shuffles: half the exponentials per thread, so a tile's S -> softmax -> PV
-// chain fits under the other tile's PV + S on the tensor core.
-template <int HD, int SW>
-__global__ void __launch_bounds__(128 + 64 * SW, 1)
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
     fmha2_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
   using C = Fmha2Cfg<HD>;
@@ -136,8 +131,8 @@ __global__ void __launch_bounds__(128 + 64 * SW, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], SW);
-      mbar_init(&p_lo[t], SW);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&p_lo[t], 4);
       mbar_init(&o_done[t], 1);
     }
     fence_barrier_init();
@@ -150,10 +145,7 @@ __global__ void __launch_bounds__(128 + 64 * SW, 1)
   // Register budget: the producer / MMA warpgroup gives registers to the two softmax
   // warpgroups (128*96 + 256*200 <= 384*168: inc blocks until the pool has them), which keeps a whole 128-column S row resident.
   if (warp < 4) {
-    if constexpr (SW == 4)
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
-    else
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
   if (warp == 0) {
     if (lane == 0) {
       const int col0 = head * HD;
@@ -229,187 +221,6 @@ __global__ void __launch_bounds__(128 + 64 * SW, 1)
       }
     }
   }
-  } else if constexpr (SW == 8) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n" ::: "memory");
-    const int sw = warp - 4;                      // 0..15
-    const int t = sw >> 3;                        // tile of this warp
-    const int lane_base = (warp & 3) * 32 + ((sw >> 2) & 1) * 16;   // quadrant (warp % 4) + half
-    const int q = lane & 3;                       // column pair 2q, 2q+1 of every 8-column group
-    const int rA = lane_base + (lane >> 2), rB = rA + 8;            // the thread's two rows
-    const uint32_t lane_off = (uint32_t)lane_base << 16;
-    const uint32_t tS = tmem + lane_off + t * 128;
-    const uint32_t tO = tmem + lane_off + 256 + t * 128;
-    float m_ref[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      uint32_t sr[64];   // rep i: [row A col 8i+2q, 8i+2q+1, row B col 8i+2q, 8i+2q+1]
-      tmem_ld_16x256b_x16(tS, sr);
-      tmem_ld_wait();
-      const int valid = p.Lk - (j0 + j) * 128;   // global key block
-      if (valid < 128) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int c = 8 * i + 2 * q;
-          if (c >= valid) sr[4 * i] = sr[4 * i + 2] = __float_as_uint(-INFINITY);
-          if (c + 1 >= valid) sr[4 * i + 1] = sr[4 * i + 3] = __float_as_uint(-INFINITY);
-        }
-      }
-      float mx[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        float c4[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          c4[u] = fmaxf(__uint_as_float(sr[4 * u + 2 * r]), __uint_as_float(sr[4 * u + 2 * r + 1]));
-#pragma unroll
-        for (int i = 4; i < 16; i += 4)   // 4 independent FMNMX3 chains
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            c4[u] = fmax3(c4[u], __uint_as_float(sr[4 * (i + u) + 2 * r]), __uint_as_float(sr[4 * (i + u) + 2 * r + 1]));
-        mx[r] = fmaxf(fmaxf(c4[0], c4[1]), fmaxf(c4[2], c4[3]));
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-        mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2)) * p.scale_log2;
-      }
-      float m_use[2];
-      bool resc[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        m_use[r] = m_ref[r];
-        resc[r] = false;
-        if (j == 0) {
-          m_use[r] = mx[r];
-        } else if (mx[r] > m_ref[r] + 8.f) {
-          m_use[r] = mx[r];
-          resc[r] = true;
-        }
-      }
-      const float2 nmA = make_float2(-m_use[0], -m_use[0]), nmB = make_float2(-m_use[1], -m_use[1]);
-      float2 rsA = make_float2(0.f, 0.f), rsB = make_float2(0.f, 0.f);
-      // P for reps [i0, i0+8) (64 keys) -> pr in the 16x128b store layout (reg 2i: row A, 2i+1: row B)
-      auto exp_half = [&](int i0, uint32_t (&pr)[16]) {
-#pragma unroll
-        for (int ii = 0; ii < 8; ++ii) {
-          const int i = i0 + ii;
-          float2 xa = ffma2(make_float2(__uint_as_float(sr[4 * i]), __uint_as_float(sr[4 * i + 1])), sc2, nmA);
-          float2 xb = ffma2(make_float2(__uint_as_float(sr[4 * i + 2]), __uint_as_float(sr[4 * i + 3])), sc2, nmB);
-          float2 ea, eb;
-          if ((ii & 3) == 3) {   // one rep in four on the FMA pipe (offloads MUFU)
-            xa.x = fmaxf(xa.x, -126.f);
-            xa.y = fmaxf(xa.y, -126.f);
-            xb.x = fmaxf(xb.x, -126.f);
-            xb.y = fmaxf(xb.y, -126.f);
-            ea = ex2_poly2(xa);
-            eb = ex2_poly2(xb);
-          } else {
-            ea = make_float2(ex2(xa.x), ex2(xa.y));
-            eb = make_float2(ex2(xb.x), ex2(xb.y));
-          }
-          rsA = fadd2(rsA, ea);
-          rsB = fadd2(rsB, eb);
-          pr[2 * ii] = pack_bf16(ea.x, ea.y);
-          pr[2 * ii + 1] = pack_bf16(eb.x, eb.y);
-        }
-      };
-      {
-        uint32_t pr[16];
-        exp_half(0, pr);
-        // PV_t(j-1) is complete here (the MMA warp committed s_full_t(j) after issuing it), so O
-        // is stable and the P region free: rescale O rows whose reference max moved
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, resc[0] || resc[1])) {
-          const float fA = resc[0] ? ex2(m_ref[0] - m_use[0]) : 1.f;
-          const float fB = resc[1] ? ex2(m_ref[1] - m_use[1]) : 1.f;
-          l[0] *= fA;
-          l[1] *= fB;
-#pragma unroll 1
-          for (int c0 = 0; c0 < HD; c0 += 32) {
-            uint32_t o[16];
-            tmem_ld_16x256b_x4(tO + c0, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              o[4 * i] = __float_as_uint(__uint_as_float(o[4 * i]) * fA);
-              o[4 * i + 1] = __float_as_uint(__uint_as_float(o[4 * i + 1]) * fA);
-              o[4 * i + 2] = __float_as_uint(__uint_as_float(o[4 * i + 2]) * fB);
-              o[4 * i + 3] = __float_as_uint(__uint_as_float(o[4 * i + 3]) * fB);
-            }
-            tmem_st_16x256b_x4(tO + c0, o);
-          }
-        }
-        tmem_st_16x128b_x8(tS + 0, pr);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_lo[t]);
-      }
-      {
-        uint32_t pr[16];
-        exp_half(8, pr);
-        tmem_st_16x128b_x8(tS + 32, pr);
-        tmem_st_wait();
-      }
-      l[0] += rsA.x + rsA.y;
-      l[1] += rsB.x + rsB.y;
-      m_ref[0] = m_use[0];
-      m_ref[1] = m_use[1];
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-    }
-    mbar_wait(&o_done[t], (n_kv - 1) & 1);
-    tc_fence_after();
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {   // full row sums over the four threads of the row
-      l[r] += __shfl_xor_sync(0xffffffffu, l[r], 1);
-      l[r] += __shfl_xor_sync(0xffffffffu, l[r], 2);
-    }
-    const int growA = qblk * 256 + t * 128 + rA, growB = growA + 8;
-    if (p.ws && (int)blockIdx.x >= p.split_first) {  // half of the keys: unnormalised O, (m_ref, l) for the combine
-      float* ws = p.ws + (size_t)(blockIdx.x - p.split_first) * (256 * HD + 512);
-      float* wA = ws + (size_t)(t * 128 + rA) * HD;
-      float* wB = ws + (size_t)(t * 128 + rB) * HD;
-#pragma unroll 1
-      for (int c0 = 0; c0 < HD; c0 += 32) {
-        uint32_t o[16];
-        tmem_ld_16x256b_x4(tO + c0, o);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int col = c0 + 8 * i + 2 * q;
-          *reinterpret_cast<float2*>(wA + col) = make_float2(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]));
-          *reinterpret_cast<float2*>(wB + col) = make_float2(__uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
-        }
-      }
-      if (q == 0) {
-        reinterpret_cast<float2*>(ws + 256 * HD)[t * 128 + rA] = make_float2(m_ref[0], l[0]);
-        reinterpret_cast<float2*>(ws + 256 * HD)[t * 128 + rB] = make_float2(m_ref[1], l[1]);
-      }
-    } else {
-      const float invA = 1.f / l[0], invB = 1.f / l[1];
-      __nv_bfloat16* oA = growA < p.Lq ? attn_out_row(p, growA) + head * HD : nullptr;
-      __nv_bfloat16* oB = growB < p.Lq ? attn_out_row(p, growB) + head * HD : nullptr;
-#pragma unroll 1
-      for (int c0 = 0; c0 < HD; c0 += 32) {
-        uint32_t o[16];
-        tmem_ld_16x256b_x4(tO + c0, o);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int col = c0 + 8 * i + 2 * q;
-          if (oA)
-            *reinterpret_cast<uint32_t*>(oA + col) =
-                pack_bf16(__uint_as_float(o[4 * i]) * invA, __uint_as_float(o[4 * i + 1]) * invA);
-          if (oB)
-            *reinterpret_cast<uint32_t*>(oB + col) =
-                pack_bf16(__uint_as_float(o[4 * i + 2]) * invB, __uint_as_float(o[4 * i + 3]) * invB);
-        }
-      }
-    }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;\n" ::: "memory");
     const int t = (warp - 4) >> 2;  // tile handled by this warpgroup
@@ -998,13 +809,13 @@ static int fmha2_split_items(int Lq, int Lk, int heads) {
 
 static size_t fmha2_ws_bytes(int R, int hd) { return (size_t)2 * R * (256 * hd + 512) * sizeof(float); }
 
-template <int HD, int SW>
+template <int HD>
 static int launch_fmha2(const AttnParams& p_in, cudaStream_t s, float* ws, size_t ws_bytes) {
   AttnParams p = p_in;
   using C = Fmha2Cfg<HD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fmha2_tc_kernel<HD, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(fmha2_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "fmha2 smem attribute");
     configured = true;
   }
@@ -1031,7 +842,7 @@ static int launch_fmha2(const AttnParams& p_in, cudaStream_t s, float* ws, size_
     p.split_first = items - R;
   }
   const int grid = p.ws ? items + R : items;
-  fmha2_tc_kernel<HD, SW><<<grid, 128 + 64 * SW, C::SMEM, s>>>(tq, tk, tv, p);
+  fmha2_tc_kernel<HD><<<grid, 384, C::SMEM, s>>>(tq, tk, tv, p);
   rc = check_launch("fmha2_tc_kernel");
   if (rc || !p.ws) return rc;
   fmha2_combine_kernel<HD><<<R, 256, 0, s>>>(p);
@@ -1060,18 +871,13 @@ static int attention_run(int32_t impl, AttnParams& p, float* ws, size_t ws_bytes
     if (head_dim == 64) return launch_xattn<64>(p, s);
     return set_error(FTB_EINVAL, "xattn: head_dim must be 64 or 128");
   }
-  if (impl == 0 || impl == 4) {  // flash kernel: 2 Q tiles per CTA; 4 (impl 0) or 8 (impl 4) softmax warps per tile
+  if (impl == 0) {  // flash kernel: 2 Q tiles per CTA, two softmax warpgroups
     if ((ldq & 7) || (ldk & 7) || (ldv & 7) || (ldo & 7)) return set_error(FTB_EINVAL, "fmha: ld alignment");
-    if (impl == 4) {
-      if (head_dim == 128) return launch_fmha2<128, 8>(p, s, ws, ws_bytes);
-      if (head_dim == 64) return launch_fmha2<64, 8>(p, s, ws, ws_bytes);
-    } else {
-      if (head_dim == 128) return launch_fmha2<128, 4>(p, s, ws, ws_bytes);
-      if (head_dim == 64) return launch_fmha2<64, 4>(p, s, ws, ws_bytes);
-    }
+    if (head_dim == 128) return launch_fmha2<128>(p, s, ws, ws_bytes);
+    if (head_dim == 64) return launch_fmha2<64>(p, s, ws, ws_bytes);
     return set_error(FTB_EINVAL, "fmha: head_dim must be 64 or 128");
   }
-  if (impl != 1) return set_error(FTB_EINVAL, "attention: impl must be 0 / 4 (flash), 1 (CUDA-core) or 3 (short KV)");
+  if (impl != 1) return set_error(FTB_EINVAL, "attention: impl must be 0 (flash), 1 (CUDA-core) or 3 (short KV)");
   if (head_dim <= 16) return launch_small<16>(p, s);
   if (head_dim <= 32) return launch_small<32>(p, s);
   if (head_dim <= 64) return launch_small<64>(p, s);

@@ -485,7 +485,7 @@ class DeviceVAEDecoder:
                 self._host[key] = host
             host.copy_(out, non_blocking=True)
         stream.synchronize()
-        return host.numpy().copy() if host.dtype == torch.uint8 else host.float().numpy()
+        return host.numpy().copy()   # the pinned buffer is reused by the next chunk
 
     def decode_device_async(self, z, stream, slot=0, gather=False):
         """decode_device without the host wait: decode + D2H into pinned buffer `slot` are
