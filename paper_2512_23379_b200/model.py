@@ -300,6 +300,10 @@ class DeviceDenoiser:
     def upload_cond(self):
         """Device half: cond input -> cond tokens (sig + frame pos ; ref) and the
         per-layer cross-attention K|V (net.py:233-237). Capturable in a CUDA graph."""
+        with ops.nvtx("cond + cross K/V fold"):
+            self._upload_cond()
+
+    def _upload_cond(self):
         cfg, B, W = self.cfg, self.buf, self.w
         nsig = self.n_cond - 1
         ci = B["cond_in"]
@@ -365,6 +369,7 @@ class DeviceDenoiser:
                      rows_per_group=T, row_offset=s0, K=W.mats["in.w"][1], M=Ls, lda=self.kin, stream=s)
         u, qkv, ao, ffb = B["u"], B["qkv"], B["ao"], B["ff"]
         for i in range(cfg.layers):
+            ops.nvtx_push("layer %d" % i)
             p = "layers.%d." % i
             if wan:
                 md = fv["mods"][i]  # [L_c + 1, 6m]
@@ -420,6 +425,7 @@ class DeviceDenoiser:
             else:
                 ops.gemm(ffb, W.mats[p + "ffn.w2"][0], h, "resid_f32", bias=W.vecs[p + "ffn.b2"], stream=s,
                          tail_counters=tail)
+            ops.nvtx_pop()
         if wan:
             fm = fv["final"]
             ops.norm_modulate(h, u, shift=fm[:, 0:m], scale=fm[:, m:2 * m], rows_per_group=T, row_offset=s0, stream=s)
@@ -456,7 +462,8 @@ class DeviceDenoiser:
             fv = self.frame_vectors(frame_t)
             if trace is not None:
                 trace.append((float(t), z.clone()))
-            self.step(motion, z, reference, fv, x0_out=x0_out, ddim=coeffs[i] if i + 1 < len(ts) else None)
+            with ops.nvtx("ladder step %d (t=%.3g)" % (i, t)):
+                self.step(motion, z, reference, fv, x0_out=x0_out, ddim=coeffs[i] if i + 1 < len(ts) else None)
             if trace is not None:
                 trace[-1] = trace[-1] + (x0_out.clone(),)
         return x0_out

@@ -7,7 +7,9 @@ is the tcgen05 B-operand layout. The reference stores (in, out) and computes
 x @ W + b (`backends/reference.py:17-18`); W^T is the same matrix.
 """
 
+import contextlib
 import ctypes as C
+import os
 
 import torch
 
@@ -38,6 +40,33 @@ class _Prof:
             self.e1.record(self.s)
             PROFILER.append((self.kind, self.e0, self.e1, self.flops, self.nbytes))
         return False
+
+
+_NVTX = os.environ.get("FTB_NVTX", "1") != "0"
+
+
+def nvtx_push(name):
+    if _NVTX and torch.cuda.is_available():
+        torch.cuda.nvtx.range_push(name)
+
+
+def nvtx_pop():
+    if _NVTX and torch.cuda.is_available():
+        torch.cuda.nvtx.range_pop()
+
+
+@contextlib.contextmanager
+def nvtx(name):
+    """NVTX range around a stage (chunk, ladder step, DiT layer, decode) for nsys / ncu
+    --nvtx filtering; host-side markers only (inside a captured graph they mark the capture)."""
+    on = _NVTX and torch.cuda.is_available()
+    if on:
+        torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        if on:
+            torch.cuda.nvtx.range_pop()
 
 
 KINDS = {"bf16": A.EPI_BF16, "gelu_bf16": A.EPI_GELU_BF16, "f32": A.EPI_F32,

@@ -164,6 +164,10 @@ class DeviceStreamer:
         return self.x0_static
 
     def denoise_chunk(self, c, window, noise=None):
+        with ops.nvtx("denoise chunk %d" % c):
+            return self._denoise_chunk(c, window, noise)
+
+    def _denoise_chunk(self, c, window, noise=None):
         """Runs chunk c on the current stream; returns the device x0 slot
         (targets). `noise` (host f64) defaults to the reference draw. Inputs are
         staged in pinned memory (double-buffered) and copied H2D in stream order."""
@@ -436,7 +440,8 @@ class StreamSession:
                     self._decode_stream.wait_event(ev)
                     d0 = torch.cuda.Event(enable_timing=True)
                     d0.record(self._decode_stream)
-                    frames = self.codec.decode_device(x0, self._decode_stream)   # waits for the frames
+                    with ops.nvtx("decode chunk %d" % c):
+                        frames = self.codec.decode_device(x0, self._decode_stream)   # waits for the frames
                     d1 = torch.cuda.Event(enable_timing=True)
                     d1.record(self._decode_stream)
                     d1.synchronize()

@@ -356,7 +356,8 @@ class DeviceVAEDecoder:
         communicator the output is this rank's row slab [T*tf, H_local, W, .]; with
         gather=True every slab is collected into rank 0's full frames (returned on rank 0,
         None on the other ranks)."""
-        out = self._decode(z, stream)
+        with ops.nvtx("vae decode"):
+            out = self._decode(z, stream)
         self.last_slab = out
         if not (gather and self.split):
             return out

@@ -78,17 +78,18 @@ def _run(world, transport, dev):
     return got, stats
 
 
-@pytest.mark.parametrize("transport", ["coll", "peer"])
-def test_stream_session_two_ranks_matches_one(cuda, transport):
+@pytest.mark.parametrize("world,transport", [(2, "coll"), (2, "peer"), (8, "peer")])
+def test_stream_session_ranks_match_one(cuda, world, transport):
+    """g = 8: 8 heads (one per rank), 12 latent rows split 2,2,2,2,1,1,1,1."""
     one, _ = _run(1, None, cuda)
-    two, st = _run(2, transport, cuda)
+    two, st = _run(world, transport, cuda)
     assert [f.index for f in two] == [f.index for f in one] == list(range(56))
     assert [f.chunk for f in two] == [f.chunk for f in one]
     a = np.stack([f.state for f in one]).astype(int)
     b = np.stack([f.state for f in two]).astype(int)
     assert a.shape == b.shape == (56, 96, 128, 3)
     assert np.mean(np.abs(a - b) <= 2) > 0.99
-    assert st[0].frames_emitted == 56 and st[1].frames_emitted == 0   # only rank 0 emits
+    assert st[0].frames_emitted == 56 and all(x.frames_emitted == 0 for x in st[1:])   # only rank 0 emits
 
 
 def test_generate_two_ranks_matches_one(cuda):
