@@ -1,7 +1,11 @@
-"""One small launch of every kernel family of libftb2.so, for compute-sanitizer
+"""One small launch of every kernel family of libftb2.so, meant for compute-sanitizer
 (memcheck / racecheck / synccheck, one tool per gpurun call):
 
     compute-sanitizer --tool memcheck python scripts/sanitize_kernels.py
+
+compute-sanitizer is CLOSED on this GPU pool (profiles/r02_sanitizer.md); the out-of-bounds
+checks run as guard-band tests instead (tests/test_guard_bands_gpu.py), and this sweep runs
+plain as a smoke of every kernel family.
 
 GEMM (single CTA, CTA pair, residual + split-K tail, QKV + RoPE, segment softmax, block-diagonal
 band), flash attention (+ KV-split + combine), short-KV and CUDA-core attention, norm / AdaLN,
