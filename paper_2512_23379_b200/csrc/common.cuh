@@ -31,6 +31,13 @@ FTB_DEV void tma_store_2d(const CUtensorMap* map, const void* smem_src, int x, i
                "r"(smem_u32(smem_src)), "r"(x), "r"(y)
                : "memory");
 }
+// 1-D bulk copy global -> shared (TMA engine, no tensor map): bytes % 16 == 0, 16-byte aligned.
+FTB_DEV void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 FTB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 FTB_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 

@@ -135,6 +135,101 @@ __global__ void __launch_bounds__(T) norm_modulate_vec_kernel(
 }
 
 
+
+// Persistent row-range LayerNorm / AdaLN (the default path for 16-byte aligned rows with
+// N % (4*T) == 0): each CTA owns a contiguous range of rows and streams them through a ring of
+// NS shared-memory slots filled by 1-D TMA bulk copies, so NS rows per CTA are in flight without
+// holding registers. The CTA keeps its slice of the modulation — mul = gamma * (1 + scale),
+// add = beta + shift of the row's frame group — in registers and reloads it only when the group
+// changes (a range spans at most a few groups), instead of re-reading both vectors from L2 for
+// every row. Two-pass fp32 statistics per row as above.
+template <int V, int T, int NS>
+__global__ void __launch_bounds__(T) norm_rows_kernel(
+    const float* __restrict__ x, long long ldx, int N, int M, int rows_per_cta, const float* __restrict__ gamma,
+    const float* __restrict__ beta, const float* __restrict__ scale, const float* __restrict__ shift,
+    long long mod_ld, int rows_per_group, long long row_offset, float eps, __nv_bfloat16* __restrict__ y,
+    long long ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  extern __shared__ __align__(128) uint8_t norm_sm[];
+  __shared__ float red[T / 32];
+  float4* ring = reinterpret_cast<float4*>(norm_sm);
+  uint64_t* full = reinterpret_cast<uint64_t*>(norm_sm + (size_t)NS * N * 4);
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int r1 = min(M, r0 + rows_per_cta);
+  if (r0 >= r1) return;
+  const uint32_t row_bytes = (uint32_t)N * 4;
+  const int n4 = N >> 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < NS && r0 + s < r1; ++s) {
+      mbar_arrive_expect_tx(&full[s], row_bytes);
+      bulk_load_1d(ring + (size_t)s * n4, x + (long long)(r0 + s) * ldx, row_bytes, &full[s]);
+    }
+  long long gcur = -1;
+  float4 mul[V], add[V];
+  for (int r = r0, it = 0; r < r1; ++r, ++it) {
+    const long long g = rows_per_group > 0 ? (r + row_offset) / rows_per_group : 0;
+    if (g != gcur) {   // CTA-uniform
+      gcur = g;
+      const float4* sc = scale ? reinterpret_cast<const float4*>(scale + g * mod_ld) : nullptr;
+      const float4* sh = shift ? reinterpret_cast<const float4*>(shift + g * mod_ld) : nullptr;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const int c = threadIdx.x + i * T;
+        float4 m = gamma ? __ldg(reinterpret_cast<const float4*>(gamma) + c) : make_float4(1.f, 1.f, 1.f, 1.f);
+        float4 a = beta ? __ldg(reinterpret_cast<const float4*>(beta) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (sc) {
+          const float4 t = __ldg(sc + c);
+          m = make_float4(m.x * (1.f + t.x), m.y * (1.f + t.y), m.z * (1.f + t.z), m.w * (1.f + t.w));
+        }
+        if (sh) {
+          const float4 t = __ldg(sh + c);
+          a = make_float4(a.x + t.x, a.y + t.y, a.z + t.z, a.w + t.w);
+        }
+        mul[i] = m;
+        add[i] = a;
+      }
+    }
+    const int slot = it % NS;
+    mbar_wait(&full[slot], (uint32_t)(it / NS) & 1);
+    float4 v[V];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      v[i] = ring[(size_t)slot * n4 + threadIdx.x + i * T];
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+    const float mean = block_sum<T>(s, red) / N;
+    // every thread has read the slot (block_sum's barriers): refill it NS rows ahead
+    if (threadIdx.x == 0 && r + NS < r1) {
+      mbar_arrive_expect_tx(&full[slot], row_bytes);
+      bulk_load_1d(ring + (size_t)slot * n4, x + (long long)(r + NS) * ldx, row_bytes, &full[slot]);
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float a = v[i].x - mean, b = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+      ss += (a * a + b * b) + (c * c + d * d);
+    }
+    const float rstd = rsqrtf(block_sum<T>(ss, red) / N + eps);
+    uint2* yr = reinterpret_cast<uint2*>(y + (long long)r * ldy);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float4 m = mul[i], a = add[i];
+      const float ox = fmaf((v[i].x - mean) * rstd, m.x, a.x), oy = fmaf((v[i].y - mean) * rstd, m.y, a.y);
+      const float oz = fmaf((v[i].z - mean) * rstd, m.z, a.z), ow = fmaf((v[i].w - mean) * rstd, m.w, a.w);
+      yr[threadIdx.x + i * T] = make_uint2(pack_bf16(ox, oy), pack_bf16(oz, ow));
+    }
+    if (threadIdx.x == 0) {
+      if (mean_out) mean_out[r] = mean;
+      if (rstd_out) rstd_out[r] = rstd;
+    }
+  }
+}
+
 // Composite assembly (diffusion.py:150-179 + stacked :133-135) fused with the
 // 2x2 spatial patchify of the wan-mode token grid. One thread per output element.
 __global__ void patchify_kernel(const float* __restrict__ motion, const float* __restrict__ z,
@@ -317,6 +412,55 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
   const bool vec = (N % 4 == 0) && N <= 4 * 256 * 8 && (ldx % 4 == 0) && (ldy % 4 == 0) && (!scale || mod_ld % 4 == 0) &&
                    al16(x) && (reinterpret_cast<uintptr_t>(y) & 7) == 0 && (!gamma || al16(gamma)) &&
                    (!beta || al16(beta)) && (!scale || al16(scale)) && (!shift || al16(shift)) && N >= 512;
+  // persistent TMA-ring kernel: whole float4 slices per thread, 16-byte aligned rows
+  {
+    const int n4 = N / 4;
+    const int T = (n4 % 256 == 0 && n4 / 256 <= 8) ? 256 : ((n4 % 128 == 0 && n4 / 128 <= 8) ? 128 : 0);
+    constexpr int NS = 4;
+    const size_t smem = (size_t)NS * N * 4 + NS * 8;
+    if (vec && T && ((ldx * 4) % 16 == 0) && smem <= 110 * 1024) {
+      const int V = n4 / T;
+      const int grid0 = sm_count() * (smem <= 100 * 1024 ? 2 : 1);
+      const int grid = M < grid0 ? M : grid0;
+      const int rpc = (M + grid - 1) / grid;
+#define FTB_NORM_ROWS(VV, TT)                                                                                        \
+  do {                                                                                                                \
+    static bool cfg_done = false;                                                                                     \
+    if (!cfg_done) {                                                                                                  \
+      cudaFuncSetAttribute(norm_rows_kernel<VV, TT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);    \
+      cfg_done = true;                                                                                                \
+    }                                                                                                                 \
+    norm_rows_kernel<VV, TT, NS><<<grid, TT, smem, S(stream)>>>(x, ldx, N, M, rpc, gamma, beta, scale, shift, mod_ld, \
+                                                                rows_per_group, row_offset, eps, (__nv_bfloat16*)y,   \
+                                                                ldy, mean_out, rstd_out);                             \
+  } while (0)
+      if (T == 256) {
+        switch (V) {
+          case 1: FTB_NORM_ROWS(1, 256); break;
+          case 2: FTB_NORM_ROWS(2, 256); break;
+          case 3: FTB_NORM_ROWS(3, 256); break;
+          case 4: FTB_NORM_ROWS(4, 256); break;
+          case 5: FTB_NORM_ROWS(5, 256); break;
+          case 6: FTB_NORM_ROWS(6, 256); break;
+          case 7: FTB_NORM_ROWS(7, 256); break;
+          default: FTB_NORM_ROWS(8, 256); break;
+        }
+      } else {
+        switch (V) {
+          case 1: FTB_NORM_ROWS(1, 128); break;
+          case 2: FTB_NORM_ROWS(2, 128); break;
+          case 3: FTB_NORM_ROWS(3, 128); break;
+          case 4: FTB_NORM_ROWS(4, 128); break;
+          case 5: FTB_NORM_ROWS(5, 128); break;
+          case 6: FTB_NORM_ROWS(6, 128); break;
+          case 7: FTB_NORM_ROWS(7, 128); break;
+          default: FTB_NORM_ROWS(8, 128); break;
+        }
+      }
+#undef FTB_NORM_ROWS
+      return check_launch("norm_rows_kernel");
+    }
+  }
   const bool narrow = N <= 4 * 128 * 4;
   if (vec && narrow && (N / 4) % 128 == 0) {
     // narrow rows (1.3B: m = 1536): 128 threads x 3 float4, every lane busy, twice the rows

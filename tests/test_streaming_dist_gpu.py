@@ -21,7 +21,7 @@ def _setup():
     from paper_2512_23379_b200.config import NetConfig
     from paper_2512_23379_b200.net import ParamStore
     from paper_2512_23379_b200.vae import VAEConfig, init_vae_params
-    cfg = NetConfig(256, 2, 8, 512, 16, mode="wan", patch=(1, 2, 2), audio_dim=16, audio_tokens=2)
+    cfg = NetConfig(512, 2, 8, 1024, 16, mode="wan", patch=(1, 2, 2), audio_dim=16, audio_tokens=2)   # hd 64
     store = ParamStore.init(cfg, 5)
     vcfg = VAEConfig(**VAE)
     P = init_vae_params(vcfg, 4)
