@@ -2,6 +2,8 @@
 // assembly / patchify, unpatchify + DDIM update, codec decode, casts, fills.
 // All are row- or element-parallel with vectorised, coalesced access; grids
 // are sized in multiples of the SM count.
+#include <algorithm>
+
 #include "common.cuh"
 #include "ftb_internal.h"
 
@@ -420,7 +422,10 @@ extern "C" int ftb_norm_modulate(const float* x, int64_t ldx, int32_t M, int32_t
     const size_t smem = (size_t)NS * N * 4 + NS * 8;
     if (vec && T && ((ldx * 4) % 16 == 0) && smem <= 110 * 1024) {
       const int V = n4 / T;
-      const int grid0 = sm_count() * (smem <= 100 * 1024 ? 2 : 1);
+      // CTAs per SM: as many rings as ~200 KB of shared memory holds (2 at m = 5120: 80 KB rings,
+      // 8 at m = 1536), so 8-16 rows per SM are in flight
+      const int cps = (int)std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / smem));
+      const int grid0 = sm_count() * cps;
       const int grid = M < grid0 ? M : grid0;
       const int rpc = (M + grid - 1) / grid;
 #define FTB_NORM_ROWS(VV, TT)                                                                                        \
