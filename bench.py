@@ -10,9 +10,10 @@ tokens at 416x720) followed by the decode of its 7 target latents
 
 `value`  : device time (CUDA events, max over ranks) with all inputs already
            resident in HBM (noise, audio features pre-uploaded).
-`e2e`    : the same chunks through the public engine API (`DeviceStreamer`,
-           host noise drawn with the reference's PCG64 stream, pinned H2D of
-           noise + driving window, D2H of the chunk's result every step).
+`e2e`    : the same chunks through the public engine API (`start_stream` ->
+           `StreamSession.push_signal / next_frames`, the reference's streaming surface):
+           host noise drawn with the reference's PCG64 stream, pinned H2D of noise +
+           driving window, D2H of the decoded RGB8 frames every step, host wall time.
 `roofline`: one extra instrumented chunk after the timed region, every GEMM
            launch bracketed by CUDA events on its stream: achieved =
            sum(2MNK) / sum(duration) vs MEASURED_PEAKS bf16_tflops_sustained.
@@ -445,50 +446,41 @@ def main():
             "decode_overlaps_denoise": overlap,
             "steps_per_chunk": scfg.sampler.steps, "frames_per_chunk": frames_per_chunk}
 
-    # ---------------- e2e through the public engine API (host inputs, D2H result)
+    # ---------------- e2e through the public engine API: a StreamSession (start_stream) on the same
+    # device weights, driven with host samples (push_signal) and drained frame by frame (next_frames):
+    # host PCG64 noise, pinned H2D of noise + window, the decode on the session's own stream, D2H of
+    # the RGB8 frames, the engine's three threads. Wall time on rank 0 from the first push of the
+    # timed chunks to the last frame, max over ranks (followers run in lockstep through the gather).
     e2e = None
     if not args.no_e2e:
-        host_out = torch.empty((S,) + fshape, dtype=torch.float32).pin_memory()
+        from paper_2512_23379_b200.streaming import start_stream
+        sess = start_stream(w, cfg, vae, None, scfg, reference_latent=ref_host, latent_hw=lat_hw, comm=comm)
+        hsync = comm.host_channel("bench") if comm is not None else None
+        rs = np.random.default_rng(11)
+        samples = (rs.standard_normal((nsteps * S, A, adim)) if cfg.mode == "wan"
+                   else rs.uniform(-1, 1, nsteps * S))
         d2h = [0]
 
-        pending = []
-
-        def e2e_chunk(c):
-            xo = ds.denoise_chunk(c, windows[c])          # host PCG64 noise + pinned H2D inside
-            if vae is not None:
-                # decoded uint8 frames -> pinned host slot c%2; the host waits for chunk c-1's
-                # frames (not chunk c's), so it enqueues chunk c+1 while chunk c runs
-                frames, ev = vae.decode_device_async(xo, stream, c & 1, gather=True)
-                if frames is not None:     # rank 0 receives the full frames
-                    pending.append((frames, ev))
-                if len(pending) > 1:
-                    f, e = pending.pop(0)
-                    e.synchronize()
-                    d2h[0] = f.numel() * f.element_size()
-            else:
-                host_out.copy_(xo, non_blocking=True)
-                d2h[0] = host_out.numel() * 4
-
-        def e2e_drain():
-            while pending:
-                f, e = pending.pop(0)
-                e.synchronize()
-                d2h[0] = f.numel() * f.element_size()
-        for c in range(args.warmup):
-            e2e_chunk(c)
-        e2e_drain()
-        torch.cuda.synchronize()
-        ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ee0.record(stream)
-        for c in range(args.warmup, nsteps):
-            e2e_chunk(c)
-        ee1.record(stream)
-        torch.cuda.synchronize()
-        e2e_drain()
-        ems = max_over_ranks(ee0.elapsed_time(ee1) / args.steps)
+        def run_chunks(c0, c1):
+            if rank == 0:
+                sess.push_signal((i, samples[i]) for i in range(c0 * S, c1 * S))
+                need, n = (c1 - c0) * frames_per_chunk, 0
+                while n < need:
+                    fr, _ = sess.next_frames(wait=True, timeout=1.0)
+                    n += len(fr)
+                    if fr:
+                        d2h[0] = int(np.asarray(fr[0].state).nbytes) * frames_per_chunk
+            if hsync is not None:
+                hsync.host_broadcast(None)      # followers wait here (gloo) while their session threads run
+        run_chunks(0, args.warmup)
+        t0 = time.perf_counter()
+        run_chunks(args.warmup, nsteps)
+        ems = max_over_ranks((time.perf_counter() - t0) * 1000.0 / args.steps)
+        sess.close()
         h2d = ds.noise_host[0].numel() * 4 + d.buf["cond_in"].numel() * 2
         e2e = {"value": frames_per_chunk * 1000.0 / ems, "unit": "FPS", "ms_per_step": ems,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0]}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h[0],
+               "api": "streaming.start_stream -> StreamSession.push_signal / next_frames (unpaced, host wall time)"}
 
     # ---------------- instrumented chunk: per-kernel durations for the roofline
     ops.PROFILER = []

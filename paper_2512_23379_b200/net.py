@@ -88,7 +88,13 @@ class _DeviceRunner:
         self.cfg = cfg
         self.device = torch.device(device)
         self.comm = comm
-        self.weights = DeviceWeights.from_host(cfg, store.params, self.device)
+        if isinstance(store, DeviceWeights):   # already resident (checkpoint.load_device_weights, synthetic)
+            if store.cfg != cfg:
+                raise ConfigError("device weights were built for a different NetConfig")
+            self.weights = store
+            self.device = store.device
+        else:
+            self.weights = DeviceWeights.from_host(cfg, store.params, self.device)
         self._geo = {}
         self.stream = None
 

@@ -476,6 +476,9 @@ class StreamSession:
 
 
 def start_stream(store, net_cfg, codec, reference_frame, cfg: StreamConfig, **kw) -> StreamSession:
+    """streaming.py:359-361. `store`: the reference's ParamStore (uploaded once, cached per
+    store) or device-resident weights (`model.DeviceWeights`, e.g. from
+    `checkpoint.load_device_weights` — a 14B host fp64 store would need 105 GiB)."""
     return StreamSession(store, net_cfg, codec, reference_frame, cfg, **kw)
 
 
