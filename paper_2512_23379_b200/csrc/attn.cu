@@ -235,6 +235,15 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&s_full[t], j & 1);
       FTB_TL(t, j, 1);
       tc_fence_after();
+#ifdef FTB_FMHA_NOSOFTMAX   // debug: MMA / TMA pipeline alone (the hand-off without any softmax work)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&p_lo[t]);
+        mbar_arrive(&p_full[t]);
+      }
+      continue;
+#endif
       uint32_t sr[128];
       tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(sr + 0));
       tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
