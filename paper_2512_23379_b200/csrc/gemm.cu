@@ -144,7 +144,7 @@ __device__ __forceinline__ bool resid_tile_pipelined(const GemmParams& p, uint32
 // four full 128-byte lines (the row-per-thread path touches 32 lines per instruction and is
 // L1-wavefront bound at short K). For RESID, h of chunk c+1 is loaded before chunk c is
 // combined. Same arithmetic as epilogue_chunk.
-template <int WIDTH>
+template <int WIDTH, bool GPF>
 __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tmem_row, int gr0, int gc_base,
                                                 float4* stg, bool add_bias = true) {
   const int lane = lane_id();
@@ -155,18 +155,37 @@ __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tm
   float* out = reinterpret_cast<float*>(p.out) + (long long)(gr0 + sub) * p.ldc + gc_base + 4 * j;
   const long long step = 4 * p.ldc;
   const int rows_left = p.M - gr0 - sub;  // row 4i+sub is live while 4i < rows_left
-  float4 hb[2][8];
-  auto load = [&](int c, float4 (&dst)[8]) {
+  const bool use_bias = add_bias && p.bias;
+  const bool gated = resid && p.group_vec;
+  // GPF (short K, where the epilogue bounds the tile): the warp's 32 rows almost always lie in one
+  // gate group (a frame: 1170 rows); then the gate row is one float4 per chunk per thread, fetched
+  // with the h rows of that chunk instead of inside the combine, where its latency sat on the
+  // critical path (K = 1600: 206 -> 180 us); a block straddling two groups takes the per-row path.
+  // Long K keeps the per-row loads: the extra registers spill there (+1-2 %).
+  long long g0 = 0;
+  bool uni = GPF;
+  if (GPF && gated && p.rows_per_group > 0) {
+    g0 = (gr0 + p.row_offset) / p.rows_per_group;
+    uni = (min(gr0 + 31, p.M - 1) + p.row_offset) / p.rows_per_group == g0;
+  }
+  float4 hb[2][8], gb[2], bb[2];
+  auto load = [&](int c, int s) {
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      dst[i] = (resid && 4 * i < rows_left) ? *reinterpret_cast<const float4*>(out + i * step + c * 32)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      hb[s][i] = (resid && 4 * i < rows_left) ? *reinterpret_cast<const float4*>(out + i * step + c * 32)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int gc = gc_base + c * 32 + 4 * j;
+    if (GPF) {
+      gb[s] = (gated && uni) ? __ldg(reinterpret_cast<const float4*>(p.group_vec + g0 * p.group_ld + gc))
+                             : make_float4(1.f, 1.f, 1.f, 1.f);
+      bb[s] = use_bias ? __ldg(reinterpret_cast<const float4*>(p.bias + gc)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   };
-  load(0, hb[0]);
+  load(0, 0);
 #pragma unroll
   for (int c = 0; c < WIDTH / 32; ++c) {
     if (c >= nch) break;  // warp-uniform
-    if (c + 1 < nch) load(c + 1, hb[(c + 1) & 1]);
+    if (c + 1 < nch) load(c + 1, (c + 1) & 1);
     uint32_t r[32];
     tmem_ld32(tmem_row + c * 32, r);
     tmem_ld_wait();
@@ -176,8 +195,8 @@ __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tm
                                                      __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
     __syncwarp();
     const int gc = gc_base + c * 32 + 4 * j;
-    const bool use_bias = add_bias && p.bias;
-    const float4 b = use_bias ? __ldg(reinterpret_cast<const float4*>(p.bias + gc)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 b = GPF ? bb[c & 1]
+                         : (use_bias ? __ldg(reinterpret_cast<const float4*>(p.bias + gc)) : make_float4(0.f, 0.f, 0.f, 0.f));
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int rr = 4 * i + sub, row = gr0 + rr;
@@ -191,8 +210,8 @@ __device__ __forceinline__ void staged_tile_f32(const GemmParams& p, uint32_t tm
         }
         float4* dst = reinterpret_cast<float4*>(out + i * step + c * 32);
         if (resid) {
-          float4 gg = make_float4(1.f, 1.f, 1.f, 1.f);
-          if (p.group_vec) {
+          float4 gg = GPF ? gb[c & 1] : make_float4(1.f, 1.f, 1.f, 1.f);
+          if (gated && !uni) {
             const long long g = (p.rows_per_group > 0) ? (row + p.row_offset) / p.rows_per_group : 0;
             gg = __ldg(reinterpret_cast<const float4*>(p.group_vec + g * p.group_ld + gc));
           }
@@ -629,7 +648,7 @@ __device__ __forceinline__ void tail_wait(const unsigned* flag, unsigned want) {
   __threadfence();
 }
 
-template <int EPG, bool STAGED>
+template <int EPG, bool STAGED, bool GPF = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmParams p) {
@@ -765,7 +784,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
         // K-slice of a tail tile: this warp's rows/columns of slice part-1 must be in h first
         if (w.slot >= 0 && w.part > 0)
           tail_wait(p.tail_flags + w.slot * 16 + rank * 8 + eg * 4 + q, (unsigned)w.part);
-        staged_tile_f32<split ? 128 : 256>(p, trow, gr - lane, gcb, stg, w.part == 0);
+        staged_tile_f32<split ? 128 : 256, GPF>(p, trow, gr - lane, gcb, stg, w.part == 0);
         const PairItem w2 = pair_item(item, num_tiles, n_clusters, p.tail_split, num_kb);  // cheaper than live regs
         if (w2.slot >= 0) {
           __threadfence();
@@ -804,19 +823,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
   if (warp == 2) tmem_dealloc_pair<512>(tmem_base);
 }
 
-template <int EPG, bool STAGED>
+template <int EPG, bool STAGED, bool GPF = false>
 static int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(gemm_tc_pair_kernel<EPG, STAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
+        cudaFuncSetAttribute(gemm_tc_pair_kernel<EPG, STAGED, GPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
     configured = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.N + 255) / 256);
   const int max_pairs = sm_count() / 2;
   const int pairs = tiles < max_pairs ? tiles : max_pairs;
-  gemm_tc_pair_kernel<EPG, STAGED><<<2 * pairs, GEMM_THREADS + (EPG - 1) * 128, PAIR_SMEM, stream>>>(ta, tb, p);
+  gemm_tc_pair_kernel<EPG, STAGED, GPF><<<2 * pairs, GEMM_THREADS + (EPG - 1) * 128, PAIR_SMEM, stream>>>(ta, tb, p);
   return check_launch("gemm_tc_pair_kernel");
 }
 
@@ -974,6 +993,7 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
         p.tail_split = sp;
       }
     }
+    if (staged && K <= 2048 && epg2) return launch_gemm_pair<2, true, true>(ta, tb, p, s);
     if (staged) return epg2 ? launch_gemm_pair<2, true>(ta, tb, p, s) : launch_gemm_pair<1, true>(ta, tb, p, s);
     return epg2 ? launch_gemm_pair<2, false>(ta, tb, p, s) : launch_gemm_pair<1, false>(ta, tb, p, s);
   }
