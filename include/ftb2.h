@@ -269,6 +269,16 @@ int ftb_conv3d_norm_bf16(const void* in, const void* halo_top, const void* halo_
                          int32_t W, int32_t Cin, const void* w_t, int32_t Cout, int32_t KT, int32_t KH, int32_t KW,
                          int32_t t0, const float* bias, const void* resid, int64_t resid_ld, void* out,
                          int64_t out_ld, int32_t T_out, int32_t mode, const ftb_conv_norm* norm, void* stream);
+/* RGB8 head of the decoder (3x3x3 causal conv, Cout = 3, uint8 RGB = clamp(rint((acc+bias+1)*127.5)))
+ * as a 1x1 GEMM per input frame with the 27 taps x 3 channels as its 81 output rows,
+ * Y[t][tap*3 + c][p] = sum_k w[c][k][tap] x[t][p][k] (w_taps bf16 [81][Cin], row tap*3 + c, tap =
+ * (dt*3 + dy)*3 + dx), stored tap-major per frame in the caller's bf16 workspace (>= 81 *
+ * (T_in*H*W + [2*T_in*W with halos]) elements), then a gather kernel summing each output pixel's
+ * 27 shifted taps. Output frame t reads input frames t0+t .. t0+t+2; spatial zero padding or halo rows as
+ * in ftb_conv3d_halo_bf16. out: uint8 [T_out][H][W][3]. */
+int ftb_conv3d_head_rgb8(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in, int32_t H,
+                         int32_t W, int32_t Cin, const void* w_taps, const float* bias, void* y_ws,
+                         int64_t y_ws_elems, void* out, int32_t T_out, int32_t t0, void* stream);
 /* y = [silu](x / max(||x||_2, eps) * sqrt(C) * gamma) per pixel, channel-last bf16. */
 int ftb_rmsnorm_silu_bf16(const void* x, int64_t n_pix, int32_t C, const float* gamma, float eps,
                           int32_t silu, void* y, void* stream);

@@ -79,6 +79,7 @@ _SIGS = {
                               i32, vp], i32),
     "ftb_conv3d_norm_bf16": ([vp, vp, vp, i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, vp, vp, i64, vp, i64, i32,
                               i32, C.POINTER(ConvNorm), vp], i32),
+    "ftb_conv3d_head_rgb8": ([vp, vp, vp, i32, i32, i32, i32, vp, vp, vp, i64, vp, i32, i32, vp], i32),
     "ftb_rmsnorm_silu_bf16": ([vp, i64, i32, vp, f32, i32, vp, vp], i32),
     "ftb_upsample2x_bf16": ([vp, i32, i32, i32, i32, vp, vp], i32),
     "ftb_nchw_to_nhwc_bf16": ([vp, i32, i32, i32, i32, vp, i32, vp], i32),

@@ -1257,3 +1257,95 @@ extern "C" int ftb_conv3d_halo_bf16(const void* in, const void* halo_top, const 
   return conv3d_impl(in, halo_top, halo_bot, T_in, H, W, Cin, w_t, Cout, KT, KH, KW, t0, bias, resid, resid_ld, out,
                      out_ld, T_out, mode, stream);
 }
+
+// ============================================================ RGB head as a 1x1 GEMM + 27-tap gather
+// The 96 -> 3 head conv (3x3x3, RGB8 store) as an implicit GEMM has N = 3 output channels: its
+// MMAs run at a few percent of the tensor rate and restage the haloed input for every tap. Here
+// the 27 taps x 3 channels become the M = 81 rows of a GEMM over the input pixels of each frame,
+//   Y[t][tap * 3 + c][p] = sum_k W[c][k][tap] x[t][p][k]      (x read once, K = Cin)
+// stored tap-major per frame (row n of frame t contiguous over its H*W pixels; one GEMM per frame
+// keeps a tile's 81 output rows within a frame's 49 MB instead of 81 rows 18 MB apart, which ran
+// 2.3x slower on address translation), and a gather sums each output pixel's 27 shifted taps:
+// coalesced 2-byte reads along x, every Y value read by exactly one output pixel. Halo rows
+// (split decode) get their own small Y block.
+namespace ftb {
+__global__ void __launch_bounds__(128) head_gather_rgb8_kernel(const __nv_bfloat16* __restrict__ Y,
+                                                               const __nv_bfloat16* __restrict__ Yt,
+                                                               const __nv_bfloat16* __restrict__ Yb, long long ldh,
+                                                               int H, int W, int t0, const float* __restrict__ bias,
+                                                               uint8_t* __restrict__ out) {
+  const int x = blockIdx.x * 128 + threadIdx.x, y = blockIdx.y, t = blockIdx.z;
+  if (x >= W) return;
+  const long long hw = (long long)H * W;
+  float acc[3] = {bias ? bias[0] : 0.f, bias ? bias[1] : 0.f, bias ? bias[2] : 0.f};
+#pragma unroll
+  for (int dt = 0; dt < 3; ++dt) {
+    const int tt = t0 + t + dt;
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      const int yy = y + dy - 1;
+      const __nv_bfloat16* base;
+      long long ld;
+      if (yy < 0) {
+        if (!Yt) continue;
+        base = Yt + (long long)tt * W, ld = ldh;
+      } else if (yy >= H) {
+        if (!Yb) continue;
+        base = Yb + (long long)tt * W, ld = ldh;
+      } else {
+        base = Y + (long long)tt * 81 * hw + (long long)yy * W, ld = hw;
+      }
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int xx = x + dx - 1;
+        if (xx < 0 || xx >= W) continue;
+        const int tap = (dt * 3 + dy) * 3 + dx;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] += __bfloat162float(base[(long long)(tap * 3 + c) * ld + xx]);
+      }
+    }
+  }
+  uint8_t* o = out + (((long long)t * H + y) * W + x) * 3;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) o[c] = (uint8_t)fminf(fmaxf(rintf((acc[c] + 1.f) * 127.5f), 0.f), 255.f);
+}
+}  // namespace ftb
+
+extern "C" int ftb_conv3d_head_rgb8(const void* in, const void* halo_top, const void* halo_bot, int32_t T_in,
+                                    int32_t H, int32_t W, int32_t Cin, const void* w_taps, const float* bias,
+                                    void* y_ws, int64_t y_ws_elems, void* out, int32_t T_out, int32_t t0,
+                                    void* stream) {
+  if (!in || !w_taps || !y_ws || !out || T_in <= 0 || H <= 0 || W <= 0 || Cin <= 0 || (Cin % 8) || T_out <= 0 ||
+      t0 < 0 || t0 + T_out + 2 > T_in || (!halo_top) != (!halo_bot))
+    return set_error(FTB_EINVAL, "conv3d_head_rgb8: bad arguments (Cin % 8 == 0, t0 + T_out + 2 <= T_in, both halos)");
+  const long long hw = (long long)H * W, npix = (long long)T_in * hw, nh = (long long)T_in * W;
+  const long long need = 81 * (npix + (halo_top ? 2 * nh : 0));
+  if (y_ws_elems < need) return set_error(FTB_EINVAL, "conv3d_head_rgb8: workspace too small");
+  if (hw > 0x7fffffffLL || nh > 0x7fffffffLL) return set_error(FTB_EINVAL, "conv3d_head_rgb8: frame too large");
+  __nv_bfloat16* Y = reinterpret_cast<__nv_bfloat16*>(y_ws);
+  const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(in);
+  ftb_epilogue e{};
+  e.kind = FTB_EPI_BF16;
+  e.ldc = hw;
+  int rc;
+  // per frame: Y[t] = W_taps . X[t]^T, M = 81 tap-channels (A = w_taps [81][Cin]), N = the frame's pixels
+  for (int t = 0; t < T_in; ++t) {
+    e.out = Y + (long long)t * 81 * hw;
+    if ((rc = ftb_gemm_bf16(w_taps, Cin, 1, 0, X + (long long)t * hw * Cin, Cin, 81, (int32_t)hw, Cin, &e, stream)))
+      return rc;
+  }
+  __nv_bfloat16 *Yt = nullptr, *Yb = nullptr;
+  if (halo_top) {
+    Yt = Y + 81 * npix;
+    Yb = Yt + 81 * nh;
+    e.ldc = nh;
+    e.out = Yt;
+    if ((rc = ftb_gemm_bf16(w_taps, Cin, 1, 0, halo_top, Cin, 81, (int32_t)nh, Cin, &e, stream))) return rc;
+    e.out = Yb;
+    if ((rc = ftb_gemm_bf16(w_taps, Cin, 1, 0, halo_bot, Cin, 81, (int32_t)nh, Cin, &e, stream))) return rc;
+  }
+  dim3 grid((W + 127) / 128, H, T_out);
+  head_gather_rgb8_kernel<<<grid, 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      Y, Yt, Yb, nh, H, W, t0, bias, reinterpret_cast<uint8_t*>(out));
+  return check_launch("head_gather_rgb8_kernel");
+}

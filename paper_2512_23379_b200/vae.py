@@ -156,12 +156,16 @@ class DeviceVAEDecoder:
     (zeros at the global edges), so the split decode equals the unsplit one.
     The causal caches of the halo rows travel with the caches of the slabs."""
 
-    def __init__(self, cfg: VAEConfig, device, params=None, seed=0, rgb8=True, comm=None, fuse_norm=True):
+    def __init__(self, cfg: VAEConfig, device, params=None, seed=0, rgb8=True, comm=None, fuse_norm=True,
+                 head_gemm=True):
         from .dist import LocalComm
         self.cfg = cfg
         self.dev = torch.device(device)
         self.prog, shapes = vae_program(cfg)
         self.rgb8 = rgb8
+        # RGB8 head as one 1x1 GEMM (27 taps x 3 channels as output rows) + a 27-tap gather
+        # (ftb_conv3d_head_rgb8) instead of the N = 3 implicit-GEMM conv
+        self.head_gemm = head_gemm
         # RMS norm + SiLU of a conv output folded into that conv's epilogue whenever one N tile
         # holds every channel of a pixel (Cout <= 192): the normalised bf16 tensor is written
         # straight into the next conv's input buffer (no fp32 re-read, no separate pass)
@@ -327,6 +331,9 @@ class DeviceVAEDecoder:
             halos = self._exchange_halos(L, inp, T_in, Cin)
         tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%d %d->%d k%d%d%d" % (
             T_out, H, W, Cin, cw.cout, kt, kh, kw)
+        if (mode & 15) == 2 and self.head_gemm and (kt, kh, kw) == (3, 3, 3) and Cin % 8 == 0:
+            self._head_rgb8(inp, T_in, H, W, Cin, cw, out, t0, T_out, stream, halos)
+            return
         mode = mode | (A.CONV_VARIANT << 8)   # kernel selection of this call (0 = auto; A/B runs)
         with ops._Prof(tag, 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
             if norm is not None:
@@ -343,6 +350,21 @@ class DeviceVAEDecoder:
             else:
                 A.call("ftb_conv3d_bf16", A.ptr(inp), T_in, H, W, Cin, A.ptr(cw.wt), cout, kt, kh, kw, t0,
                        A.ptr(cw.b), A.ptr(resid), resid_ld, A.ptr(out), out_ld, T_out, mode, A.stream_ptr(stream))
+
+    def _head_rgb8(self, inp, T_in, H, W, Cin, cw, out, t0, T_out, stream, halos):
+        if getattr(cw, "w_taps", None) is None:   # [81][Cin]: row tap*3 + c, tap = (dt*3+dy)*3+dx
+            cw.w_taps = cw.wt[:3].reshape(3, 27, Cin).permute(1, 0, 2).reshape(81, Cin).contiguous()
+        need = 81 * (T_in * H * W + (2 * T_in * W if halos else 0))
+        ws = getattr(self, "_head_ws", None)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.bfloat16, device=self.dev)
+            self._head_ws = ws
+        tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%d %d->3 head gemm+gather" % (T_out, H, W, Cin)
+        with ops._Prof(tag, 2.0 * T_out * H * W * 3 * 27 * Cin, 0.0, stream):
+            A.call("ftb_conv3d_head_rgb8", A.ptr(inp), A.ptr(halos[0]) if halos else None,
+                   A.ptr(halos[1]) if halos else None, T_in, H, W, Cin, A.ptr(cw.w_taps), A.ptr(cw.b), A.ptr(ws),
+                   ws.numel(), A.ptr(out), T_out, t0, A.stream_ptr(stream))
+        A.LAUNCHES[0] += T_in + (2 if halos is not None else 0)   # per-frame GEMMs (+ halos) + gather
 
     def _rms(self, x, npix, C, g, y, stream):
         fn = "ftb_rmsnorm_silu_f32" if x.dtype == torch.float32 else "ftb_rmsnorm_silu_bf16"

@@ -191,6 +191,47 @@ def test_split_vae_matches_unsplit(cuda, world, transport):
         assert len(gathered) == 1 and np.array_equal(gathered[0], cat)   # rank 0 alone gets all slabs
 
 
+@pytest.mark.parametrize("transport", ["coll", "peer"])
+def test_split_vae_rgb8_head_equals_unsplit(cuda, transport):
+    """RGB8 decode (head as 1x1 GEMM + 27-tap gather, halo rows through their own GEMM blocks),
+    split over 3 ranks and gathered into rank 0 == the unsplit RGB8 decode, byte for byte."""
+    from paper_2512_23379_b200.dist import ThreadComm, ThreadPeerComm
+    from paper_2512_23379_b200.vae import DeviceVAEDecoder, VAEConfig, init_vae_params
+    cfg = VAEConfig(**SMALL_VAE)
+    P = init_vae_params(cfg, 6)
+    r = np.random.default_rng(2)
+    zs = [r.standard_normal((3, 16, 7, 9)) for _ in range(2)]
+    ref = DeviceVAEDecoder(cfg, cuda, params=P, rgb8=True)
+    want = [ref.decode_device(torch.as_tensor(z, dtype=torch.float32, device=cuda), torch.cuda.current_stream())
+            for z in zs]
+    world = 3
+    comms = (ThreadPeerComm if transport == "peer" else ThreadComm).make(world)
+    got, errs = [None, None], []
+
+    def worker(rk):
+        try:
+            torch.cuda.set_device(cuda)
+            s = torch.cuda.Stream(device=cuda)
+            dec = DeviceVAEDecoder(cfg, cuda, params=P, rgb8=True, comm=comms[rk])
+            for i, z in enumerate(zs):
+                with torch.cuda.stream(s):
+                    zd = torch.as_tensor(z, dtype=torch.float32, device=cuda)
+                out = dec.decode_device(zd, s)
+                if rk == 0:
+                    got[i] = out
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            raise
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    for i in range(2):
+        assert got[i].dtype == np.uint8 and np.array_equal(got[i], want[i]), i
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_peer_barrier_protocol_concurrent_ranks(cuda, world):
     """The device barrier's protocol (release-store of the epoch into every rank's flag word,

@@ -237,3 +237,34 @@ def test_conv3d_fused_norm_kernel(cuda):
         nrmv = ref / np.maximum(np.linalg.norm(ref, axis=-1, keepdims=True), 1e-12) * np.sqrt(Cout) * g
         want = nrmv / (1 + np.exp(-nrmv))
         assert rel(nout.float().cpu().numpy(), want) < 5e-3, (T, H, W, Cin, Cout)
+
+
+@pytest.mark.parametrize("T,H,W,C,halo", [(2, 3, 150, 96, False), (3, 5, 37, 32, False), (2, 4, 130, 96, True)])
+def test_head_gemm_gather_matches_conv(cuda, T, H, W, C, halo):
+    """RGB8 head as 1x1 GEMM (27 taps x 3 channels = 81 output rows) + 27-tap gather
+    (ftb_conv3d_head_rgb8) vs the implicit-GEMM conv and the fp64 oracle: within one RGB8 step
+    (the tap partial sums are rounded to bf16 before the 27-term sum), halo rows included."""
+    from paper_2512_23379_b200 import _capi as A
+    r = np.random.default_rng(T * 7 + W)
+    x = bfr(r.standard_normal((T + 2, H, W, C)))
+    w3 = bfr(r.standard_normal((3, C, 3, 3, 3)) / 40)
+    b = r.standard_normal(3) * 0.1
+    top = bfr(r.standard_normal((T + 2, 1, W, C))) if halo else np.zeros((T + 2, 1, W, C))
+    bot = bfr(r.standard_normal((T + 2, 1, W, C))) if halo else np.zeros((T + 2, 1, W, C))
+    full = np.concatenate([top, x, bot], axis=1)
+    want = VO.to_rgb8(VO.conv3d(full, w3, b)[:, 1:H + 1])
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a)).to(torch.bfloat16).to(cuda)  # noqa: E731
+    xd = dev(x)
+    wt3 = torch.zeros(32, 27 * C, dtype=torch.bfloat16)
+    wt3[:3] = torch.as_tensor(np.transpose(w3, (0, 2, 3, 4, 1)).reshape(3, -1)).to(torch.bfloat16)
+    w_taps = wt3[:3].reshape(3, 27, C).permute(1, 0, 2).reshape(81, C).contiguous().to(cuda)
+    bd = torch.as_tensor(b, dtype=torch.float32).to(cuda)
+    ws = torch.empty(81 * ((T + 2) * H * W + 2 * (T + 2) * W), dtype=torch.bfloat16, device=cuda)
+    rgb = torch.empty(T, H, W, 3, dtype=torch.uint8, device=cuda)
+    td, bd_ = dev(top), dev(bot)   # keep the halo tensors alive until the launch has run
+    A.call("ftb_conv3d_head_rgb8", A.ptr(xd), A.ptr(td) if halo else None, A.ptr(bd_) if halo else None,
+           T + 2, H, W, C, A.ptr(w_taps), A.ptr(bd), A.ptr(ws), ws.numel(), A.ptr(rgb), T, 0, A.stream_ptr())
+    got = rgb.cpu().numpy().astype(int)
+    d = np.abs(got - want.astype(int))
+    # tap partials are rounded to bf16 before the 27-term sum: at most one RGB8 step off
+    assert d.max() <= 1 and np.mean(d == 0) > 0.8
