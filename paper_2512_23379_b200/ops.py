@@ -100,7 +100,7 @@ class RopeTables:
 def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=0, row_offset=0,
          M=None, K=None, lda=None, a_chunks=1, a_chunk_stride=0, heads=0, head_dim=0,
          heads_per_rank=0, rope=None, peers=None, band=None, stream=None, algo_flops=None, variant=None,
-         tail_counters=None):
+         tail_counters=None, prof_kind=None):
     """out <- epilogue(a[M,K] @ w_t[N,K]^T). `a` may be a raw buffer when
     a_chunks > 1 (Ulysses gather: M, K, lda, a_chunk_stride explicit).
     peers: device addresses (ints) for the peer-store epilogues (qkv_rope: one
@@ -150,7 +150,8 @@ def gemm(a, w_t, out, kind="bf16", *, bias=None, group_vec=None, rows_per_group=
     # algo_flops: the algorithmic FLOPs when the operands are structurally sparse (the
     # block-diagonal fold GEMMs), so the profile's TFLOP/s do not count multiplications by zero
     fl = 2.0 * M * N * K if algo_flops is None else float(algo_flops)
-    with _Prof("gemm" if PROFILE_DETAIL is None else "gemm:%s:%dx%dx%d" % (kind, M, N, K), fl, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
+    pk = prof_kind or ("gemm" if PROFILE_DETAIL is None else "gemm:%s:%dx%dx%d" % (kind, M, N, K))
+    with _Prof(pk, fl, 2.0 * (M * K + N * K) + out.element_size() * M * N, stream):
         A.call("ftb_gemm_bf16", A.ptr(a), lda, a_chunks, a_chunk_stride, A.ptr(w_t), _ld(w_t), M, N, K,
                C.byref(epi), A.stream_ptr(stream))
     return out

@@ -334,6 +334,16 @@ class DeviceVAEDecoder:
         if (mode & 15) == 2 and self.head_gemm and (kt, kh, kw) == (3, 3, 3) and Cin % 8 == 0:
             self._head_rgb8(inp, T_in, H, W, Cin, cw, out, t0, T_out, stream, halos)
             return
+        if (kt, kh, kw) == (1, 1, 1) and mode == self.OUT_F32 and resid is None and cw.cout % 32 == 0:
+            # 1x1x1 conv (resblock shortcut) = a plain GEMM over the pixels (the implicit-GEMM conv
+            # ran it at ~60 TFLOP/s)
+            npx = T_out * H * W
+            a = inp[t0 * H * W * Cin:(t0 + T_out) * H * W * Cin].view(npx, Cin)
+            tag = "conv" if ops.PROFILE_DETAIL is None else "conv:%dx%dx%d %d->%d k111 gemm" % (
+                T_out, H, W, Cin, cw.cout)
+            ops.gemm(a, cw.wt, out[:npx * out_ld].view(npx, out_ld)[:, :cw.cout], "f32", bias=cw.b[:cw.cout],
+                     stream=stream, prof_kind=tag)
+            return
         mode = mode | (A.CONV_VARIANT << 8)   # kernel selection of this call (0 = auto; A/B runs)
         with ops._Prof(tag, 2.0 * T_out * H * W * cw.cout * kt * kh * kw * Cin, 0.0, stream):
             if norm is not None:
