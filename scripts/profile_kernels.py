@@ -61,6 +61,20 @@ def main(which):
         for _ in range(3):
             A.call("ftb_conv3d_bf16", A.ptr(x), T + 2, Hh, W, C, A.ptr(wt), C, 3, 3, 3, 0, None, None, 0, A.ptr(out),
                    C, T, 16, A.stream_ptr())
+    if which in ("convres", "all"):   # conv2 of a 96-ch resblock: fp32 residual in, fp32 x + normalised bf16 out
+        import ctypes as Cty
+        T, Hh, W, C = 28, 416, 720, 96
+        x = torch.randn((T + 2) * Hh * W * C, device=dev).to(torch.bfloat16)
+        wt = (torch.randn(C, 27 * C, device=dev) / 50).to(torch.bfloat16)
+        res = torch.randn(T * Hh * W * C, device=dev)
+        out = torch.empty(T * Hh * W * C, device=dev, dtype=torch.float32)
+        nout = torch.empty(T * Hh * W * C, device=dev, dtype=torch.bfloat16)
+        g = torch.ones(C, device=dev)
+        b = torch.zeros(C, device=dev)
+        nrm = A.ConvNorm(A.ptr(g), A.ptr(nout), C, 1, 1)
+        for _ in range(3):
+            A.call("ftb_conv3d_norm_bf16", A.ptr(x), None, None, T + 2, Hh, W, C, A.ptr(wt), C, 3, 3, 3, 0, A.ptr(b),
+                   A.ptr(res), C, A.ptr(out), C, T, 16 | 32, Cty.byref(nrm), A.stream_ptr())
     torch.cuda.synchronize()
     print("ok", which)
 
