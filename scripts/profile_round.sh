@@ -16,7 +16,7 @@ fi
 for w in $WHICH; do
   python scripts/profile_kernels.py $w > /dev/null
 done
-declare -A K=([gemm]=gemm_tc [fmha]=fmha2 [xpb]=gemm_tc [xs]=gemm_tc [conv]=conv_ [norm]=norm_modulate)
+declare -A K=([gemm]=gemm_tc [fmha]=fmha2 [xpb]=gemm_tc [xs]=gemm_tc [conv]=conv_ [norm]=norm_)
 for w in $WHICH; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:${K[$w]} -s 1 -c 1 \
     -o $OUT/full_${R}_$w python scripts/profile_kernels.py $w > $OUT/full_${R}_$w.log 2>&1 || true
