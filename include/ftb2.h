@@ -152,6 +152,14 @@ int ftb_attention_impl(int32_t impl, const void* q, int64_t ldq, const void* k, 
                        int32_t heads, int32_t head_dim, float scale, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* The attention probabilities themselves, p[h][r][j] = softmax_j(q_r . k_j * scale) (fp32,
+ * [heads][Lq][Lk] dense): the `p` entry of the reference's mha_forward cache
+ * (backends/reference.py:86-88, returned at :92), which the flash kernels never materialise.
+ * CUDA-core, one CTA per (query, head); any head_dim <= 256. For the drop-in backend table's
+ * cache, not for the hot path. */
+int ftb_attention_probs(const void* q, int64_t ldq, const void* k, int64_t ldk, int32_t Lq, int32_t Lk,
+                        int32_t heads, int32_t head_dim, float scale, float* p, void* stream);
+
 /* Ulysses all-to-all #2 fused into the epilogue: output row r is stored at row r % peer_rows
  * of o_peers[r / peer_rows] (device pointers, peer-mapped; host array of n_peers entries). */
 int ftb_attention_scatter(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,

@@ -47,6 +47,7 @@ _SIGS = {
     "ftb_norm_modulate": ([vp, i64, i32, i32, vp, vp, vp, vp, i64, i32, i64, f32, vp, i64, vp, vp, vp], i32),
     "ftb_attention": ([vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp, C.c_size_t, vp], i32),
     "ftb_attention_workspace_bytes": ([i32, i32, i32, i32], C.c_size_t),
+    "ftb_attention_probs": ([vp, i64, vp, i64, i32, i32, i32, i32, f32, vp, vp], i32),
     "ftb_attention_impl": ([i32, vp, i64, vp, i64, vp, i64, vp, i64, i32, i32, i32, i32, f32, vp, C.c_size_t, vp],
                            i32),
     "ftb_attention_scatter": ([vp, i64, vp, i64, vp, i64, C.POINTER(vp), i32, i64, i64, i32, i32, i32, i32, f32,

@@ -865,6 +865,48 @@ static int launch_small(const AttnParams& p, cudaStream_t s) {
   return check_launch("attn_small_kernel");
 }
 
+// Attention probabilities for the reference mha_forward cache (backends/reference.py:86-88):
+// one CTA per (query r, head h); scores for every key into smem-free registers/global, row max
+// and sum by block reduction, then the normalised row. Any Lk; head_dim <= 256 (q row in smem).
+__global__ void __launch_bounds__(128) attn_probs_kernel(const __nv_bfloat16* __restrict__ q, long long ldq,
+                                                         const __nv_bfloat16* __restrict__ k, long long ldk, int Lq,
+                                                         int Lk, int hd, float scale, float* __restrict__ p) {
+  __shared__ float qs[256];
+  __shared__ float red[4];
+  const int r = blockIdx.x, h = blockIdx.y;
+  for (int d = threadIdx.x; d < hd; d += 128) qs[d] = __bfloat162float(q[(long long)r * ldq + h * hd + d]);
+  __syncthreads();
+  float* prow = p + ((long long)h * Lq + r) * Lk;
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < Lk; j += 128) {
+    const __nv_bfloat16* kr = k + (long long)j * ldk + h * hd;
+    float s = 0.f;
+    for (int d = 0; d < hd; ++d) s = fmaf(qs[d], __bfloat162float(kr[d]), s);
+    s *= scale;
+    prow[j] = s;
+    mx = fmaxf(mx, s);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  float sum = 0.f;
+  for (int j = threadIdx.x; j < Lk; j += 128) {
+    const float e = expf(prow[j] - mx);
+    prow[j] = e;
+    sum += e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  const float inv = 1.f / ((red[0] + red[1]) + (red[2] + red[3]));
+  for (int j = threadIdx.x; j < Lk; j += 128) prow[j] *= inv;
+}
+
 }  // namespace ftb
 
 using namespace ftb;
@@ -903,6 +945,19 @@ extern "C" size_t ftb_attention_workspace_bytes(int32_t Lq, int32_t Lk, int32_t 
   if (Lq <= 0 || Lk <= 0 || heads <= 0 || default_impl(Lq, Lk, head_dim) != 0) return 0;
   const int R = fmha2_split_items(Lq, Lk, heads);
   return R ? fmha2_ws_bytes(R, head_dim) : 0;
+}
+
+extern "C" int ftb_attention_probs(const void* q, int64_t ldq, const void* k, int64_t ldk, int32_t Lq, int32_t Lk,
+                                   int32_t heads, int32_t head_dim, float scale, float* p, void* stream) {
+  if (!q || !k || !p || Lq < 0 || Lk <= 0 || heads <= 0 || head_dim <= 0 || head_dim > 256)
+    return set_error(FTB_EINVAL, "attention_probs: bad arguments (head_dim must be in [1, 256])");
+  if (ldq < (int64_t)heads * head_dim || ldk < (int64_t)heads * head_dim)
+    return set_error(FTB_EINVAL, "attention_probs: ld smaller than heads * head_dim");
+  if (Lq == 0) return FTB_OK;
+  attn_probs_kernel<<<dim3(Lq, heads), 128, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(q), ldq, static_cast<const __nv_bfloat16*>(k), ldk, Lq, Lk, head_dim, scale,
+      p);
+  return check_launch("attn_probs_kernel");
 }
 
 #ifdef FTB_FMHA_TIMELINE

@@ -81,8 +81,9 @@ def layernorm_forward(x, gamma, beta):
 
 
 def mha_forward(xq, xkv, wq, wk, wv, wo, heads):
-    """(y, cache) (backends/reference.py:77-92). The flash kernel never
-    materialises the probabilities, so cache = (q, k, v, None, ctx)."""
+    """(y, cache) (backends/reference.py:77-92), cache = (q, k, v, p, ctx) as the reference's:
+    the flash kernel never materialises the probabilities, so p comes from a separate
+    device pass (ops.attention_probs) over the same bf16 q and k."""
     m = np.asarray(xq).shape[1]
     hd = m // heads
 
@@ -97,8 +98,9 @@ def mha_forward(xq, xkv, wq, wk, wv, wo, heads):
     ctx = torch.empty_like(q)
     ops.attention(q, k, v, ctx, heads, hd, q.shape[0], k.shape[0], 1.0 / math.sqrt(hd))
     y = dense_forward(ctx.double().cpu().numpy(), wo, np.zeros(np.asarray(wo).shape[1]))
+    probs = ops.attention_probs(q, k, heads, hd, q.shape[0], k.shape[0], 1.0 / math.sqrt(hd))
     split = [t.double().cpu().numpy().reshape(t.shape[0], heads, hd).transpose(1, 0, 2) for t in (q, k, v)]
-    return y, (split[0], split[1], split[2], None, ctx.double().cpu().numpy())
+    return y, (split[0], split[1], split[2], probs.double().cpu().numpy(), ctx.double().cpu().numpy())
 
 
 def _training_only(*_a, **_k):

@@ -175,6 +175,20 @@ def norm_modulate(x, out, *, gamma=None, beta=None, scale=None, shift=None, rows
     return out
 
 
+def attention_probs(q, k, heads, head_dim, Lq, Lk, scale, out=None, stream=None):
+    """softmax(q . k^T * scale) per head as fp32 [heads, Lq, Lk] (ftb_attention_probs): the p of
+    the reference mha_forward cache (backends/reference.py:86-88), which the flash kernels
+    never materialise."""
+    _need(q, torch.bfloat16, "q")
+    _need(k, torch.bfloat16, "k")
+    if out is None:
+        out = torch.empty(heads, Lq, Lk, dtype=torch.float32, device=q.device)
+    _need(out, torch.float32, "out")
+    A.call("ftb_attention_probs", A.ptr(q), _ld(q), A.ptr(k), _ld(k), int(Lq), int(Lk), int(heads), int(head_dim),
+           float(scale), A.ptr(out), A.stream_ptr(stream))
+    return out
+
+
 def attention_workspace_bytes(Lq, Lk, heads, head_dim):
     """fp32 workspace bytes of the flash kernel's KV-split tail round for this shape (0: none)."""
     return int(A.lib.ftb_attention_workspace_bytes(int(Lq), int(Lk), int(heads), int(head_dim)))
