@@ -8,7 +8,8 @@ checks run as guard-band tests instead (tests/test_guard_bands_gpu.py), and this
 plain as a smoke of every kernel family.
 
 GEMM (single CTA, CTA pair, residual + split-K tail, QKV + RoPE, segment softmax, block-diagonal
-band), flash attention (+ KV-split + combine), short-KV and CUDA-core attention, norm / AdaLN,
+band), flash attention (+ KV-split + combine), short-KV and CUDA-core attention, attention
+probabilities, norm / AdaLN,
 patchify / unpatch + DDIM, causal conv (per-tap, dx-reuse pair / vertical, fused norm, halo, RGB
 head), VAE norm / upsample, codec, barrier self-test. Shapes are the smallest that reach each
 kernel's code paths (ragged tiles included)."""
@@ -71,6 +72,7 @@ def main():
     ops.attention(q, kv[:, :512], kv[:, 512:], torch.empty_like(q), 4, 128, 500, 37, 0.088)
     ops.attention(bf(9, 32), bf(10, 32), bf(10, 32), torch.empty(9, 32, device=dev, dtype=torch.bfloat16), 2, 16,
                   9, 10, 0.25)
+    ops.attention_probs(bf(9, 32), bf(10, 32), 2, 16, 9, 10, 0.25)
     # ---------------- norm / elementwise
     x = torch.randn(300, 1536, device=dev)
     ops.norm_modulate(x, torch.empty(300, 1536, device=dev, dtype=torch.bfloat16),
