@@ -301,6 +301,15 @@ int ftb_upsample2x_f32_bf16(const float* x, int32_t T, int32_t H, int32_t W, int
 int ftb_nchw_to_nhwc_bf16(const float* x, int32_t T, int32_t C, int32_t H, int32_t W, void* y, int32_t ldy,
                           void* stream);
 
+/* Decoder mid-block attention (single head over a frame's H*W pixels, head_dim = C):
+ * p[r][j] = bf16(softmax_j(s[r][j] * scale)) for fp32 scores s [rows][ld_s] (one CTA per row,
+ * any cols), and a bf16 transpose y[c][r] = x[r][c] ([rows][ld_x] -> [cols][ld_y]) that turns V
+ * into the K-major operand of the P.V GEMM. */
+int ftb_softmax_rows_bf16(const float* s, int64_t ld_s, int32_t rows, int32_t cols, float scale, void* p,
+                          int64_t ld_p, void* stream);
+int ftb_transpose_bf16(const void* x, int64_t ld_x, int32_t rows, int32_t cols, void* y, int64_t ld_y,
+                       void* stream);
+
 /* Counter-based N(0,1)*scale fill (synthetic random-init weights at 14B shape). */
 int ftb_fill_normal_bf16(void* out, int64_t n, uint64_t seed, float scale, void* stream);
 int ftb_fill_normal_f32(float* out, int64_t n, uint64_t seed, float scale, void* stream);

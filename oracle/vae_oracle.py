@@ -65,12 +65,31 @@ class VAEOracle:
                                                                    self.P[name + ".shortcut.b"])
         return h + sc
 
+    def attn(self, name, x):
+        """Mid-block attention, per frame: one head over the frame's h*w pixels,
+        x + proj(softmax(q k^T / sqrt(C)) v) with q|k|v = rms(x) @ Wqkv^T + b (no SiLU)."""
+        T, H, W, Cc = x.shape
+        wq = self.P[name + ".qkv.w"][:, :, 0, 0, 0]
+        wp = self.P[name + ".proj.w"][:, :, 0, 0, 0]
+        out = x.copy()
+        for t in range(T):
+            u = rms(x[t], self.P[name + ".norm.g"], silu=False).reshape(-1, Cc)
+            qkv = u @ wq.T + self.P[name + ".qkv.b"]
+            q, k, v = qkv[:, :Cc], qkv[:, Cc:2 * Cc], qkv[:, 2 * Cc:]
+            s = q @ k.T / np.sqrt(Cc)
+            p = np.exp(s - s.max(1, keepdims=True))
+            p /= p.sum(1, keepdims=True)
+            out[t] += ((p @ v) @ wp.T + self.P[name + ".proj.b"]).reshape(H, W, Cc)
+        return out
+
     def decode(self, z):
         """z [T, z_dim, h, w] -> frames [T*tf, 8h, 8w, 3] (float, pre-quantisation)."""
         x = np.transpose(np.asarray(z, dtype=np.float64), (0, 2, 3, 1))
         x = self.causal("conv_in", x)
         for j in range(2):
             x = self.res("mid.%d" % j, x)
+            if j == 0 and "mid.attn.qkv.w" in self.P:
+                x = self.attn("mid.attn", x)
         for i in range(self.n_up):
             for j in range(self.nres + 1):
                 x = self.res("up.%d.res.%d" % (i, j), x)

@@ -67,6 +67,8 @@ _SIGS = {
     "ftb_cast_f32_bf16": ([vp, vp, i64, vp], i32),
     "ftb_cast_bf16_f32": ([vp, vp, i64, vp], i32),
     "ftb_patchify_composite": ([vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp, i64, vp], i32),
+    "ftb_softmax_rows_bf16": ([vp, i64, i32, i32, f32, vp, i64, vp], i32),
+    "ftb_transpose_bf16": ([vp, i64, i32, i32, vp, i64, vp], i32),
     "ftb_patchify_stacked": ([vp, i32, i32, i32, i32, i32, i32, vp, i64, vp], i32),
     "ftb_unpatch_ddim": ([vp, i64, i32, i32, i32, i32, i32, i32, i32, vp, vp, f32, f32, f32, f32, i32, vp], i32),
     "ftb_codec_decode": ([vp, vp, vp, i32, i32, vp], i32),

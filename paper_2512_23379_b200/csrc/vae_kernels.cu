@@ -189,7 +189,74 @@ __global__ void upsample2x_f32_kernel(const float4* __restrict__ x, int H, int W
     y0[orow + o + cv] = v;
   }
 }
+// Decoder mid-block attention helpers. Row softmax: one CTA per score row (fp32 in, bf16 P
+// out), three passes over the row (max, sum, write) that re-read it from L1/L2.
+__global__ void __launch_bounds__(256) softmax_rows_bf16_kernel(const float* __restrict__ s, long long ld_s, int cols,
+                                                                float scale, __nv_bfloat16* __restrict__ p,
+                                                                long long ld_p) {
+  __shared__ float red[8];
+  const float* row = s + (long long)blockIdx.x * ld_s;
+  __nv_bfloat16* out = p + (long long)blockIdx.x * ld_p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float mx = -INFINITY;
+  for (int j = threadIdx.x; j < cols; j += 256) mx = fmaxf(mx, row[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int j = threadIdx.x; j < cols; j += 256) sum += __expf((row[j] - mx) * scale);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = 1.f / tot;
+  for (int j = threadIdx.x; j < cols; j += 256) out[j] = __float2bfloat16_rn(__expf((row[j] - mx) * scale) * inv);
+}
+
+// 32 x 32 tiles through shared memory (padded against bank conflicts).
+__global__ void __launch_bounds__(256) transpose_bf16_kernel(const __nv_bfloat16* __restrict__ x, long long ld_x,
+                                                             int rows, int cols, __nv_bfloat16* __restrict__ y,
+                                                             long long ld_y) {
+  __shared__ __nv_bfloat16 tile[32][34];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8)
+    if (r0 + i < rows && c0 + tx < cols) tile[i][tx] = x[(long long)(r0 + i) * ld_x + c0 + tx];
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8)
+    if (c0 + i < cols && r0 + tx < rows) y[(long long)(c0 + i) * ld_y + r0 + tx] = tile[tx][i];
+}
+
 }  // namespace ftb
+
+extern "C" int ftb_softmax_rows_bf16(const float* s, int64_t ld_s, int32_t rows, int32_t cols, float scale, void* p,
+                                     int64_t ld_p, void* stream) {
+  if (!s || !p || rows < 0 || cols <= 0 || ld_s < cols || ld_p < cols)
+    return set_error(FTB_EINVAL, "softmax_rows: bad arguments");
+  if (rows == 0) return FTB_OK;
+  softmax_rows_bf16_kernel<<<rows, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      s, ld_s, cols, scale, static_cast<__nv_bfloat16*>(p), ld_p);
+  return check_launch("softmax_rows_bf16_kernel");
+}
+
+extern "C" int ftb_transpose_bf16(const void* x, int64_t ld_x, int32_t rows, int32_t cols, void* y, int64_t ld_y,
+                                  void* stream) {
+  if (!x || !y || rows < 0 || cols < 0 || ld_x < cols || ld_y < rows)
+    return set_error(FTB_EINVAL, "transpose: bad arguments");
+  if (rows == 0 || cols == 0) return FTB_OK;
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  transpose_bf16_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(x), ld_x, rows, cols, static_cast<__nv_bfloat16*>(y), ld_y);
+  return check_launch("transpose_bf16_kernel");
+}
 
 extern "C" int ftb_rmsnorm_silu_f32(const float* x, int64_t n_pix, int32_t C, const float* gamma, float eps,
                                     int32_t silu, void* y, void* stream) {

@@ -100,6 +100,9 @@ class LocalComm:
     def gather_rows(self, full_name, full, slab, sizes, stream=None):
         full.copy_(slab)
 
+    def all_gather_rows(self, full_name, full, slab, sizes, stream=None):
+        full.copy_(slab)
+
 
 def _on(stream):
     import contextlib
@@ -155,6 +158,20 @@ class TorchComm:
                 for r, n in enumerate(sizes):
                     full[:, r0:r0 + n].copy_(parts[r][:, :n])
                     r0 += n
+
+    def all_gather_rows(self, full_name, full, slab, sizes, stream=None):
+        """gather_rows into EVERY rank's `full` (the decoder's mid attention needs every row's keys)."""
+        mx = max(sizes)
+        T, rows = slab.shape[0], slab.shape[1]
+        with _on(stream):
+            pad = torch.zeros((T, mx) + tuple(slab.shape[2:]), dtype=slab.dtype, device=slab.device)
+            pad[:, :rows].copy_(slab)
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            self.dist.all_gather(parts, pad, group=self.group)
+            r0 = 0
+            for r, n in enumerate(sizes):
+                full[:, r0:r0 + n].copy_(parts[r][:, :n])
+                r0 += n
 
     def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
         """Spatial-split halo swap: my first row -> rank-1 (its bottom halo), my last
@@ -264,6 +281,19 @@ class ThreadComm:
             s.synchronize()
         self.hub.barrier.wait()
 
+    def all_gather_rows(self, full_name, full, slab, sizes, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        s.synchronize()
+        self.hub.slots[self.rank] = slab
+        self.hub.barrier.wait()
+        with torch.cuda.stream(s):
+            r0 = 0
+            for r, n in enumerate(sizes):
+                full[:, r0:r0 + n].copy_(self.hub.slots[r])
+                r0 += n
+        s.synchronize()
+        self.hub.barrier.wait()
+
     def neighbor_exchange(self, send_first, send_last, recv_top, recv_bot, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream()
         s.synchronize()
@@ -370,6 +400,20 @@ class PeerComm:
         self.barrier(s)
         _copy_2d_to_peer(self._addrs[full_name][0] + row0 * row_b, H * row_b, slab, rows * row_b, rows * row_b, T,
                          s)
+        self.barrier(s)
+
+    def all_gather_rows(self, full_name, full, slab, sizes, stream=None):
+        """gather_rows into every rank's symmetric `full_name`: each rank stores its slab into all
+        ranks' buffers at its row offset (one strided copy per destination), between two barriers."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        T, rows = slab.shape[0], slab.shape[1]
+        row_b = slab[0, 0].numel() * slab.element_size()
+        H = sum(sizes)
+        row0 = sum(sizes[:self.rank])
+        self.barrier(s)
+        for dst in range(self.world):
+            _copy_2d_to_peer(self._addrs[full_name][dst] + row0 * row_b, H * row_b, slab, rows * row_b, rows * row_b,
+                             T, s)
         self.barrier(s)
 
     # collective fallbacks used outside the fused path (VAE halo, tests)

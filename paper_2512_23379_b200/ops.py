@@ -289,6 +289,26 @@ def cast_f32_bf16(x, out, stream=None):
     return out
 
 
+def softmax_rows_bf16(s, out, scale, stream=None):
+    """out[r] = bf16(softmax(s[r] * scale)) over 2-d views (fp32 scores, bf16 probabilities)."""
+    _need(s, torch.float32, "s")
+    _need(out, torch.bfloat16, "out")
+    rows, cols = s.shape
+    with _Prof("vae_attn", 0.0, float(rows) * cols * 6, stream):
+        A.call("ftb_softmax_rows_bf16", A.ptr(s), _ld(s), rows, cols, float(scale), A.ptr(out), _ld(out),
+               A.stream_ptr(stream))
+    return out
+
+
+def transpose_bf16(x, out, stream=None):
+    """out[c][r] = x[r][c] over 2-d bf16 views."""
+    _need(x, torch.bfloat16, "x")
+    _need(out, torch.bfloat16, "out")
+    rows, cols = x.shape
+    A.call("ftb_transpose_bf16", A.ptr(x), _ld(x), rows, cols, A.ptr(out), _ld(out), A.stream_ptr(stream))
+    return out
+
+
 def gelu_bf16(x, out, stream=None):
     A.call("ftb_gelu_bf16", A.ptr(x), A.ptr(out), x.numel(), A.stream_ptr(stream))
     return out

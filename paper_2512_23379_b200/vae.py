@@ -4,7 +4,9 @@ Build-defined "Wan-2.1-shaped" decoder (PAPER.md:151 names the Wan2.1 VAE;
 the reference stands it in with an orthogonal codec, world.py:181-210):
 
   conv_in  CausalConv3d(z -> d0, 3x3x3)
-  mid      2 x ResBlock(d0)                     (Wan's mid attention block: see DESIGN.md)
+  mid      ResBlock(d0) -> AttentionBlock(d0) -> ResBlock(d0)
+           AttentionBlock(x) = x + proj(attn(qkv(rms(x))))  per frame, one head over the
+           frame's h*w pixels (head_dim d0, scale 1/sqrt(d0)); qkv / proj are 1x1 convs
   stage i  (num_res_blocks+1) x ResBlock(in_i -> d_{i+1});
            i < 3: [time_conv CausalConv3d(C -> 2C, 3x1x1) -> frames x2]  (temporal_upsample[i])
                    nearest 2x spatial upsample -> Conv2d 3x3 (C -> C/2)
@@ -41,6 +43,7 @@ class VAEConfig:
     dim_mult: tuple = (1, 2, 4, 4)
     num_res_blocks: int = 2
     temporal_upsample: tuple = (True, True, False)
+    mid_attention: bool = True
 
     @property
     def dims(self):
@@ -70,13 +73,17 @@ def _res(name, cin, cout):
 
 def vae_program(cfg: VAEConfig):
     """Ordered op list: (op, name, cin, cout) with op in
-    conv_in | res | time | resample | head; plus param shapes."""
+    conv_in | res | attn | time | resample | head; plus param shapes."""
     d = cfg.dims
     prog = [("conv_in", "conv_in", cfg.z_dim, d[0])]
     shapes = _conv("conv_in", cfg.z_dim, d[0], (3, 3, 3))
     for j in range(2):
         prog.append(("res", "mid.%d" % j, d[0], d[0]))
         shapes += _res("mid.%d" % j, d[0], d[0])
+        if j == 0 and cfg.mid_attention:
+            prog.append(("attn", "mid.attn", d[0], d[0]))
+            shapes += [("mid.attn.norm.g", (d[0],))] + _conv("mid.attn.qkv", d[0], 3 * d[0], (1, 1, 1))
+            shapes += _conv("mid.attn.proj", d[0], d[0], (1, 1, 1))
     n_up = len(cfg.dim_mult)
     for i in range(n_up):
         cin = d[i] // 2 if i > 0 else d[i]
@@ -245,6 +252,24 @@ class DeviceVAEDecoder:
                                  s_first=torch.empty(Tp * row, dtype=bf, device=self.dev),
                                  s_last=torch.empty(Tp * row, dtype=bf, device=self.dev))
         self.levels = levels
+        self.attn = None
+        if any(op == "attn" for op, *_ in self.prog):
+            g0 = geo[0]
+            C0, HWl, HW = g0["C"], g0["H"] * g0["W"], h * w
+            HWp = (HW + 7) // 8 * 8   # GEMM operand rows 16-byte aligned
+            npx0 = g0["T"] * HWl
+            kv_shape = (g0["T"], h, w, 2 * C0)
+            self.attn = dict(q=torch.empty(npx0, C0, dtype=bf, device=self.dev),
+                             kv=torch.empty(npx0, 2 * C0, dtype=bf, device=self.dev),
+                             vt=torch.empty(C0, HWp, dtype=bf, device=self.dev),
+                             s=torch.empty(HWl, HWp, dtype=f32, device=self.dev),
+                             p=torch.empty(HWl, HWp, dtype=bf, device=self.dev),
+                             o=torch.empty(npx0, C0, dtype=bf, device=self.dev),
+                             kv_full=None)
+            if self.split:   # every rank needs every row's keys and values
+                self.attn["kv_full"] = (self.comm.sym("vae_kv", kv_shape, bf, self.dev)
+                                        if getattr(self.comm, "peer", False)
+                                        else torch.empty(kv_shape, dtype=bf, device=self.dev))
         self.upbuf = torch.empty(ups, dtype=bf, device=self.dev)
         self.full0 = torch.empty(T * h * w * geo[0]["C"], dtype=f32, device=self.dev) if self.split else None
         last = levels[len(geo) - 1]
@@ -455,6 +480,9 @@ class DeviceVAEDecoder:
                              work_key="work2",
                              norm=(nxt, L["work"][2 * fr2:], True) if nxt is not None else None)
                 pre = (l, "work") if nxt is not None else None
+            elif op == "attn":
+                self._mid_attention(name, L, cin, s)
+                pre = None
             elif op == "time":
                 nxt = lv[l + 1]
                 self._causal(self.W[name], L, cin, lambda dst: ops.cast_f32_bf16(x[:npx * cin], dst, stream=s),
@@ -482,6 +510,43 @@ class DeviceVAEDecoder:
                 self._causal(hw_, L, cin, prod, self.out_f, 32, F32, stream=s)
                 return self.out_f[:npx * 32].view(T_, H_, W_, 32)
         raise ConfigError("VAE program has no head")
+
+    def _mid_attention(self, name, L, C, s):
+        """x += proj(softmax(q k^T / sqrt(C)) v) per frame, q/k/v = qkv(rms(x)) (1x1 convs as
+        GEMMs over the pixels): scores as an fp32 GEMM per frame, a row softmax to bf16 P, V
+        transposed into the K-major operand of the P.V GEMM, and the projection added into the
+        fp32 residual stream by the GEMM's residual epilogue. Split decode: each rank's query rows
+        attend to every rank's keys (all_gather_rows of K|V)."""
+        T_, H_, W_ = L["T"], L["H"], L["W"]
+        HWl, npx = H_ * W_, T_ * H_ * W_
+        x, a = L["x"], self.attn
+        u = L["xb"][:npx * C].view(npx, C)
+        with ops._Prof("vae_norm", 0.0, float(npx) * C * 6, s):
+            A.call("ftb_rmsnorm_silu_f32", A.ptr(x), npx, C, A.ptr(self.G[name + ".norm"]), 1e-12, 0, A.ptr(u),
+                   A.stream_ptr(s))
+        qkv = self.W[name + ".qkv"]
+        q, kv = a["q"][:npx], a["kv"][:npx]
+        ops.gemm(u, qkv.wt[:C], q, "bf16", bias=qkv.b[:C], stream=s, prof_kind="vae_attn")
+        ops.gemm(u, qkv.wt[C:3 * C], kv, "bf16", bias=qkv.b[C:3 * C], stream=s, prof_kind="vae_attn")
+        if self.split:
+            h = sum(self.sizes)
+            full = a["kv_full"]
+            self.comm.all_gather_rows("vae_kv", full, kv.view(T_, H_, W_, 2 * C), self.sizes, s)
+            kv_frames = full.view(T_, h * W_, 2 * C)
+        else:
+            kv_frames = kv.view(T_, HWl, 2 * C)
+        HW = kv_frames.shape[1]
+        vt, sc, pr = a["vt"][:, :HW], a["s"][:HWl, :HW], a["p"][:HWl, :HW]
+        scale = 1.0 / float(np.sqrt(C))
+        for t in range(T_):
+            kt, vv = kv_frames[t][:, :C], kv_frames[t][:, C:]
+            ops.transpose_bf16(vv, vt, stream=s)
+            ops.gemm(q[t * HWl:(t + 1) * HWl], kt, sc, "f32", stream=s, prof_kind="vae_attn")
+            ops.softmax_rows_bf16(sc, pr, scale, stream=s)
+            ops.gemm(pr, vt, a["o"][t * HWl:(t + 1) * HWl], "bf16", stream=s, prof_kind="vae_attn")
+        proj = self.W[name + ".proj"]
+        ops.gemm(a["o"][:npx], proj.wt, x[:npx * C].view(npx, C), "resid_f32", bias=proj.b, stream=s,
+                 prof_kind="vae_attn")
 
     def _next_norm(self, i, c):
         """Gain of the RMS norm that consumes op i's c-channel output (next resblock's norm1

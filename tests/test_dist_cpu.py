@@ -139,6 +139,10 @@ def _engine_io_worker(rank, world, port, q):
         if rank == 0:
             want = torch.arange(7, dtype=torch.float32).view(1, 7, 1, 1).expand(2, 7, 3, 2)
             assert torch.equal(full, want)
+        # every rank gets every slab (the decoder mid attention's keys / values)
+        full2 = torch.full((2, 7, 3, 2), -1.0)
+        vae.all_gather_rows("kv", full2, slab, sizes)
+        assert torch.equal(full2, torch.arange(7, dtype=torch.float32).view(1, 7, 1, 1).expand(2, 7, 3, 2))
         q.put((rank, "ok", 0))
     except Exception as e:  # noqa: BLE001
         q.put((rank, repr(e), 0))
