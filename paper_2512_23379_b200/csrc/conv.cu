@@ -55,9 +55,16 @@ struct ConvCfg {
 // acc -> + bias (+ residual) for the norm path (mode 0, full 32-column chunks)
 __device__ __forceinline__ void conv_epilogue_values(const ConvParams& p, int t, int y, int x, int gc0,
                                                      float (&v)[32]) {
-  if (p.bias) {
+  if (p.bias) {  // float4 loads: 32 scalar broadcast loads each stalled their FADD (ncu)
+    const float4* b4 = reinterpret_cast<const float4*>(p.bias + gc0);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] += __ldg(p.bias + gc0 + j);
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = __ldg(b4 + q);
+      v[4 * q] += b.x;
+      v[4 * q + 1] += b.y;
+      v[4 * q + 2] += b.z;
+      v[4 * q + 3] += b.w;
+    }
   }
   if (p.resid) {
     const long long pix = ((long long)t * p.H + y) * p.W + x;
@@ -112,9 +119,21 @@ __device__ __forceinline__ void conv_store(const ConvParams& p, int t, int y, in
 __device__ __forceinline__ void conv_epilogue(const ConvParams& p, int t, int y, int x, int gc0, float (&v)[32]) {
   const bool full = gc0 + 32 <= p.Cout;
   if (p.bias) {
+    if (full) {
+      const float4* b4 = reinterpret_cast<const float4*>(p.bias + gc0);
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (full || gc0 + j < p.Cout) v[j] += __ldg(p.bias + gc0 + j);
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(b4 + q);
+        v[4 * q] += b.x;
+        v[4 * q + 1] += b.y;
+        v[4 * q + 2] += b.z;
+        v[4 * q + 3] += b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (gc0 + j < p.Cout) v[j] += __ldg(p.bias + gc0 + j);
+    }
   }
   const long long pix = ((long long)t * p.H + y) * p.W + x;
   if (p.mode == 2) {  // RGB8 head: frames in [-1, 1] -> uint8
@@ -213,9 +232,12 @@ __device__ __forceinline__ void conv_epilogue_tile(const ConvParams& p, uint32_t
       for (int q = 0; q < BN / 8; ++q) {
         if (q * 8 >= p.Cout) break;
         float a[8];
+        const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.norm_gamma + 8 * q));
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.norm_gamma + 8 * q) + 1);
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          float f = vals[8 * q + e] * inv * __ldg(p.norm_gamma + 8 * q + e);
+          float f = vals[8 * q + e] * inv * gg[e];
           if (p.norm_silu) f = f * fmaf(0.5f, tanh_fast(0.5f * f), 0.5f);
           a[e] = f;
         }
@@ -277,9 +299,12 @@ __device__ __forceinline__ void conv_epilogue_tile(const ConvParams& p, uint32_t
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       float a[8];
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.norm_gamma + c0 + 8 * q));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.norm_gamma + c0 + 8 * q) + 1);
+      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        float f = v[8 * q + e] * inv * __ldg(p.norm_gamma + c0 + 8 * q + e);
+        float f = v[8 * q + e] * inv * gg[e];
         if (p.norm_silu) f = f * fmaf(0.5f, tanh_fast(0.5f * f), 0.5f);   // silu = f * sigmoid(f), one MUFU
         a[e] = f;
       }
