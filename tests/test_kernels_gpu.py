@@ -540,3 +540,23 @@ def test_fmha_kv_split_graph_replay(ops, cuda):
             ops.attention(q2, q2, q2, o2, 10, 128, 4000, 4000, 0.088, impl=0, workspace=ws2, stream=other)
         torch.cuda.synchronize()
         assert torch.equal(o, eager)
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (37, 5), (300, 4680), (9, 1031)])
+def test_softmax_rows_and_transpose(ops, cuda, rows, cols):
+    """The decoder mid attention's helpers: fp32 row softmax -> bf16 P (vs torch fp32, bf16
+    rounding), and the bf16 transpose (bit-exact), on ragged shapes with padded leading dims."""
+    g = torch.Generator().manual_seed(rows * 7 + cols)
+    ldp = (cols + 7) // 8 * 8 + 8
+    s = torch.empty(rows, ldp, device=cuda)[:, :cols]
+    s.copy_((torch.randn(rows, cols, generator=g) * 4).to(cuda))
+    p = torch.full((rows, ldp), 7.0, device=cuda, dtype=torch.bfloat16)
+    ops.softmax_rows_bf16(s, p[:, :cols], 0.3)
+    ref = torch.softmax(s * 0.3, dim=-1)
+    assert torch.allclose(p[:, :cols].float(), ref, atol=1e-3, rtol=8e-3)
+    assert torch.all(p[:, cols:] == 7.0)          # nothing written past the row
+    x = bf(torch.randn(rows, cols, generator=g)).to(cuda)
+    y = torch.full((cols, rows + 8), -1.0, device=cuda, dtype=torch.bfloat16)
+    ops.transpose_bf16(x, y[:, :rows])
+    assert torch.equal(y[:, :rows], x.t())
+    assert torch.all(y[:, rows:] == -1.0)
