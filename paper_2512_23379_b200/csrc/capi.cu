@@ -72,6 +72,20 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, int rank, const uint64_t* 
   return FTB_OK;
 }
 
+int make_tmap_f32(CUtensorMap* map, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
+                  const uint32_t* box) {
+  auto enc = get_encode();
+  if (!enc) return set_error(FTB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(ptr) & 15) return set_error(FTB_EINVAL, "TMA base pointer must be 16B aligned");
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(ptr),
+                   reinterpret_cast<const cuuint64_t*>(dims), reinterpret_cast<const cuuint64_t*>(strides),
+                   reinterpret_cast<const cuuint32_t*>(box), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(FTB_EINVAL, "cuTensorMapEncodeTiled (f32) failed");
+  return FTB_OK;
+}
+
 }  // namespace ftb
 
 extern "C" int ftb_version(void) { return 1; }

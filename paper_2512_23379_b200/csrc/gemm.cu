@@ -603,6 +603,11 @@ constexpr int PAIR_B_BYTES = 128 * GEMM_BK * 2;
 constexpr int PAIR_STAGE_BYTES = PAIR_A_BYTES + PAIR_B_BYTES;
 constexpr int PAIR_EPI_STAGE = 8 * 4096;  // per-epilogue-warp 32 x 32 fp32 staging tiles
 constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 1024 + 256 + PAIR_EPI_STAGE;
+// HT variant (short-K fp32 residual GEMMs): a 3-stage ring and, per epilogue warp, its whole
+// 32-row x 128-column h tile (4 TMA boxes of 32 x 32 fp32, 128-byte swizzled) in shared memory
+constexpr int PAIR_STAGES_HT = 3;
+constexpr int PAIR_HT_WARP_BYTES = 4 * 4096;
+constexpr int PAIR_SMEM_HT = PAIR_STAGES_HT * PAIR_STAGE_BYTES + 1024 + 1024 + 8 * PAIR_HT_WARP_BYTES;
 
 __device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int group_m, int& m_blk, int& n_blk) {
   const int group = group_m * num_n;
@@ -648,15 +653,16 @@ __device__ __forceinline__ void tail_wait(const unsigned* flag, unsigned want) {
   __threadfence();
 }
 
-template <int EPG, bool STAGED, bool GPF = false>
+template <int EPG, bool STAGED, bool GPF = false, bool HT = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG - 1) * 128, 1)
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmH, const GemmParams p) {
+  constexpr int NSTG = HT ? PAIR_STAGES_HT : PAIR_STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES);
-  uint64_t* empty_bar = full_bar + PAIR_STAGES;
-  uint64_t* tfull_bar = empty_bar + PAIR_STAGES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + NSTG * PAIR_STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + NSTG;
+  uint64_t* tfull_bar = empty_bar + NSTG;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
@@ -669,10 +675,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
   const int num_kb = (p.K + GEMM_BK - 1) / GEMM_BK;
   const int num_items = pair_num_items(num_tiles, n_clusters, p.tail_split);
 
+  uint64_t* h_bar = reinterpret_cast<uint64_t*>(smem + NSTG * PAIR_STAGE_BYTES + 512);  // HT: [8 warps][4 boxes]
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
-    for (int s = 0; s < PAIR_STAGES; ++s) {
+    if (HT) {
+      tma_prefetch(&tmH);
+      for (int i = 0; i < 32; ++i) mbar_init(&h_bar[i], 1);
+    }
+    for (int s = 0; s < NSTG; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
@@ -708,7 +719,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
           const int chunk = k0 / p.kc;
           tma_load_3d_pair(sa, &tmA, &full_bar[stage], k0 - chunk * p.kc, m_blk * 256 + rank * 128, chunk);
           tma_load_2d_pair(sb, &tmB, &full_bar[stage], k0, n_blk * 256 + rank * 128);
-          if (++stage == PAIR_STAGES) {
+          if (++stage == NSTG) {
             stage = 0;
             phase ^= 1;
           }
@@ -743,7 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
             mma_bf16_ss_pair_elect(tmem_d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
                              (kb != w.kb0 || k) ? 1u : 0u);
           mma_commit_pair_elect(&empty_bar[stage], 0x3);
-          if (++stage == PAIR_STAGES) {
+          if (++stage == NSTG) {
             stage = 0;
             phase ^= 1;
           }
@@ -759,6 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
     // one mainloop whichever warpgroup runs it); otherwise warpgroup eg drains accumulator eg
     constexpr bool split = EPG == 2;
     const int col0 = split ? eg * 128 : 0;
+    uint32_t h_phase = 0;  // HT: parity bit per h box barrier (edge tiles may use fewer boxes)
     int it = 0;
     for (int item = cluster; item < num_items; item += n_clusters, ++it) {
       if (EPG == 2 && !split && (it & 1) != eg) continue;
@@ -769,7 +781,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       const int gr = m_blk * 256 + rank * 128 + q * 32 + lane;
       const int width = split ? 128 : 256;
       const int gcb = n_blk * 256 + col0;
-      if (STAGED && p.prefetch && p.kind == FTB_EPI_RESID_F32 && gr < p.M && gcb < p.N) {
+      // HT: this warp's h tile (rows gr - lane .. +32, columns gcb .. +128) is fetched by TMA
+      // before the accumulator is even ready; the boxes of the previous tile must have left
+      // shared memory first (their TMA stores read it)
+      float4* hbuf = reinterpret_cast<float4*>(smem + NSTG * PAIR_STAGE_BYTES + 1024 + (warp - 4) * PAIR_HT_WARP_BYTES);
+      const int hch = HT ? max(0, min(width, p.N - gcb) >> 5) : 0;
+      if (HT && lane == 0) {
+        bulk_wait_read0();
+        for (int c = 0; c < hch; ++c) {
+          mbar_arrive_expect_tx(&h_bar[(warp - 4) * 4 + c], 4096);
+          tma_load_2d(hbuf + c * 256, &tmH, &h_bar[(warp - 4) * 4 + c], gcb + 32 * c, gr - lane);
+        }
+      }
+      if (!HT && STAGED && p.prefetch && p.kind == FTB_EPI_RESID_F32 && gr < p.M && gcb < p.N) {
         // pull this thread's row segment of h (<= 1 KB) into L2 while the tile's MMAs run, so
         // the epilogue's h loads hit L2 (DRAM latency x the few loads in flight per warp otherwise bound it)
         const float* hrow = reinterpret_cast<const float*>(p.out) + (long long)gr * p.ldc + gcb;
@@ -779,8 +803,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       mbar_wait(&tfull_bar[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256 + col0;
-      if (STAGED) {  // host guarantees RESID_F32 / F32 (no peers), N % 32 == 0, aligned rows / gate / bias
-        float4* stg = reinterpret_cast<float4*>(smem + PAIR_STAGES * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
+      if constexpr (HT) {  // host: RESID_F32, EPG 2, N % 32 == 0, no tail split
+        // thread = row (TMEM lane): its 32-column slice of the swizzled h box, h += g*(acc + bias)
+        // in place, then one TMA store per box (rows past M / columns past N are clipped)
+        const float4* gv = nullptr;
+        if (p.group_vec) {
+          const long long g = p.rows_per_group > 0 ? (min(gr, p.M - 1) + p.row_offset) / p.rows_per_group : 0;
+          gv = reinterpret_cast<const float4*>(p.group_vec + g * p.group_ld + gcb);
+        }
+        const float4* bv = p.bias ? reinterpret_cast<const float4*>(p.bias + gcb) : nullptr;
+        for (int c = 0; c < hch; ++c) {
+          uint32_t r[32];
+          tmem_ld32(trow + c * 32, r);
+          mbar_wait(&h_bar[(warp - 4) * 4 + c], (h_phase >> c) & 1u);
+          h_phase ^= 1u << c;
+          tmem_ld_wait();
+          float4* row = hbuf + c * 256 + lane * 8;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            float4 a = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]), __uint_as_float(r[4 * k + 2]),
+                                   __uint_as_float(r[4 * k + 3]));
+            if (bv) {
+              const float4 b = __ldg(bv + c * 8 + k);
+              a.x += b.x;
+              a.y += b.y;
+              a.z += b.z;
+              a.w += b.w;
+            }
+            const float4 gg = gv ? __ldg(gv + c * 8 + k) : make_float4(1.f, 1.f, 1.f, 1.f);
+            float4 h = row[k ^ (lane & 7)];
+            h.x = fmaf(gg.x, a.x, h.x);
+            h.y = fmaf(gg.y, a.y, h.y);
+            h.z = fmaf(gg.z, a.z, h.z);
+            h.w = fmaf(gg.w, a.w, h.w);
+            row[k ^ (lane & 7)] = h;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmH, hbuf + c * 256, gcb + 32 * c, gr - lane);
+            bulk_commit();
+          }
+        }
+      } else if (STAGED) {  // host guarantees RESID_F32 / F32 (no peers), N % 32 == 0, aligned rows / gate / bias
+        float4* stg = reinterpret_cast<float4*>(smem + NSTG * PAIR_STAGE_BYTES + 256 + (warp - 4) * 4096);
         // K-slice of a tail tile: this warp's rows/columns of slice part-1 must be in h first
         if (w.slot >= 0 && w.part > 0)
           tail_wait(p.tail_flags + w.slot * 16 + rank * 8 + eg * 4 + q, (unsigned)w.part);
@@ -817,25 +883,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
     }
   }
+  if (HT && warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair<512>(tmem_base);
 }
 
-template <int EPG, bool STAGED, bool GPF = false>
-static int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream) {
+template <int EPG, bool STAGED, bool GPF = false, bool HT = false>
+static int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t stream,
+                            const CUtensorMap* th = nullptr) {
+  constexpr int SMEM = HT ? PAIR_SMEM_HT : PAIR_SMEM;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_tc_pair_kernel<EPG, STAGED, GPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, PAIR_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_pair_kernel<EPG, STAGED, GPF, HT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return set_cuda_error(e, "gemm pair smem attribute");
     configured = true;
   }
   const int tiles = ((p.M + 255) / 256) * ((p.N + 255) / 256);
   const int max_pairs = sm_count() / 2;
   const int pairs = tiles < max_pairs ? tiles : max_pairs;
-  gemm_tc_pair_kernel<EPG, STAGED, GPF><<<2 * pairs, GEMM_THREADS + (EPG - 1) * 128, PAIR_SMEM, stream>>>(ta, tb, p);
+  gemm_tc_pair_kernel<EPG, STAGED, GPF, HT><<<2 * pairs, GEMM_THREADS + (EPG - 1) * 128, SMEM, stream>>>(
+      ta, tb, th ? *th : tb, p);
   return check_launch("gemm_tc_pair_kernel");
 }
 
@@ -895,9 +965,10 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
   }
   // kernel selection of this call (ftb_epilogue.variant; 0 = product defaults)
   const int variant = epi->variant;
-  if (variant < 0 || (variant & 3) == 3 || variant > 31)
+  if (variant < 0 || (variant & 3) == 3 || variant > 63)
     return set_error(FTB_EINVAL, "gemm: variant must be 0/1/2 (auto / single CTA / CTA pair) + 4 (row-per-thread "
-                                 "residual epilogue) + 8 (no h prefetch) + 16 (one epilogue warpgroup at long K)");
+                                 "residual epilogue) + 8 (no h prefetch) + 16 (one epilogue warpgroup at long K) + 32 "
+                                 "(no TMA-staged short-K residual epilogue)");
   if (epi->raster_group < 0) return set_error(FTB_EINVAL, "gemm: raster_group must be >= 0");
   GemmParams p{};
   p.n_peers = epi->n_peers;
@@ -992,6 +1063,19 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
         p.tail_flags = epi->tail_counters;
         p.tail_split = sp;
       }
+    }
+    if (staged && K <= 1536 && epg2 && p.kind == FTB_EPI_RESID_F32 && p.tail_split <= 1 && !(variant & 32)) {
+      // short-K fp32 residual GEMMs: h tiles in and out by TMA (the per-thread h loads of the
+      // staged epilogue bound these shapes at ~2 TB/s of h traffic). Measured vs the staged
+      // epilogue (10530 rows): N 1536 K 480 -39 %, K 1536 -19 %; N 5120 K 1024 -16 %; at K >= 1600
+      // the 3-stage mainloop ring costs more than the epilogue saves (+2 %)
+      CUtensorMap th;
+      uint64_t hd[2] = {(uint64_t)N, (uint64_t)M};
+      uint64_t hs[1] = {(uint64_t)epi->ldc * 4};
+      uint32_t hbox[2] = {32, 32};
+      int rc = make_tmap_f32(&th, epi->out, 2, hd, hs, hbox);
+      if (rc) return rc;
+      return launch_gemm_pair<2, true, false, true>(ta, tb, p, s, &th);
     }
     if (staged && K <= 2048 && epg2) return launch_gemm_pair<2, true, true>(ta, tb, p, s);
     if (staged) return epg2 ? launch_gemm_pair<2, true>(ta, tb, p, s) : launch_gemm_pair<1, true>(ta, tb, p, s);

@@ -560,3 +560,26 @@ def test_softmax_rows_and_transpose(ops, cuda, rows, cols):
     ops.transpose_bf16(x, y[:, :rows])
     assert torch.equal(y[:, :rows], x.t())
     assert torch.all(y[:, rows:] == -1.0)
+
+
+@pytest.mark.parametrize("M,N,K", [(10530, 1536, 480), (300, 1536, 1536), (257, 2592, 544), (1000, 5120, 1024)])
+def test_gemm_resid_tma_staged_epilogue(ops, cuda, M, N, K):
+    """Short-K fp32 residual GEMMs take the TMA-staged h epilogue (whole h boxes in and out by
+    TMA): bit-identical to the per-thread staged epilogue (variant bit 32), within fp32
+    rounding of an fp32 reference, and nothing written outside the logical rows / columns."""
+    g = torch.Generator().manual_seed(M + N + K)
+    a = bf(torch.randn(M, K, generator=g)).to(cuda)
+    w = bf(torch.randn(N, K, generator=g) / K ** 0.5).to(cuda)
+    gate = torch.randn(10, N, generator=g).to(cuda)
+    bias = torch.randn(N, generator=g).to(cuda)
+    pad = 8
+    base = torch.randn(M + 64, N + pad, generator=g).to(cuda)
+    outs = []
+    for var in (0, 32):
+        buf = base.clone()
+        ops.gemm(a, w, buf[:M, :N], "resid_f32", group_vec=gate, rows_per_group=1170, bias=bias, variant=var)
+        outs.append(buf)
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0][:, N:], base[:, N:]) and torch.equal(outs[0][M:], base[M:])
+    ref = base[:M, :N] + gate.repeat_interleave(1170, 0)[:M] * (a.float() @ w.float().t() + bias)
+    assert ((outs[0][:M, :N] - ref).norm() / (ref - base[:M, :N]).norm()).item() < 1e-5
