@@ -101,7 +101,7 @@ typedef struct ftb_epilogue {
    * bits 0-1: 0 auto (CTA pair when M, N >= 256), 1 single CTA, 2 CTA pair; +4 row-per-thread
    * residual epilogue of the pair kernel (instead of the smem-staged one); +8 no L2 prefetch of
    * the residual rows; +16 long-K residual GEMMs on one epilogue warpgroup; +32 no TMA-staged h
-   * tiles for short-K (<= 1536) residual GEMMs. */
+   * tiles for short-K (<= 2048) residual GEMMs. */
   int32_t variant;
   /* CTA-pair raster group (256-row m-blocks sharing one B sweep in L2): 0 auto (A panels of the
    * group ~40 MB, at least 8). */

@@ -603,11 +603,13 @@ constexpr int PAIR_B_BYTES = 128 * GEMM_BK * 2;
 constexpr int PAIR_STAGE_BYTES = PAIR_A_BYTES + PAIR_B_BYTES;
 constexpr int PAIR_EPI_STAGE = 8 * 4096;  // per-epilogue-warp 32 x 32 fp32 staging tiles
 constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 1024 + 256 + PAIR_EPI_STAGE;
-// HT variant (short-K fp32 residual GEMMs): a 3-stage ring and, per epilogue warp, its whole
-// 32-row x 128-column h tile (4 TMA boxes of 32 x 32 fp32, 128-byte swizzled) in shared memory
-constexpr int PAIR_STAGES_HT = 3;
-constexpr int PAIR_HT_WARP_BYTES = 4 * 4096;
-constexpr int PAIR_SMEM_HT = PAIR_STAGES_HT * PAIR_STAGE_BYTES + 1024 + 1024 + 8 * PAIR_HT_WARP_BYTES;
+// HT variant (short-K fp32 residual GEMMs): a 4-stage ring and, per epilogue warp, three of the
+// four 32 x 32 fp32 boxes (128-byte swizzled) of its 32-row x 128-column h tile in shared memory;
+// the fourth box reuses the first buffer once that box's TMA store has read it. (All four boxes
+// with a 3-stage ring measured 2-9 % slower at K >= 1024.)
+constexpr int PAIR_STAGES_HT = 4;
+constexpr int PAIR_BOXES_HT = 3;
+constexpr int PAIR_SMEM_HT = PAIR_STAGES_HT * PAIR_STAGE_BYTES + 1024 + 1024 + 8 * PAIR_BOXES_HT * 4096;
 
 __device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int group_m, int& m_blk, int& n_blk) {
   const int group = group_m * num_n;
@@ -658,6 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
     gemm_tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmH, const GemmParams p) {
   constexpr int NSTG = HT ? PAIR_STAGES_HT : PAIR_STAGES;
+  constexpr int HB = HT ? PAIR_BOXES_HT : 1;   // h boxes per epilogue warp
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + NSTG * PAIR_STAGE_BYTES);
@@ -784,11 +787,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
       // HT: this warp's h tile (rows gr - lane .. +32, columns gcb .. +128) is fetched by TMA
       // before the accumulator is even ready; the boxes of the previous tile must have left
       // shared memory first (their TMA stores read it)
-      float4* hbuf = reinterpret_cast<float4*>(smem + NSTG * PAIR_STAGE_BYTES + 1024 + (warp - 4) * PAIR_HT_WARP_BYTES);
+      float4* hbuf = reinterpret_cast<float4*>(smem + NSTG * PAIR_STAGE_BYTES + 1024 + (warp - 4) * HB * 4096);
       const int hch = HT ? max(0, min(width, p.N - gcb) >> 5) : 0;
       if (HT && lane == 0) {
         bulk_wait_read0();
-        for (int c = 0; c < hch; ++c) {
+        for (int c = 0; c < hch && c < HB; ++c) {
           mbar_arrive_expect_tx(&h_bar[(warp - 4) * 4 + c], 4096);
           tma_load_2d(hbuf + c * 256, &tmH, &h_bar[(warp - 4) * 4 + c], gcb + 32 * c, gr - lane);
         }
@@ -813,12 +816,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
         }
         const float4* bv = p.bias ? reinterpret_cast<const float4*>(p.bias + gcb) : nullptr;
         for (int c = 0; c < hch; ++c) {
+          const int b = c % HB;
           uint32_t r[32];
           tmem_ld32(trow + c * 32, r);
-          mbar_wait(&h_bar[(warp - 4) * 4 + c], (h_phase >> c) & 1u);
-          h_phase ^= 1u << c;
+          mbar_wait(&h_bar[(warp - 4) * 4 + b], (h_phase >> b) & 1u);
+          h_phase ^= 1u << b;
           tmem_ld_wait();
-          float4* row = hbuf + c * 256 + lane * 8;
+          float4* row = hbuf + b * 256 + lane * 8;
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             float4 a = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]), __uint_as_float(r[4 * k + 2]),
@@ -841,8 +845,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS + (EPG 
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmH, hbuf + c * 256, gcb + 32 * c, gr - lane);
+            tma_store_2d(&tmH, hbuf + b * 256, gcb + 32 * c, gr - lane);
             bulk_commit();
+            if (c + HB < hch) {  // box b takes chunk c + HB once its store has read it
+              bulk_wait_read0();
+              mbar_arrive_expect_tx(&h_bar[(warp - 4) * 4 + b], 4096);
+              tma_load_2d(hbuf + b * 256, &tmH, &h_bar[(warp - 4) * 4 + b], gcb + 32 * (c + HB), gr - lane);
+            }
           }
         }
       } else if (STAGED) {  // host guarantees RESID_F32 / F32 (no peers), N % 32 == 0, aligned rows / gate / bias
@@ -1064,11 +1073,11 @@ extern "C" int ftb_gemm_bf16(const void* A, int64_t lda, int32_t a_chunks, int64
         p.tail_split = sp;
       }
     }
-    if (staged && K <= 1536 && epg2 && p.kind == FTB_EPI_RESID_F32 && p.tail_split <= 1 && !(variant & 32)) {
+    if (staged && K <= 2048 && epg2 && p.kind == FTB_EPI_RESID_F32 && p.tail_split <= 1 && !(variant & 32)) {
       // short-K fp32 residual GEMMs: h tiles in and out by TMA (the per-thread h loads of the
       // staged epilogue bound these shapes at ~2 TB/s of h traffic). Measured vs the staged
-      // epilogue (10530 rows): N 1536 K 480 -39 %, K 1536 -19 %; N 5120 K 1024 -16 %; at K >= 1600
-      // the 3-stage mainloop ring costs more than the epilogue saves (+2 %)
+      // epilogue (10530 rows): N 1536 K 480 -37 %, K 1536 -24 %, K 2048 -8 %; N 2592 K 1600 -11 %;
+      // N 5120 K 1024 -25 %, K 1600 -9 %, K 2560 -1 %, K 3072 +9 % (the 4-stage ring)
       CUtensorMap th;
       uint64_t hd[2] = {(uint64_t)N, (uint64_t)M};
       uint64_t hs[1] = {(uint64_t)epi->ldc * 4};
