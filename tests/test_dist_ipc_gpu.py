@@ -64,9 +64,19 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
+def _reference(outdir):
+    np.save(os.path.join(outdir, "ref.npy"), _step(None))
+
+
 def test_ipc_peer_transport_two_processes(cuda, tmp_path):
-    want = _step(None)
+    # every CUDA step runs in a spawned child (the single-process reference too): the pytest
+    # process itself stays out of this test's multi-process CUDA work
     ctx = mp.get_context("spawn")
+    ref = ctx.Process(target=_reference, args=(str(tmp_path),))
+    ref.start()
+    ref.join(timeout=600)
+    assert ref.exitcode == 0
+    want = np.load(tmp_path / "ref.npy")
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, str(tmp_path))) for r in range(2)]
     for p in procs:
