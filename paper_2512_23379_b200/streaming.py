@@ -141,7 +141,10 @@ class DeviceStreamer:
         from . import _capi
         n0 = _capi.LAUNCHES[0]
         try:
-            with torch.cuda.graph(g, stream=s):
+            # thread_local: the engine's ingest / decode threads keep issuing their own CUDA work
+            # (H2D staging, decode) while the denoise thread captures; only this thread's
+            # capture-unsafe calls are errors
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
                 self._device_chunk()
         finally:
             self.d.stream = keep
