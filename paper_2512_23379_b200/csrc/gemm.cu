@@ -603,12 +603,13 @@ constexpr int PAIR_B_BYTES = 128 * GEMM_BK * 2;
 constexpr int PAIR_STAGE_BYTES = PAIR_A_BYTES + PAIR_B_BYTES;
 constexpr int PAIR_EPI_STAGE = 8 * 4096;  // per-epilogue-warp 32 x 32 fp32 staging tiles
 constexpr int PAIR_SMEM = PAIR_STAGES * PAIR_STAGE_BYTES + 1024 + 256 + PAIR_EPI_STAGE;
-// HT variant (short-K fp32 residual GEMMs): a 4-stage ring and, per epilogue warp, three of the
+// HT variant (short-K fp32 residual GEMMs): a 5-stage ring and, per epilogue warp, two of the
 // four 32 x 32 fp32 boxes (128-byte swizzled) of its 32-row x 128-column h tile in shared memory;
-// the fourth box reuses the first buffer once that box's TMA store has read it. (All four boxes
-// with a 3-stage ring measured 2-9 % slower at K >= 1024.)
-constexpr int PAIR_STAGES_HT = 4;
-constexpr int PAIR_BOXES_HT = 3;
+// box c + 2 reuses box c's buffer once that box's TMA store has read it. Ring depth beats box
+// count: 5 stages / 2 boxes vs 4 / 3 at 10530 rows: N 5120 K 1600 158.6 vs 170.3 us, N 1536
+// K 1536 70.4 vs 83.2, K 480 56.2 vs 60.0 (3 stages / 4 boxes lost 2-9 % at K >= 1024).
+constexpr int PAIR_STAGES_HT = 5;
+constexpr int PAIR_BOXES_HT = 2;
 constexpr int PAIR_SMEM_HT = PAIR_STAGES_HT * PAIR_STAGE_BYTES + 1024 + 1024 + 8 * PAIR_BOXES_HT * 4096;
 
 __device__ __forceinline__ void pair_raster(int tile, int num_m, int num_n, int group_m, int& m_blk, int& n_blk) {
